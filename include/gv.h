@@ -1,0 +1,295 @@
+/*
+ * gv.h — C ABI of the B200-native parallel-negative-sampling trainer
+ * (GraphVite, Zhu et al., arXiv 1903.00757).
+ *
+ * Citation keys: P:n = PAPER.md line n (LaTeX source of the paper),
+ * S:n = SPEC.md line n, SURVEY §x = /root/repo/SURVEY.md section.
+ *
+ * What the library computes (the "hot path"):
+ *   Per pool of positive edge samples (u,v) (Alg. 2):
+ *     a2  stage the pool in device memory (gv_push_sample_pool)
+ *     a3  relabel + histogram into the n x n partition grid              Alg. 3
+ *     a4  scan -> block offsets
+ *     a5  stable scatter into blocks (i,j), local ids
+ *     a6  block-row exchange between ranks (D>1)                         Alg. 3
+ *     a7  block-SGD on block (i,(i+t) mod n) per offset step t           Alg. 3 P:245-252,
+ *         skip-gram negative-sampling objective, Hogwild
+ *     a8  context rotation between ranks (D>1)                           Alg. 3
+ *   gv_train_episode runs a3..a8 for one pushed pool.
+ *
+ * Conventions (all functions):
+ *   - Every call returns gv_status; no exception or abort crosses the ABI.
+ *     On error the context keeps the state it had before the call unless
+ *     stated otherwise, and gv_last_error() returns a one-line message.
+ *   - All pointers are HOST pointers unless the parameter name ends in _dev.
+ *   - The caller owns every input array; the library copies what it needs
+ *     before returning (the caller may free/reuse the buffer on return).
+ *   - Output arrays are caller-allocated host buffers.
+ *   - Embedding matrices cross the ABI as row-major float32 [num_nodes][dim]
+ *     indexed by ORIGINAL node id (the library un-relabels them).
+ *   - One caller thread per context, except that gv_push_sample_pool may run
+ *     on a producer thread concurrently with gv_train_episode on the consumer
+ *     thread (the collaboration strategy).
+ *
+ * Call order: gv_create -> gv_load_edges -> (gv_push_sample_pool+ ->
+ *             gv_train_episode)* -> gv_get_* -> gv_destroy.
+ * Anything else returns GV_ERR_STATE.
+ *
+ * Ranks ("devices" in the paper's Alg. 3): the n_partitions x n_partitions
+ * grid is trained by D ranks. Rank d owns vertex partitions
+ * [d*m, (d+1)*m), m = n_partitions / D, and at offset step t holds the
+ * context partitions (d*m + t + g) mod n, g = 0..m-1 (a sliding window that
+ * moves by one partition per step). D ranks are either
+ *   - D separate processes (one per GPU, world_size = D, NCCL transport), or
+ *   - D virtual ranks inside one process on one GPU (virtual_ranks = D,
+ *     device-copy transport) — the same schedule, used to test the
+ *     multi-rank path on a single device.
+ */
+#ifndef GV_H_
+#define GV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GV_ABI_VERSION 1
+
+typedef struct gv_ctx gv_ctx; /* opaque; owned by the library */
+
+typedef enum {
+  GV_OK = 0,
+  GV_ERR_INVALID_ARG = 1, /* bad size/shape/parameter                          */
+  GV_ERR_STATE = 2,       /* call out of order                                 */
+  GV_ERR_OUT_OF_RANGE = 3,/* a node id >= num_nodes in a pool or edge list     */
+  GV_ERR_EMPTY = 4,       /* empty graph / partition with zero noise mass      */
+  GV_ERR_CAPACITY = 5,    /* block > 2^32-1 samples, pool > max_pool_samples   */
+  GV_ERR_NOMEM = 6,       /* host or device allocation failed                  */
+  GV_ERR_CUDA = 7,        /* CUDA runtime failure (text in gv_last_error)      */
+  GV_ERR_COMM = 8         /* NCCL failure                                      */
+} gv_status;
+
+/* Learning-rate schedule ("initial learning rate of 0.025 and the
+ * linear learning rate decay mechanism in LINE"). Before offset step t:
+ *   lr_t = (float)(lr0 * max(1 - S_before/total_samples, floor_ratio))
+ * where S_before counts every sample (all ranks) trained in earlier offset
+ * steps of this and earlier pools. Constant within a step. GV_LR_CONSTANT or
+ * total_samples == 0 gives lr_t = lr0. SURVEY §8(c) step 8. */
+typedef enum { GV_LR_CONSTANT = 0, GV_LR_LINEAR = 1 } gv_lr_kind;
+typedef struct {
+  gv_lr_kind kind;
+  double floor_ratio;     /* default 1e-4                    */
+  uint64_t total_samples; /* epochs * |E|                    */
+} gv_lr_schedule;
+
+typedef struct {
+  uint64_t seed;          /* key of the negative-sample Philox stream            */
+  uint64_t init_seed;     /* key of the embedding-init Philox stream             */
+  float neg_weight;       /* gradient scale of negatives, default 5       */
+  int device;             /* CUDA ordinal used by this process (default 0)        */
+  int rank;               /* process rank (default 0)                             */
+  int world_size;         /* number of processes, one per GPU (default 1)         */
+  int virtual_ranks;      /* ranks simulated in this process (default 1);
+                             world_size > 1 requires virtual_ranks == 1           */
+  int ordered;            /* 1 = ordered verification mode: one warp per block,
+                             samples in block order (bit-comparable schedule)     */
+  int compute_loss;       /* 1 = accumulate the per-sample loss (default 1)       */
+  int host_threads;       /* threads for host graph preparation (0 = all cores)   */
+  uint64_t max_pool_samples; /* per rank; 0 = grow on demand                      */
+} gv_options;
+
+/* Per-pool statistics of THIS process (all its virtual ranks). Times are
+ * CUDA-event durations on the rank's streams, in milliseconds. */
+typedef struct {
+  uint64_t pool_index;    /* e: the pool counter used in the Philox counter      */
+  uint64_t samples;       /* samples trained by this process in this pool         */
+  uint64_t samples_global;/* samples in this pool over all ranks                  */
+  uint32_t n_steps;       /* offset steps run (= n_partitions)                    */
+  float lr_first, lr_last;
+  double loss_sum;        /* sum over samples of -log s(x+) - sum_k log s(-x_k)
+                             (0 if compute_loss == 0)                             */
+  double ms_bucket;       /* a3..a5 (max over virtual ranks)                      */
+  double ms_exchange;     /* a6                                                   */
+  double ms_sgd;          /* a7 kernel time summed over steps (max over v-ranks)  */
+  double ms_rotate;       /* a8 transfers not hidden behind a7                    */
+  double ms_total;        /* first bucketing launch -> last kernel/transfer       */
+  uint32_t sgd_launches;  /* number of block-SGD kernel launches                  */
+  uint32_t kernel_launches; /* all kernels launched by this call                  */
+} gv_episode_stats;
+
+/* ---------------------------------------------------------------------- */
+
+/* Fills *opt with defaults: seed 5, init_seed 4 (SURVEY §8(d) seeds),
+ * neg_weight 5, device 0, rank 0, world_size 1, virtual_ranks 1, ordered 0,
+ * compute_loss 1, host_threads 0, max_pool_samples 0. */
+void gv_default_options(gv_options* opt);
+
+/* Create a trainer for |V| = num_nodes nodes with dim-dimensional vertex and
+ * context embeddings, an n_partitions x n_partitions grid,
+ * num_negatives negatives per positive sample, initial learning rate
+ * lr0 and schedule alpha (nullable -> linear decay with floor 1e-4 and
+ * total_samples 0, i.e. constant). opt nullable -> gv_default_options.
+ * Allocates nothing on the device yet.
+ * Errors: GV_ERR_INVALID_ARG if num_nodes == 0, dim == 0, dim % 4 != 0,
+ *   dim > 512, num_negatives == 0 or > 8, n_partitions == 0, n_partitions >
+ *   num_nodes, n_partitions > 64, n_partitions % (world_size*virtual_ranks)
+ *   != 0, lr0 < 0, or bad rank/world_size/virtual_ranks; GV_ERR_CUDA if the
+ *   device cannot be selected. *out is set only on GV_OK. */
+gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
+                    uint32_t num_negatives, float lr0,
+                    const gv_lr_schedule* alpha, const gv_options* opt,
+                    gv_ctx** out);
+
+/* Multi-process only (world_size > 1): rank 0 calls gv_comm_unique_id, the
+ * caller broadcasts the 128 bytes to every rank (e.g. torch.distributed),
+ * then every rank calls gv_comm_init before gv_load_edges. */
+gv_status gv_comm_unique_id(uint8_t id_out[128]);
+gv_status gv_comm_init(gv_ctx* ctx, const uint8_t id[128]);
+
+/* Load the graph G=(V,E) as an edge list src[k]-dst[k] with optional
+ * weights (nullable -> 1). The graph is treated as undirected:
+ * self-loops are dropped, both directions are stored, duplicate edges have
+ * their weights summed (in input order, in double). Weighted degree
+ * deg[v] = sum of incident merged weights, summed in ascending neighbour id.
+ * Then: degree-guided zig-zag partition and relabel (P:392,
+ * fig:zig-zag_partition), one integer alias table per
+ * context partition over deg^0.75,
+ * per-node neighbour and departure alias tables for gv_augment, device
+ * allocation of the rank's shards and Philox initialisation of the
+ * embeddings (vertex U[-0.5/d, 0.5/d), context 0).
+ * Every rank passes the SAME full edge list.
+ * Errors: GV_ERR_OUT_OF_RANGE (id >= num_nodes), GV_ERR_INVALID_ARG
+ *   (negative or non-finite weight), GV_ERR_EMPTY (no edge left, or a
+ *   partition whose deg^0.75 mass is 0), GV_ERR_CAPACITY (a partition larger
+ *   than the packed-id range), GV_ERR_NOMEM, GV_ERR_CUDA, GV_ERR_STATE
+ *   (called twice). */
+gv_status gv_load_edges(gv_ctx* ctx, const uint32_t* src, const uint32_t* dst,
+                        const float* weight, uint64_t num_edges);
+
+/* Append count edge samples (pairs[2k], pairs[2k+1]) = (u, v), ORIGINAL ids,
+ * to the pending pool (Alg. 2's concatenated pool). Copies host ->
+ * device before returning (batched transfer P:284, on a copy stream).
+ * With virtual_ranks = D the whole pool is pushed and rank r trains on the
+ * contiguous segment [r*P/D, (r+1)*P/D); with world_size = D each process
+ * pushes its own segment. Ids are range-checked on the device at
+ * gv_train_episode (GV_ERR_OUT_OF_RANGE, no update applied).
+ * u == v is allowed. Errors: GV_ERR_STATE (before gv_load_edges),
+ * GV_ERR_CAPACITY (pending pool would exceed max_pool_samples), GV_ERR_CUDA. */
+gv_status gv_push_sample_pool(gv_ctx* ctx, const uint32_t* pairs, uint64_t count);
+
+/* Same as gv_push_sample_pool but pairs_dev is a device pointer on this
+ * process's device (device-to-device copy). */
+gv_status gv_push_sample_pool_device(gv_ctx* ctx, const uint32_t* pairs_dev,
+                                     uint64_t count);
+
+/* Re-arm the last trained pool as the pending pool without any copy
+ * (benchmarks replay one resident pool; the pool counter still advances so
+ * negatives differ). GV_ERR_STATE if no pool was trained or one is pending. */
+gv_status gv_replay_pool(gv_ctx* ctx);
+
+/* Train the pending pool: bucket (a3-a5), exchange (a6), then for offset
+ * steps t = 0..n-1 train block (i, (i+t) mod n) for every vertex partition i
+ * owned by each rank, rotating context partitions between steps (a7, a8;
+ * Alg. 3). Blocks of one step share no rows, so ranks need
+ * no synchronisation within a step. Returns after the device work has been
+ * ENQUEUED and the block sizes are known; call gv_synchronize (or read
+ * stats, which synchronises when out != NULL) to wait. An empty pending pool
+ * is a no-op that still advances nothing and returns GV_ERR_EMPTY.
+ * Errors: GV_ERR_STATE, GV_ERR_EMPTY, GV_ERR_OUT_OF_RANGE (pool contains an
+ * id >= num_nodes; detected before any SGD launch, embeddings unchanged),
+ * GV_ERR_CAPACITY (a block > 2^32-1 samples), GV_ERR_CUDA, GV_ERR_COMM. */
+gv_status gv_train_episode(gv_ctx* ctx, gv_episode_stats* out);
+
+/* Wait for all device work of the context. */
+gv_status gv_synchronize(gv_ctx* ctx);
+
+/* Copy embeddings to out (num_nodes*dim floats, ORIGINAL id order).
+ * In multi-process mode only rows owned by this rank (vertex: its vertex
+ * partitions; context: its canonical window [d*m,(d+1)*m)) are written.
+ * Errors: GV_ERR_INVALID_ARG (out_len != num_nodes*dim), GV_ERR_STATE. */
+gv_status gv_get_vertex_embeddings(gv_ctx* ctx, float* out, uint64_t out_len);
+gv_status gv_get_context_embeddings(gv_ctx* ctx, float* out, uint64_t out_len);
+/* Overwrite embeddings (tests, checkpoint resume); same layout and rules. */
+gv_status gv_set_vertex_embeddings(gv_ctx* ctx, const float* in, uint64_t in_len);
+gv_status gv_set_context_embeddings(gv_ctx* ctx, const float* in, uint64_t in_len);
+
+/* Library-owned compute stream of virtual rank r (cudaStream_t as uintptr),
+ * so a caller can time device work with its own events on that stream. */
+gv_status gv_get_stream(gv_ctx* ctx, int vrank, uintptr_t* stream_out);
+
+/* Host online augmentation (Alg. 2): `threads` private segments,
+ * each filled by random walks of walk_len edges from departures drawn
+ * proportional to degree, pairs (w_a, w_b) with 0 < b-a <= s and w_a != w_b,
+ * pseudo-shuffled into s sub-blocks, segments concatenated.
+ * Writes exactly `count` pairs (ORIGINAL ids) to out_pairs[2*count].
+ * Deterministic given (seed, threads): walks draw from a Philox stream with
+ * counter (walk, step, thread, 0x57414C4B) and key = seed (SURVEY §8(c),
+ * reading R-AUG in DESIGN.md).
+ * Errors: GV_ERR_STATE (no graph), GV_ERR_INVALID_ARG (walk_len == 0,
+ * s == 0, s > walk_len, threads == 0). */
+gv_status gv_augment(gv_ctx* ctx, uint32_t walk_len, uint32_t s,
+                     uint32_t threads, uint64_t count, uint64_t seed,
+                     uint32_t* out_pairs);
+
+/* Collaboration strategy: two pinned host pools; producer
+ * threads fill one with gv_augment while the trainer pushes and trains the
+ * other; pools swap when both sides are done. Trains ceil(total/pool) pools.
+ * collaborate = 0 runs fill-then-train sequentially (ablation,
+ * tab:main_components). Single-process only. Wall-clock results go to
+ * *report (nullable). */
+typedef struct {
+  uint32_t walk_len;      /* 40               */
+  uint32_t s;             /* augmentation distance    */
+  uint32_t threads;       /* sampler threads          */
+  uint64_t pool_samples;  /* samples per pool         */
+  uint64_t seed;          /* augmentation Philox key (pool k uses seed + k) */
+  int collaborate;        /* 1 = double-buffered      */
+} gv_augment_cfg;
+typedef struct {
+  uint64_t pools, samples;
+  double wall_ms, produce_ms, train_wait_ms, producer_wait_ms;
+  double loss_sum;
+} gv_run_report;
+gv_status gv_run(gv_ctx* ctx, const gv_augment_cfg* cfg, uint64_t total_samples,
+                 gv_run_report* report);
+
+/* ---- introspection / verification (tests) -------------------------------- */
+
+/* Zig-zag relabel map: perm[orig] = new id; part_off[n_partitions+1]. */
+gv_status gv_get_partition(gv_ctx* ctx, uint32_t* perm, uint64_t* part_off);
+/* Integer alias table of context partition p over its members in local order
+ * (prob[k], alias[k]; k < partition size), and the departure table over all
+ * nodes in original order (p == UINT32_MAX). */
+gv_status gv_get_alias(gv_ctx* ctx, uint32_t p, uint32_t* prob, uint32_t* alias,
+                       uint64_t cap);
+/* Bucket the pending pool without training (a3-a6) so that the blocks and
+ * negatives can be inspected; the next gv_train_episode trains it. */
+gv_status gv_prepare_episode(gv_ctx* ctx);
+/* Global block layout of the prepared pool: pairs_out[2*P] local ids in
+ * canonical (i,j) row-major block order; block_off[n*n+1]. Multi-process:
+ * only this rank's block rows are filled. */
+gv_status gv_debug_get_buckets(gv_ctx* ctx, uint32_t* pairs_out, uint64_t cap,
+                               uint64_t* block_off);
+/* Negatives of block (i,j) of the prepared pool: out[q*K + k] = local id in
+ * context partition j, as the SGD kernel draws them (device Philox). */
+gv_status gv_debug_get_negatives(gv_ctx* ctx, uint32_t i, uint32_t j,
+                                 uint32_t* out, uint64_t cap);
+/* One ordered update per sample with caller-given negatives (hand-derived
+ * tests): u, v, negs in ORIGINAL ids, negs[q*K + k]. */
+gv_status gv_train_explicit(gv_ctx* ctx, const uint32_t* u, const uint32_t* v,
+                            const uint32_t* negs, uint64_t count, float lr);
+
+/* Bytes of device memory allocated by this context (all virtual ranks). */
+gv_status gv_device_bytes(gv_ctx* ctx, uint64_t* bytes);
+
+const char* gv_last_error(const gv_ctx* ctx); /* ctx may be NULL (global) */
+const char* gv_status_string(gv_status s);
+int gv_abi_version(void);
+void gv_destroy(gv_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GV_H_ */
