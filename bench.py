@@ -1,0 +1,301 @@
+#!/usr/bin/env python
+"""Benchmark of the GraphVite hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one pass of the whole hot path over one pool of edge samples:
+bucketing (a3-a5), block-row exchange (a6, N > 1), the n offset steps of
+block-SGD (a7) and the context rotations (a8) — gv_train_episode on a pool
+already resident in HBM (gv_replay_pool), so `value` is device throughput.
+`e2e` runs the same steps through the C ABI from pinned HOST memory
+(gv_push_sample_pool every step, stats read back every step).
+
+N = 1: configs[1] — Youtube-shaped synthetic graph, 1,138,499 nodes /
+4,945,382 edges (tab:datasets P:272), d = 128, K = 1, walks of 40 edges,
+augmentation distance s = 5, pool = episode size 2e8, n = 1.
+N > 1 (torchrun): configs[2] — the same graph on an N x N grid, one rank per
+GPU, 2e8 samples per rank per pool (weak scaling), NCCL between ranks.
+Inputs (pool 1.6 GB per rank + 2 x 583 MB of embeddings) are larger than the
+126 MB L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "edge samples/sec (device-timed, max over ranks) at 1/2/4/8 B200; HBM GB/s vs peak"
+CFG = dict(nv=1_138_499, ne=4_945_382, gamma=2.1, wmax=3e4, d=128, K=1, s=5, walk=40,
+           pool=200_000_000)
+BYTES_PER_SAMPLE = lambda d, K: 2 * (2 + K) * d * 4  # noqa: E731  (BASELINE.json north_star)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pool", type=int, default=CFG["pool"], help="samples per rank per pool")
+    ap.add_argument("--threads", type=int, default=0, help="sampler threads (0 = all cores)")
+    ap.add_argument("--cpu-sample", type=int, default=4_000_000,
+                    help="samples of the bounded oracle run (cpu_baseline)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ordered", action="store_true", help="ordered verification kernel (slow)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def make_graph():
+    import synth
+    return synth.chung_lu(CFG["nv"], CFG["ne"], gamma=CFG["gamma"], wmax=CFG["wmax"], seed=1)
+
+
+def cpu_baseline(src, dst, sample, threads, seed):
+    """The oracle as it stands (serial C, 1 core) on a bounded sample of the
+    same workload: the first `sample` pairs of a pool augmented the same way."""
+    from oracle import oracle as O
+    t = O.Trainer(CFG["nv"], CFG["d"], 1, K=CFG["K"], lr0=0.025, lr_kind=1,
+                  total_samples=sample)
+    t.load_edges(src, dst)
+    sampler = O.Sampler(O.Graph(CFG["nv"], src, dst))
+    pool = sampler.augment(CFG["walk"], CFG["s"], threads, sample, seed)
+    t0 = time.perf_counter()
+    t.train_pool(pool)
+    dt = time.perf_counter() - t0
+    return {"value": sample / dt, "unit": "samples/s", "cores": 1, "kind": "oracle",
+            "sample": f"{sample} samples (first pool segment, s={CFG['s']}, walk {CFG['walk']}) of "
+                      f"the Youtube-shaped graph, d={CFG['d']}, n=1, serial oracle, {dt:.2f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    src, dst = make_graph()
+    steps = []
+    res = None
+    for k in range(args.warmup + args.steps):
+        res = cpu_baseline(src, dst, args.cpu_sample, 16, 1000 + k)
+        if k >= args.warmup:
+            steps.append(res["value"])
+    value = statistics.median(steps)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * args.cpu_sample / value, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2 youtube-shaped 1,138,499 nodes / 4,945,382 edges, d=128, K=1, "
+                                   "s=5, walk 40, n=1; serial oracle on a bounded sample per step",
+                       "sample_per_step": args.cpu_sample},
+            "cpu_baseline": dict(res, value=value),
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1903_00757_b200 import gv as G
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = world  # one partition per GPU (configs[2]); n = 1 on one GPU (configs[1])
+    threads = args.threads or max(1, (os.cpu_count() or 16) // max(1, world))
+    src, dst = make_graph()
+    P = args.pool
+    steps_total = args.warmup + args.steps
+    total_samples = P * world * (steps_total + (0 if args.no_e2e else args.steps))
+    g = G.GraphVite(CFG["nv"], CFG["d"], n, CFG["K"], 0.025, total_samples=total_samples,
+                    device=local, rank=rank, world_size=world, ordered=1 if args.ordered else 0)
+    if world > 1:
+        uid = [G.gv_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        G.gv_comm_init(g.ctx, uid[0])
+    t0 = time.perf_counter()
+    g.load_edges(src, dst)
+    t_load = time.perf_counter() - t0
+    # the rank's pool segment: host augmentation (Alg. 2), pinned host buffer
+    host_pool = torch.empty((P, 2), dtype=torch.int32, pin_memory=True)
+    t0 = time.perf_counter()
+    g.augment(CFG["walk"], CFG["s"], threads, P, 1000 + rank, out=host_pool)
+    t_aug = time.perf_counter() - t0
+    g.push(host_pool)
+    stream = torch.cuda.ExternalStream(g.stream())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    stats = g.train_episode()  # first pool (also warm-up)
+    for _ in range(max(0, args.warmup - 1)):
+        g.replay()
+        stats = g.train_episode()
+    barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    sgd_ms, sgd_launches, launches, samples, tot_ms = 0.0, 0, 0, 0, []
+    for _ in range(args.steps):
+        g.replay()
+        st = g.train_episode()
+        sgd_ms += st["ms_sgd"]
+        sgd_launches += st["sgd_launches"]
+        launches += st["kernel_launches"]
+        samples += st["samples_global"]
+        tot_ms.append(st["ms_total"])
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = samples / (ms / 1e3)
+    # roofline of the dominant kernel (block-SGD): algorithmic bytes per launch / launch time
+    bps = BYTES_PER_SAMPLE(CFG["d"], CFG["K"])
+    local_samples = samples // world
+    avg_launch_ms = sgd_ms / max(sgd_launches, 1)
+    per_launch_samples = local_samples / max(sgd_launches, 1)
+    achieved = per_launch_samples * bps / (avg_launch_ms / 1e3) / 1e9
+    peak, peak_kind = peaks()
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "kernel": "sgd_hogwild_kernel<1,1>",
+            "peak_source": peak_kind, "sgd_share_of_step": sgd_ms / sum(tot_ms),
+            "bytes_per_sample": bps}
+    # end to end through the C ABI from pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        t0 = time.perf_counter()
+        e2e_samples = 0
+        for _ in range(args.steps):
+            g.push(host_pool)               # H2D of the step's pool
+            st = g.train_episode()          # waits for the result; stats read back (D2H)
+            e2e_samples += st["samples_global"]
+        barrier()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": e2e_samples / dt, "unit": "samples/s",
+               "h2d_bytes_per_step": P * 8,
+               "d2h_bytes_per_step": 8 * (n * n + 2) + 8}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(src, dst, args.cpu_sample, threads, 1000)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": ("C2 youtube-shaped" if world == 1 else "C3 youtube-shaped grid")
+                       + f" synthetic power-law graph {CFG['nv']:,} nodes / {CFG['ne']:,} edges "
+                       f"(chung-lu gamma {CFG['gamma']}), d={CFG['d']}, K={CFG['K']}, walk 40, "
+                       f"s={CFG['s']}, pool {P:,} samples per rank, n={n}",
+                       "partitions": n, "pool_per_rank": P, "l2": "inputs > L2 (no flush)",
+                       "mode": "ordered" if args.ordered else "hogwild"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+            "detail": {"ms_total_per_pool": tot_ms, "sgd_ms_per_pool": sgd_ms / args.steps,
+                       "bucket_ms": stats["ms_bucket"], "load_edges_s": t_load,
+                       "augment_s": t_aug, "augment_threads": threads,
+                       "alg_gbs_step": value / world * bps / 1e9},
+        }
+        print(json.dumps(line))
+    g.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -436,6 +436,11 @@ int or_trainer_negatives(const or_trainer* t, uint64_t count, uint32_t i, uint32
   return OR_OK;
 }
 
+uint32_t or_trainer_negative_at(const or_trainer* t, uint32_t q, uint32_t i, uint32_t j,
+                                uint32_t e, uint32_t k) {
+  return negative_local(t, q, i, j, e, k);
+}
+
 int or_trainer_train_block(or_trainer* t, const uint32_t* lp, uint64_t count, uint32_t i,
                            uint32_t j, uint32_t e, float lr, double* loss_out) {
   float* C[9];

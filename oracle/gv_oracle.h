@@ -79,6 +79,8 @@ int or_trainer_train_block(or_trainer* t, const uint32_t* local_pairs, uint64_t 
 /* Negatives of block (i,j) at pool index e: out[q*K + k] local ids. */
 int or_trainer_negatives(const or_trainer* t, uint64_t count, uint32_t i, uint32_t j,
                          uint32_t e, uint32_t* out);
+uint32_t or_trainer_negative_at(const or_trainer* t, uint32_t q, uint32_t i, uint32_t j,
+                                uint32_t e, uint32_t k);
 int or_trainer_explicit(or_trainer* t, const uint32_t* u, const uint32_t* v,
                         const uint32_t* negs, uint64_t count, float lr);
 void or_trainer_get(const or_trainer* t, int which, float* out);      /* 0 vertex, 1 context */

@@ -74,6 +74,7 @@ def _declare(L):
         "or_trainer_train_block": (C.c_int, [vp, u32p, C.c_uint64, C.c_uint32, C.c_uint32,
                                              C.c_uint32, C.c_float, f64p]),
         "or_trainer_negatives": (C.c_int, [vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, u32p]),
+        "or_trainer_negative_at": (C.c_uint32, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
         "or_trainer_explicit": (C.c_int, [vp, u32p, u32p, u32p, C.c_uint64, C.c_float]),
         "or_trainer_get": (None, [vp, C.c_int, f32p]),
         "or_trainer_set": (None, [vp, C.c_int, f32p]),
@@ -309,6 +310,9 @@ class Trainer:
         out = np.zeros(max(count * self.K, 1), np.uint32)
         _check(lib().or_trainer_negatives(self.h, count, i, j, e, _p(out, u32p)), "negatives")
         return out[:count * self.K].reshape(count, self.K)
+
+    def negative_at(self, q, i, j, e, k=0):
+        return int(lib().or_trainer_negative_at(self.h, q, i, j, e, k))
 
     def explicit(self, u, v, negs, lr_):
         u = _u32(u)

@@ -1,0 +1,98 @@
+// augment.cpp — parallel online augmentation (Alg. 2).
+//
+// Each sampler thread owns a private segment of the pool ("each thread is
+// allocated with an independent sample pool in advance"). It draws a
+// departure node proportional to degree, walks walk_len edges choosing each
+// neighbour proportional to the edge weight, emits the pairs of walk
+// positions within distance s, and finally pseudo-shuffles its
+// segment: pair k goes to sub-block k mod s, sub-blocks concatenated
+// (P:198-199). Random numbers come from Philox with counter
+// {walk, step, thread, 'WALK'} and key = seed (DESIGN.md R-AUG), so a pool is
+// a pure function of (graph, seed, threads) whatever the thread timing.
+#include "augment.hpp"
+
+#include <thread>
+
+#include "../../include/gv.h"
+#include "philox.cuh"
+
+namespace gv {
+
+int build_walk_tables(const HostGraph& g, int threads, WalkTables* t) {
+  t->g = &g;
+  t->departure.prob.resize(g.nv);
+  t->departure.alias.resize(g.nv);
+  int rc = build_alias(g.deg.data(), g.nv, t->departure.prob.data(), t->departure.alias.data());
+  if (rc) return rc;
+  t->eprob.assign(g.nbr.size(), 0);
+  t->ealias.assign(g.nbr.size(), 0);
+  parallel_for(g.nv, threads, [&](uint64_t b, uint64_t e) {
+    for (uint64_t v = b; v < e; ++v) {
+      const uint64_t o = g.off[v], m = g.off[v + 1] - o;
+      if (m == 0 || !(g.deg[v] > 0.0)) continue;  // unreachable by any walk
+      build_alias(g.w.data() + o, static_cast<uint32_t>(m), t->eprob.data() + o,
+                  t->ealias.data() + o);
+    }
+  });
+  return GV_OK;
+}
+
+namespace {
+
+inline uint32_t draw(const uint32_t* prob, const uint32_t* alias, uint32_t m, const u32x4& r) {
+  const uint32_t slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, m);
+  return alias_pick(prob[slot], alias[slot], slot, r.z);
+}
+
+void fill_segment(const WalkTables& t, uint32_t walk_len, uint32_t s, uint32_t thread,
+                  uint64_t cap, uint64_t seed, uint32_t* out) {
+  const HostGraph& g = *t.g;
+  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+  std::vector<uint32_t> seg(2 * cap);
+  std::vector<uint32_t> walk(walk_len + 1);
+  uint64_t filled = 0;
+  for (uint32_t w = 0; filled < cap; ++w) {
+    u32x4 r = philox4x32_10(u32x4{w, 0u, thread, kTagWalk}, k0, k1);
+    walk[0] = draw(t.departure.prob.data(), t.departure.alias.data(), g.nv, r);
+    for (uint32_t k = 1; k <= walk_len; ++k) {
+      const uint32_t x = walk[k - 1];
+      const uint64_t o = g.off[x];
+      const uint32_t m = static_cast<uint32_t>(g.off[x + 1] - o);
+      r = philox4x32_10(u32x4{w, k, thread, kTagWalk}, k0, k1);
+      walk[k] = g.nbr[o + draw(t.eprob.data() + o, t.ealias.data() + o, m, r)];
+    }
+    // pairs within distance s, by increasing start then end position
+    for (uint32_t a = 0; a <= walk_len && filled < cap; ++a) {
+      const uint32_t last = a + s < walk_len ? a + s : walk_len;
+      for (uint32_t b = a + 1; b <= last && filled < cap; ++b) {
+        if (walk[a] == walk[b]) continue;
+        seg[2 * filled] = walk[a];
+        seg[2 * filled + 1] = walk[b];
+        ++filled;
+      }
+    }
+  }
+  // pseudo shuffle: sub-block j holds pairs j, j+s, j+2s, ...
+  uint64_t pos = 0;
+  for (uint32_t j = 0; j < s; ++j)
+    for (uint64_t k = j; k < cap; k += s, ++pos) {
+      out[2 * pos] = seg[2 * k];
+      out[2 * pos + 1] = seg[2 * k + 1];
+    }
+}
+
+}  // namespace
+
+void augment(const WalkTables& t, uint32_t walk_len, uint32_t s, uint32_t threads,
+             uint64_t count, uint64_t seed, uint32_t* out) {
+  std::vector<std::thread> pool;
+  for (uint32_t th = 0; th < threads; ++th) {
+    const uint64_t b = static_cast<uint64_t>((static_cast<unsigned __int128>(count) * th) / threads);
+    const uint64_t e =
+        static_cast<uint64_t>((static_cast<unsigned __int128>(count) * (th + 1)) / threads);
+    pool.emplace_back(fill_segment, std::cref(t), walk_len, s, th, e - b, seed, out + 2 * b);
+  }
+  for (auto& x : pool) x.join();
+}
+
+}  // namespace gv

@@ -1,0 +1,1119 @@
+// engine.cpp — context, episode scheduler and C ABI (include/gv.h).
+//
+// One gv_ctx per process. It drives D ranks of Alg. 3: either
+// the single rank of this process (world_size = D, NCCL between processes)
+// or D virtual ranks on this process's GPU (virtual_ranks = D, device copies).
+// Rank d owns vertex partitions [d m, (d+1) m), m = n / D, and at offset
+// step t holds the context window (d m + t + g) mod n, g = 0..m-1. After it
+// trains its first block of step t (context (d m + t) mod n) it sends that
+// partition to rank d-1, which needs it for the LAST block of step t+1, so
+// the transfer overlaps the rank's remaining m-1 blocks.
+// With m = 1 this is Alg. 3's train -> rotate -> train ring.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/gv.h"
+#include "augment.hpp"
+#include "host_graph.hpp"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+// ------------------------------------------------------------------ NCCL
+// Loaded lazily so that single-process use has no NCCL dependency.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    void* h = nullptr;
+    for (const char* n : names)
+      if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return;
+#define GV_SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, "nccl" #f))
+    GV_SYM(GetUniqueId); GV_SYM(CommInitRank); GV_SYM(CommDestroy); GV_SYM(Send);
+    GV_SYM(Recv); GV_SYM(AllGather); GV_SYM(GroupStart); GV_SYM(GroupEnd); GV_SYM(GetErrorString);
+#undef GV_SYM
+    api.ok = api.GetUniqueId && api.CommInitRank && api.Send && api.Recv && api.AllGather &&
+             api.GroupStart && api.GroupEnd;
+  });
+  return api;
+}
+
+// -------------------------------------------------------------- buffers
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;  // elements
+  size_t bytes_total() const { return cap * sizeof(T); }
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T));
+    if (e == cudaSuccess) cap = std::max<size_t>(n, 1);
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct Rank {
+  int d = 0;  // global rank index
+  cudaStream_t compute = nullptr, comm = nullptr;
+  float* vertex = nullptr;
+  uint64_t vrow_first = 0, vrows = 0;  // new-id range of the vertex shard
+  float* context = nullptr;
+  uint64_t crows = 0, slot_rows = 0;
+  std::vector<int> slot_of;  // partition -> context slot (D > 1)
+  int free_slot = -1;
+  DevBuf<uint2> local_blocks, recv, blocks;
+  DevBuf<uint8_t> scratch;
+  DevBuf<uint64_t> counts;      // [0, bins]: block_off; [bins+1]: error flag
+  DevBuf<uint64_t> all_counts;  // NCCL: gathered counts of every rank
+  DevBuf<gv::BlockDesc> desc;
+  DevBuf<gv::CopySeg> segs;
+  DevBuf<double> loss;
+  uint64_t* counts_host = nullptr;  // pinned
+  std::vector<uint64_t> local_off;  // this rank's local block_off (bins + 1)
+  std::vector<uint64_t> final_off;  // m*n + 1: layout of blocks (g, j) in `blocks`
+  uint64_t seg_begin = 0, seg_count = 0;
+  // events
+  cudaEvent_t ev_start = nullptr, ev_bucket = nullptr, ev_exch = nullptr, ev_end = nullptr;
+  cudaEvent_t ev_recv_consumed = nullptr, ev_exch_sent = nullptr;
+  std::vector<cudaEvent_t> ev_first_done, ev_recv, ev_sent;  // per step
+  cudaEvent_t ev_last_recv = nullptr;  // rotation into the window of the next pool
+  bool have_last_recv = false;
+  std::vector<cudaEvent_t> ev_sgd;  // pairs (begin, end) per launch
+  int sgd_launches = 0;
+  int kernel_launches = 0;
+  double ms_bucket = 0, ms_exchange = 0, ms_sgd = 0, ms_total = 0;
+};
+
+enum class PoolState { Idle, Prepared };
+
+}  // namespace
+
+struct gv_ctx {
+  // parameters
+  uint32_t nv = 0, dim = 0, n = 1, K = 1;
+  float lr0 = 0.025f;
+  gv_lr_schedule alpha{GV_LR_LINEAR, 1e-4, 0};
+  gv_options opt{};
+  int D = 1;       // total ranks
+  int local = 1;   // ranks driven by this process
+  uint32_t m = 1;  // partitions per rank
+  uint32_t stride = 0;
+  int threads = 1;
+  int sms = 148;
+  std::string err;
+  bool loaded = false;
+  // graph
+  gv::HostGraph graph;
+  gv::Partitioning part;
+  std::vector<uint32_t> nprob, nalias;  // negative tables, new-id order
+  gv::WalkTables walks;
+  // shared device tables
+  uint32_t* d_packed = nullptr;
+  uint2* d_alias = nullptr;
+  uint32_t* d_inv_perm = nullptr;
+  // pools
+  std::mutex mu;
+  DevBuf<uint2> raw[2];
+  uint64_t raw_count[2] = {0, 0};
+  cudaEvent_t raw_ready[2] = {nullptr, nullptr};
+  cudaEvent_t raw_free[2] = {nullptr, nullptr};
+  int pending = 0;
+  int last_active = -1;
+  uint64_t last_count = 0;
+  cudaStream_t copy_stream = nullptr;
+  PoolState state = PoolState::Idle;
+  int active = -1;
+  uint64_t pool_P = 0;        // samples of the prepared pool (this process)
+  uint64_t pool_P_global = 0; // all ranks
+  std::vector<uint64_t> global_counts;  // bins (sum over ranks)
+  // progress
+  uint64_t pool_index = 0;
+  uint64_t samples_done = 0;  // global samples trained in earlier steps
+  std::vector<Rank> ranks;
+  ncclComm_t comm = nullptr;
+  bool comm_ready = false;
+};
+
+namespace {
+
+gv_status fail(gv_ctx* c, gv_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  g_last_error = msg;
+  return s;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(c, GV_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define NK(call)                                                                         \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      return fail(c, GV_ERR_COMM,                                                        \
+                  std::string(#call) + ": " +                                            \
+                      (nccl().GetErrorString ? nccl().GetErrorString(r_) : "nccl error")); \
+  } while (0)
+
+float lr_at(const gv_ctx* c, uint64_t s_before) {
+  if (c->alpha.kind == GV_LR_CONSTANT || c->alpha.total_samples == 0) return c->lr0;
+  double r = 1.0 - static_cast<double>(s_before) / static_cast<double>(c->alpha.total_samples);
+  if (r < c->alpha.floor_ratio) r = c->alpha.floor_ratio;
+  return static_cast<float>(static_cast<double>(c->lr0) * r);
+}
+
+uint64_t psize(const gv_ctx* c, uint32_t p) { return c->part.off[p + 1] - c->part.off[p]; }
+
+cudaEvent_t new_event(bool timing) {
+  cudaEvent_t e = nullptr;
+  cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming);
+  return e;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return 0.f;
+  return ms;
+}
+
+// Context row of local id 0 of partition j on rank r (valid while held).
+uint64_t crow0(const gv_ctx* c, const Rank& r, uint32_t j) {
+  if (c->D == 1) return c->part.off[j];
+  return static_cast<uint64_t>(r.slot_of[j]) * r.slot_rows;
+}
+
+gv_status sync_all(gv_ctx* c) {
+  for (auto& r : c->ranks) {
+    CK(cudaStreamSynchronize(r.compute));
+    CK(cudaStreamSynchronize(r.comm));
+  }
+  if (c->copy_stream) CK(cudaStreamSynchronize(c->copy_stream));
+  return GV_OK;
+}
+
+// --------------------------------------------------------------- prepare
+// a3-a6: bucket every local rank's pool segment, exchange block rows.
+gv_status prepare(gv_ctx* c) {
+  if (c->state == PoolState::Prepared) return GV_OK;
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (c->raw_count[c->pending] == 0) return fail(c, GV_ERR_EMPTY, "no pending samples");
+    c->active = c->pending;
+    c->pool_P = c->raw_count[c->active];
+    c->pending ^= 1;
+    c->raw_count[c->pending] = 0;
+  }
+  const int a = c->active;
+  const uint32_t n = c->n, bins = n * n;
+  const uint64_t P = c->pool_P;
+  // 1) bucketing per rank (a3-a5)
+  for (auto& r : c->ranks) {
+    r.kernel_launches = 0;
+    r.sgd_launches = 0;
+    if (c->opt.world_size > 1) {
+      r.seg_begin = 0;
+      r.seg_count = P;
+    } else {
+      r.seg_begin = P * static_cast<uint64_t>(r.d) / c->D;
+      r.seg_count = P * static_cast<uint64_t>(r.d + 1) / c->D - r.seg_begin;
+    }
+    CK(cudaStreamWaitEvent(r.compute, c->raw_ready[a], 0));
+    CK(cudaEventRecord(r.ev_start, r.compute));
+    const gv::BucketPlan plan = gv::make_bucket_plan(n, r.seg_count);
+    CK(r.scratch.ensure(gv::bucket_scratch_bytes(plan)));
+    DevBuf<uint2>& out = (c->D == 1) ? r.blocks : r.local_blocks;
+    CK(out.ensure(r.seg_count));
+    CK(cudaMemsetAsync(r.counts.p + bins + 1, 0, sizeof(uint64_t), r.compute));
+    CK(gv::launch_bucket(c->raw[a].p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
+                         c->part.pbits, plan, r.scratch.p, out.p, r.counts.p,
+                         reinterpret_cast<uint32_t*>(r.counts.p + bins + 1), r.compute,
+                         &r.kernel_launches));
+    CK(cudaEventRecord(r.ev_bucket, r.compute));
+  }
+  // the raw buffer may be refilled once every rank has bucketed it
+  for (auto& r : c->ranks) CK(cudaStreamWaitEvent(c->copy_stream, r.ev_bucket, 0));
+  CK(cudaEventRecord(c->raw_free[a], c->copy_stream));
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->last_active = a;
+    c->last_count = P;
+  }
+  // 2) counts to the host (NCCL: all-gather first)
+  std::vector<std::vector<uint64_t>> cnt(c->D, std::vector<uint64_t>(bins + 2, 0));
+  if (c->opt.world_size > 1) {
+    Rank& r = c->ranks[0];
+    NK(nccl().AllGather(r.counts.p, r.all_counts.p, bins + 2, ncclUint64, c->comm, r.compute));
+    CK(cudaMemcpyAsync(r.counts_host, r.all_counts.p, sizeof(uint64_t) * (bins + 2) * c->D,
+                       cudaMemcpyDeviceToHost, r.compute));
+    CK(cudaStreamSynchronize(r.compute));
+    for (int q = 0; q < c->D; ++q)
+      std::copy(r.counts_host + q * (bins + 2), r.counts_host + (q + 1) * (bins + 2),
+                cnt[q].begin());
+  } else {
+    for (auto& r : c->ranks)
+      CK(cudaMemcpyAsync(r.counts_host, r.counts.p, sizeof(uint64_t) * (bins + 2),
+                         cudaMemcpyDeviceToHost, r.compute));
+    for (auto& r : c->ranks) {
+      CK(cudaStreamSynchronize(r.compute));
+      std::copy(r.counts_host, r.counts_host + bins + 2, cnt[r.d].begin());
+    }
+  }
+  bool bad = false;
+  for (int q = 0; q < c->D; ++q) bad |= cnt[q][bins + 1] != 0;
+  if (bad) {
+    c->state = PoolState::Idle;
+    return fail(c, GV_ERR_OUT_OF_RANGE, "sample pool contains a node id >= num_nodes");
+  }
+  // per-rank bin counts from block offsets
+  std::vector<std::vector<uint64_t>> bc(c->D, std::vector<uint64_t>(bins));
+  c->global_counts.assign(bins, 0);
+  c->pool_P_global = 0;
+  for (int q = 0; q < c->D; ++q)
+    for (uint32_t b = 0; b < bins; ++b) {
+      bc[q][b] = cnt[q][b + 1] - cnt[q][b];
+      c->global_counts[b] += bc[q][b];
+    }
+  for (uint32_t b = 0; b < bins; ++b) {
+    c->pool_P_global += c->global_counts[b];
+    if (c->global_counts[b] > 0xFFFFFFFFull) {
+      c->state = PoolState::Idle;
+      return fail(c, GV_ERR_CAPACITY, "a block holds more than 2^32-1 samples");
+    }
+  }
+  // 3) final layout of each local rank's block rows; exchange (a6)
+  const uint32_t m = c->m;
+  for (auto& r : c->ranks) {
+    r.local_off.assign(cnt[r.d].begin(), cnt[r.d].begin() + bins + 1);
+    r.final_off.assign(static_cast<size_t>(m) * n + 1, 0);
+    const uint32_t b0 = r.d * m * n;
+    for (uint32_t q = 0; q < m * n; ++q) r.final_off[q + 1] = r.final_off[q] + c->global_counts[b0 + q];
+  }
+  if (c->D > 1) {
+    // chunk from rank s to rank d = local bins of rows [d m, (d+1) m) of rank s
+    auto chunk_begin = [&](int s, int d) { return cnt[s][d * m * n]; };
+    auto chunk_len = [&](int s, int d) { return cnt[s][(d + 1) * m * n] - cnt[s][d * m * n]; };
+    for (auto& r : c->ranks) {
+      uint64_t total = 0;
+      for (int s = 0; s < c->D; ++s) total += chunk_len(s, r.d);
+      CK(r.recv.ensure(total));
+      CK(r.blocks.ensure(total));
+    }
+    if (c->opt.world_size > 1) {
+      Rank& r = c->ranks[0];
+      NK(nccl().GroupStart());
+      uint64_t roff = 0;
+      for (int p = 0; p < c->D; ++p) {
+        if (chunk_len(r.d, p))
+          NK(nccl().Send(r.local_blocks.p + chunk_begin(r.d, p), 2 * chunk_len(r.d, p), ncclUint32,
+                         p, c->comm, r.compute));
+        if (chunk_len(p, r.d))
+          NK(nccl().Recv(r.recv.p + roff, 2 * chunk_len(p, r.d), ncclUint32, p, c->comm,
+                         r.compute));
+        roff += chunk_len(p, r.d);
+      }
+      NK(nccl().GroupEnd());
+    } else {
+      // virtual ranks: rank s copies its chunk into rank d's receive buffer
+      for (auto& s : c->ranks) {
+        for (auto& d : c->ranks) CK(cudaStreamWaitEvent(s.compute, d.ev_recv_consumed, 0));
+        for (auto& d : c->ranks) {
+          uint64_t roff = 0;
+          for (int q = 0; q < s.d; ++q) roff += chunk_len(q, d.d);
+          const uint64_t len = chunk_len(s.d, d.d);
+          if (len)
+            CK(cudaMemcpyAsync(d.recv.p + roff, s.local_blocks.p + chunk_begin(s.d, d.d),
+                               len * sizeof(uint2), cudaMemcpyDeviceToDevice, s.compute));
+        }
+        CK(cudaEventRecord(s.ev_exch_sent, s.compute));
+      }
+      for (auto& d : c->ranks)
+        for (auto& s : c->ranks) CK(cudaStreamWaitEvent(d.compute, s.ev_exch_sent, 0));
+    }
+    // placement: block (i, j) = concatenation of the sub-blocks of ranks 0..D-1
+    for (auto& r : c->ranks) {
+      std::vector<gv::CopySeg> segs;
+      const uint32_t b0 = r.d * m * n;
+      uint64_t roff = 0;
+      std::vector<uint64_t> within(m * n, 0);
+      for (int s = 0; s < c->D; ++s) {
+        const uint64_t cb = chunk_begin(s, r.d);
+        for (uint32_t q = 0; q < m * n; ++q) {
+          const uint64_t len = bc[s][b0 + q];
+          if (len) segs.push_back({roff + (cnt[s][b0 + q] - cb), r.final_off[q] + within[q], len});
+          within[q] += len;
+        }
+        roff += chunk_len(s, r.d);
+      }
+      CK(r.segs.ensure(std::max<size_t>(segs.size(), 1)));
+      if (!segs.empty()) {
+        CK(cudaMemcpyAsync(r.segs.p, segs.data(), segs.size() * sizeof(gv::CopySeg),
+                           cudaMemcpyHostToDevice, r.compute));
+        CK(gv::launch_segmented_copy(r.recv.p, r.blocks.p, r.segs.p, static_cast<int>(segs.size()),
+                                     r.compute));
+        r.kernel_launches += 1;
+      }
+      CK(cudaEventRecord(r.ev_recv_consumed, r.compute));
+    }
+  }
+  for (auto& r : c->ranks) CK(cudaEventRecord(r.ev_exch, r.compute));
+  c->state = PoolState::Prepared;
+  return GV_OK;
+}
+
+// ---------------------------------------------------------------- steps
+// a7-a8 for the prepared pool.
+gv_status run_steps(gv_ctx* c) {
+  const uint32_t n = c->n, m = c->m;
+  const uint32_t e = static_cast<uint32_t>(c->pool_index);
+  const uint32_t key0 = static_cast<uint32_t>(c->opt.seed), key1 = static_cast<uint32_t>(c->opt.seed >> 32);
+  // lr per offset step from the global sample counts (R-LR)
+  std::vector<float> lr(n);
+  uint64_t s_before = c->samples_done;
+  for (uint32_t t = 0; t < n; ++t) {
+    lr[t] = lr_at(c, s_before);
+    for (uint32_t i = 0; i < n; ++i) s_before += c->global_counts[i * n + (i + t) % n];
+  }
+  // descriptors: D == 1 -> one launch per step over all n blocks;
+  //              D > 1  -> one launch per block (g), so the first block of a
+  //              step can release its context partition early.
+  for (auto& r : c->ranks) {
+    std::vector<gv::BlockDesc> desc(static_cast<size_t>(n) * m);
+    // slot bookkeeping is simulated here exactly as the rotation will move data
+    std::vector<int> slot_of = r.slot_of;
+    int free_slot = r.free_slot;
+    for (uint32_t t = 0; t < n; ++t) {
+      uint64_t prefix = 0;
+      for (uint32_t g = 0; g < m; ++g) {
+        const uint32_t i = r.d * m + g, j = (i + t) % n;
+        gv::BlockDesc& d = desc[t * m + g];
+        d.sample_off = r.final_off[g * n + j];
+        d.count_lo = static_cast<uint32_t>(r.final_off[g * n + j + 1] - r.final_off[g * n + j]);
+        d.prefix = (c->D == 1) ? prefix : 0;
+        prefix += d.count_lo;
+        d.vrow0 = static_cast<uint32_t>(c->part.off[i] - r.vrow_first);
+        d.crow0 = static_cast<uint32_t>(c->D == 1 ? c->part.off[j]
+                                                  : static_cast<uint64_t>(slot_of[j]) * r.slot_rows);
+        d.alias0 = static_cast<uint32_t>(c->part.off[j]);
+        d.m = static_cast<uint32_t>(psize(c, j));
+        d.ij = (i << 16) | j;
+      }
+      if (c->D > 1) {  // after step t: partition (d m + t) leaves, ((d+1) m + t) arrives
+        const uint32_t out_p = (r.d * m + t) % n, in_p = ((r.d + 1) * m + t) % n;
+        const int s_out = slot_of[out_p];
+        slot_of[in_p] = free_slot;
+        slot_of[out_p] = -1;
+        free_slot = s_out;
+      }
+    }
+    CK(r.desc.ensure(desc.size()));
+    CK(cudaMemcpyAsync(r.desc.p, desc.data(), desc.size() * sizeof(gv::BlockDesc),
+                       cudaMemcpyHostToDevice, r.compute));
+    // (pageable source: the copy is staged before cudaMemcpyAsync returns)
+    if (c->opt.compute_loss) CK(cudaMemsetAsync(r.loss.p, 0, sizeof(double), r.compute));
+    const size_t need = static_cast<size_t>(2) * (c->D == 1 ? n : n * m);
+    while (r.ev_sgd.size() < need) r.ev_sgd.push_back(new_event(true));
+  }
+  // enqueue the steps
+  for (uint32_t t = 0; t < n; ++t) {
+    for (auto& r : c->ranks) {
+      gv::SgdArgs a{};
+      a.samples = r.blocks.p;
+      a.vertex = r.vertex;
+      a.context = r.context;
+      a.alias = c->d_alias;
+      a.stride = c->stride;
+      a.lr = lr[t];
+      a.neg_weight = c->opt.neg_weight;
+      a.pool_index = e;
+      a.key0 = key0;
+      a.key1 = key1;
+      a.loss_acc = c->opt.compute_loss ? r.loss.p : nullptr;
+      auto launch = [&](uint32_t g0, uint32_t cnt_blk) -> gv_status {
+        a.desc = r.desc.p + t * m + g0;
+        a.nblk = static_cast<int>(cnt_blk);
+        uint64_t tot = 0;
+        for (uint32_t g = g0; g < g0 + cnt_blk; ++g)
+          tot += r.final_off[g * n + (r.d * m + g + t) % n + 1] - r.final_off[g * n + (r.d * m + g + t) % n];
+        a.total = tot;
+        cudaEvent_t eb = r.ev_sgd[2 * r.sgd_launches], ee = r.ev_sgd[2 * r.sgd_launches + 1];
+        CK(cudaEventRecord(eb, r.compute));
+        if (c->opt.ordered)
+          CK(gv::launch_sgd_ordered(a, c->dim, c->K, r.compute));
+        else
+          CK(gv::launch_sgd_hogwild(a, c->dim, c->K, c->sms, r.compute));
+        CK(cudaEventRecord(ee, r.compute));
+        r.sgd_launches++;
+        r.kernel_launches++;
+        return GV_OK;
+      };
+      if (c->D == 1) {
+        gv_status st = launch(0, m);
+        if (st) return st;
+        continue;
+      }
+      for (uint32_t g = 0; g < m; ++g) {
+        if (g == m - 1) {
+          // the last block's context arrived by the previous rotation
+          if (t > 0) CK(cudaStreamWaitEvent(r.compute, r.ev_recv[t - 1], 0));
+          else if (r.have_last_recv) CK(cudaStreamWaitEvent(r.compute, r.ev_last_recv, 0));
+        }
+        gv_status st = launch(g, 1);
+        if (st) return st;
+        if (g == 0) CK(cudaEventRecord(r.ev_first_done[t], r.compute));
+      }
+    }
+    if (c->D == 1) continue;
+    // rotation of step t (a8): rank d sends partition (d m + t) to rank d-1
+    if (c->opt.world_size > 1) {
+      Rank& r = c->ranks[0];
+      const uint32_t out_p = (r.d * m + t) % n, in_p = ((r.d + 1) * m + t) % n;
+      const int prev = (r.d + c->D - 1) % c->D, next = (r.d + 1) % c->D;
+      CK(cudaStreamWaitEvent(r.comm, r.ev_first_done[t], 0));
+      NK(nccl().GroupStart());
+      NK(nccl().Send(r.context + static_cast<uint64_t>(r.slot_of[out_p]) * r.slot_rows * c->stride,
+                     psize(c, out_p) * c->stride, ncclFloat32, prev, c->comm, r.comm));
+      NK(nccl().Recv(r.context + static_cast<uint64_t>(r.free_slot) * r.slot_rows * c->stride,
+                     psize(c, in_p) * c->stride, ncclFloat32, next, c->comm, r.comm));
+      NK(nccl().GroupEnd());
+      CK(cudaEventRecord(r.ev_recv[t], r.comm));
+      const int s_out = r.slot_of[out_p];
+      r.slot_of[in_p] = r.free_slot;
+      r.slot_of[out_p] = -1;
+      r.free_slot = s_out;
+    } else {
+      // device copies between virtual ranks; slot moves computed first
+      std::vector<int> dst_slot(c->D), src_slot(c->D);
+      for (auto& r : c->ranks) {
+        const uint32_t out_p = (r.d * m + t) % n;
+        src_slot[r.d] = r.slot_of[out_p];
+        dst_slot[r.d] = r.free_slot;  // where rank r receives
+      }
+      for (auto& r : c->ranks) {
+        Rank& prev = c->ranks[(r.d + c->D - 1) % c->D];
+        const uint32_t out_p = (r.d * m + t) % n;
+        CK(cudaStreamWaitEvent(r.comm, r.ev_first_done[t], 0));
+        // prev's free slot was released by prev's own send of step t-1
+        if (t > 0) CK(cudaStreamWaitEvent(r.comm, prev.ev_sent[t - 1], 0));
+        else if (prev.have_last_recv) CK(cudaStreamWaitEvent(r.comm, prev.ev_last_recv, 0));
+        CK(cudaMemcpyAsync(
+            prev.context + static_cast<uint64_t>(dst_slot[prev.d]) * prev.slot_rows * c->stride,
+            r.context + static_cast<uint64_t>(src_slot[r.d]) * r.slot_rows * c->stride,
+            psize(c, out_p) * c->stride * sizeof(float), cudaMemcpyDeviceToDevice, r.comm));
+        CK(cudaEventRecord(r.ev_sent[t], r.comm));
+        CK(cudaEventRecord(prev.ev_recv[t], r.comm));
+      }
+      for (auto& r : c->ranks) {
+        const uint32_t out_p = (r.d * m + t) % n, in_p = ((r.d + 1) * m + t) % n;
+        r.slot_of[in_p] = dst_slot[r.d];
+        r.slot_of[out_p] = -1;
+        r.free_slot = src_slot[r.d];
+      }
+    }
+  }
+  for (auto& r : c->ranks) {
+    if (c->D > 1) {
+      // the pool ends after the last rotation (Alg. 3 order); the next pool's
+      // step-0 last block and the next rotation wait on it
+      CK(cudaStreamWaitEvent(r.compute, r.ev_recv[n - 1], 0));
+      CK(cudaEventRecord(r.ev_last_recv, r.compute));
+      r.have_last_recv = true;
+    }
+    CK(cudaEventRecord(r.ev_end, r.compute));
+  }
+  c->samples_done = s_before;
+  c->pool_index++;
+  c->state = PoolState::Idle;
+  return GV_OK;
+}
+
+gv_status collect_stats(gv_ctx* c, gv_episode_stats* out) {
+  gv_status st = sync_all(c);
+  if (st) return st;
+  std::memset(out, 0, sizeof(*out));
+  out->pool_index = c->pool_index - 1;
+  out->samples_global = c->pool_P_global;
+  out->n_steps = c->n;
+  uint64_t before = c->samples_done - c->pool_P_global;
+  out->lr_first = lr_at(c, before);
+  uint64_t s = before;
+  for (uint32_t t = 0; t + 1 < c->n; ++t)
+    for (uint32_t i = 0; i < c->n; ++i) s += c->global_counts[i * c->n + (i + t) % c->n];
+  out->lr_last = lr_at(c, s);
+  for (auto& r : c->ranks) {
+    out->samples += r.final_off.empty() ? 0 : r.final_off.back();
+    r.ms_bucket = elapsed(r.ev_start, r.ev_bucket);
+    r.ms_exchange = elapsed(r.ev_bucket, r.ev_exch);
+    r.ms_total = elapsed(r.ev_start, r.ev_end);
+    double sgd = 0;
+    for (int k = 0; k < r.sgd_launches; ++k) sgd += elapsed(r.ev_sgd[2 * k], r.ev_sgd[2 * k + 1]);
+    r.ms_sgd = sgd;
+    out->ms_bucket = std::max(out->ms_bucket, r.ms_bucket);
+    out->ms_exchange = std::max(out->ms_exchange, r.ms_exchange);
+    out->ms_sgd = std::max(out->ms_sgd, r.ms_sgd);
+    out->ms_total = std::max(out->ms_total, r.ms_total);
+    out->sgd_launches += r.sgd_launches;
+    out->kernel_launches += r.kernel_launches;
+    if (c->opt.compute_loss) {
+      double l = 0;
+      CK(cudaMemcpy(&l, r.loss.p, sizeof(double), cudaMemcpyDeviceToHost));
+      out->loss_sum += l;
+    }
+  }
+  out->ms_rotate = std::max(0.0, out->ms_total - out->ms_bucket - out->ms_exchange - out->ms_sgd);
+  return GV_OK;
+}
+
+gv_status setup_device(gv_ctx* c) {
+  const uint32_t nv = c->nv, n = c->n, m = c->m;
+  CK(cudaMalloc(&c->d_packed, sizeof(uint32_t) * nv));
+  CK(cudaMalloc(&c->d_alias, sizeof(uint2) * nv));
+  CK(cudaMalloc(&c->d_inv_perm, sizeof(uint32_t) * nv));
+  std::vector<uint2> al(nv);
+  for (uint32_t k = 0; k < nv; ++k) al[k] = make_uint2(c->nprob[k], c->nalias[k]);
+  CK(cudaMemcpy(c->d_packed, c->part.packed.data(), sizeof(uint32_t) * nv, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_alias, al.data(), sizeof(uint2) * nv, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_inv_perm, c->part.inv_perm.data(), sizeof(uint32_t) * nv,
+                cudaMemcpyHostToDevice));
+  CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k) {
+    c->raw_ready[k] = new_event(false);
+    c->raw_free[k] = new_event(false);
+  }
+  const uint32_t key0 = static_cast<uint32_t>(c->opt.init_seed);
+  const uint32_t key1 = static_cast<uint32_t>(c->opt.init_seed >> 32);
+  const uint64_t max_part = c->part.max_part();
+  for (auto& r : c->ranks) {
+    CK(cudaStreamCreateWithFlags(&r.compute, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&r.comm, cudaStreamNonBlocking));
+    r.vrow_first = c->part.off[r.d * m];
+    r.vrows = c->part.off[(r.d + 1) * m] - r.vrow_first;
+    CK(cudaMalloc(&r.vertex, sizeof(float) * std::max<uint64_t>(r.vrows, 1) * c->stride));
+    CK(cudaMemsetAsync(r.vertex, 0, sizeof(float) * r.vrows * c->stride, r.compute));
+    CK(gv::launch_init_vertex(r.vertex, c->stride, c->dim, r.vrow_first, r.vrows, c->d_inv_perm,
+                              key0, key1, r.compute));
+    if (c->D == 1) {
+      r.crows = nv;
+      r.slot_rows = 0;
+    } else {
+      r.slot_rows = max_part;
+      r.crows = (m + 1) * max_part;
+      r.slot_of.assign(n, -1);
+      for (uint32_t g = 0; g < m; ++g) r.slot_of[r.d * m + g] = static_cast<int>(g);
+      r.free_slot = static_cast<int>(m);
+      r.ev_first_done.resize(n);
+      r.ev_recv.resize(n);
+      r.ev_sent.resize(n);
+      for (uint32_t t = 0; t < n; ++t) {
+        r.ev_first_done[t] = new_event(false);
+        r.ev_recv[t] = new_event(false);
+        r.ev_sent[t] = new_event(false);
+      }
+      r.ev_last_recv = new_event(false);
+    }
+    CK(cudaMalloc(&r.context, sizeof(float) * r.crows * c->stride));
+    CK(cudaMemsetAsync(r.context, 0, sizeof(float) * r.crows * c->stride, r.compute));
+    CK(r.counts.ensure(n * n + 2));
+    if (c->opt.world_size > 1) CK(r.all_counts.ensure(static_cast<size_t>(n * n + 2) * c->D));
+    CK(r.loss.ensure(1));
+    CK(cudaMallocHost(&r.counts_host, sizeof(uint64_t) * (n * n + 2) * c->D));
+    r.ev_start = new_event(true);
+    r.ev_bucket = new_event(true);
+    r.ev_exch = new_event(true);
+    r.ev_end = new_event(true);
+    r.ev_recv_consumed = new_event(false);
+    r.ev_exch_sent = new_event(false);
+    CK(cudaEventRecord(r.ev_recv_consumed, r.compute));
+  }
+  return sync_all(c);
+}
+
+gv_status check_ctx(gv_ctx* c, bool need_loaded) {
+  if (!c) return fail(nullptr, GV_ERR_INVALID_ARG, "null context");
+  if (need_loaded && !c->loaded) return fail(c, GV_ERR_STATE, "gv_load_edges has not been called");
+  return GV_OK;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+void gv_default_options(gv_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->seed = 5;
+  o->init_seed = 4;
+  o->neg_weight = 5.0f;
+  o->device = 0;
+  o->rank = 0;
+  o->world_size = 1;
+  o->virtual_ranks = 1;
+  o->ordered = 0;
+  o->compute_loss = 1;
+  o->host_threads = 0;
+  o->max_pool_samples = 0;
+}
+
+int gv_abi_version(void) { return GV_ABI_VERSION; }
+
+const char* gv_status_string(gv_status s) {
+  switch (s) {
+    case GV_OK: return "GV_OK";
+    case GV_ERR_INVALID_ARG: return "GV_ERR_INVALID_ARG";
+    case GV_ERR_STATE: return "GV_ERR_STATE";
+    case GV_ERR_OUT_OF_RANGE: return "GV_ERR_OUT_OF_RANGE";
+    case GV_ERR_EMPTY: return "GV_ERR_EMPTY";
+    case GV_ERR_CAPACITY: return "GV_ERR_CAPACITY";
+    case GV_ERR_NOMEM: return "GV_ERR_NOMEM";
+    case GV_ERR_CUDA: return "GV_ERR_CUDA";
+    case GV_ERR_COMM: return "GV_ERR_COMM";
+  }
+  return "unknown";
+}
+
+const char* gv_last_error(const gv_ctx* c) { return c ? c->err.c_str() : g_last_error.c_str(); }
+
+gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
+                    uint32_t num_negatives, float lr0, const gv_lr_schedule* alpha,
+                    const gv_options* opt, gv_ctx** out) {
+  gv_ctx* c = nullptr;
+  if (!out) return fail(nullptr, GV_ERR_INVALID_ARG, "out is null");
+  gv_options o;
+  if (opt) o = *opt; else gv_default_options(&o);
+  if (num_nodes == 0 || dim == 0 || dim % 4 != 0 || dim > 512)
+    return fail(nullptr, GV_ERR_INVALID_ARG, "num_nodes > 0 and dim in {4, 8, ..., 512} required");
+  if (num_negatives == 0 || num_negatives > 8)
+    return fail(nullptr, GV_ERR_INVALID_ARG, "num_negatives must be in [1, 8]");
+  if (n_partitions == 0 || n_partitions > num_nodes || n_partitions > 64)
+    return fail(nullptr, GV_ERR_INVALID_ARG, "n_partitions must be in [1, min(64, num_nodes)]");
+  if (!(lr0 >= 0.0f)) return fail(nullptr, GV_ERR_INVALID_ARG, "lr0 must be >= 0");
+  if (o.world_size < 1 || o.virtual_ranks < 1 || o.rank < 0 || o.rank >= o.world_size ||
+      (o.world_size > 1 && o.virtual_ranks != 1))
+    return fail(nullptr, GV_ERR_INVALID_ARG, "bad rank / world_size / virtual_ranks");
+  const int D = o.world_size * o.virtual_ranks;
+  if (n_partitions % D != 0)
+    return fail(nullptr, GV_ERR_INVALID_ARG, "n_partitions must be a multiple of the rank count");
+  if (alpha && (alpha->kind != GV_LR_CONSTANT && alpha->kind != GV_LR_LINEAR))
+    return fail(nullptr, GV_ERR_INVALID_ARG, "bad lr schedule kind");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(nullptr, GV_ERR_CUDA, "no CUDA device");
+  if (o.device < 0 || o.device >= ndev) return fail(nullptr, GV_ERR_INVALID_ARG, "bad device");
+  if (cudaSetDevice(o.device) != cudaSuccess) return fail(nullptr, GV_ERR_CUDA, "cudaSetDevice failed");
+  c = new gv_ctx();
+  c->nv = num_nodes;
+  c->dim = dim;
+  c->n = n_partitions;
+  c->K = num_negatives;
+  c->lr0 = lr0;
+  if (alpha) c->alpha = *alpha;
+  c->opt = o;
+  c->D = D;
+  c->local = o.virtual_ranks;
+  c->m = n_partitions / D;
+  c->stride = (dim + 3) / 4 * 4;
+  c->threads = o.host_threads > 0 ? o.host_threads : gv::default_threads();
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, o.device);
+  c->ranks.resize(c->local);
+  for (int v = 0; v < c->local; ++v) c->ranks[v].d = (o.world_size > 1) ? o.rank : v;
+  *out = c;
+  return GV_OK;
+}
+
+gv_status gv_comm_unique_id(uint8_t id_out[128]) {
+  gv_ctx* c = nullptr;
+  if (!nccl().ok) return fail(nullptr, GV_ERR_COMM, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  NK(nccl().GetUniqueId(&id));
+  std::memcpy(id_out, id.internal, 128);
+  return GV_OK;
+}
+
+gv_status gv_comm_init(gv_ctx* c, const uint8_t id[128]) {
+  if (gv_status s = check_ctx(c, false)) return s;
+  if (c->opt.world_size <= 1) return fail(c, GV_ERR_STATE, "gv_comm_init needs world_size > 1");
+  if (c->loaded || c->comm_ready) return fail(c, GV_ERR_STATE, "call gv_comm_init before gv_load_edges, once");
+  if (!nccl().ok) return fail(c, GV_ERR_COMM, "libnccl.so.2 not loadable");
+  CK(cudaSetDevice(c->opt.device));
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, 128);
+  NK(nccl().CommInitRank(&c->comm, c->opt.world_size, uid, c->opt.rank));
+  c->comm_ready = true;
+  return GV_OK;
+}
+
+gv_status gv_load_edges(gv_ctx* c, const uint32_t* src, const uint32_t* dst, const float* weight,
+                        uint64_t num_edges) {
+  if (gv_status s = check_ctx(c, false)) return s;
+  if (c->loaded) return fail(c, GV_ERR_STATE, "gv_load_edges called twice");
+  if (c->opt.world_size > 1 && !c->comm_ready) return fail(c, GV_ERR_STATE, "gv_comm_init first");
+  if (num_edges && (!src || !dst)) return fail(c, GV_ERR_INVALID_ARG, "null edge arrays");
+  CK(cudaSetDevice(c->opt.device));
+  std::string msg;
+  int rc = gv::build_graph(c->nv, src, dst, weight, num_edges, c->threads, &c->graph, &msg);
+  if (rc) return fail(c, static_cast<gv_status>(rc), msg);
+  rc = gv::build_partitioning(c->graph, c->n, &c->part, &msg);
+  if (rc) return fail(c, static_cast<gv_status>(rc), msg);
+  // negative tables: deg^0.75 over each partition in local order
+  c->nprob.assign(c->nv, 0);
+  c->nalias.assign(c->nv, 0);
+  std::vector<double> w(c->nv);
+  for (uint32_t k = 0; k < c->nv; ++k) w[k] = std::pow(c->graph.deg[c->part.inv_perm[k]], 0.75);
+  for (uint32_t p = 0; p < c->n; ++p) {
+    const uint64_t b = c->part.off[p];
+    rc = gv::build_alias(w.data() + b, static_cast<uint32_t>(psize(c, p)), c->nprob.data() + b,
+                         c->nalias.data() + b);
+    if (rc) return fail(c, GV_ERR_EMPTY, "context partition " + std::to_string(p) + " has zero noise mass");
+  }
+  rc = gv::build_walk_tables(c->graph, c->threads, &c->walks);
+  if (rc) return fail(c, static_cast<gv_status>(rc), "departure table has zero mass");
+  gv_status st = setup_device(c);
+  if (st) return st;
+  c->loaded = true;
+  return GV_OK;
+}
+
+static gv_status push_impl(gv_ctx* c, const uint32_t* pairs, uint64_t count, cudaMemcpyKind kind) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  if (count == 0) return GV_OK;
+  if (!pairs) return fail(c, GV_ERR_INVALID_ARG, "null pairs");
+  CK(cudaSetDevice(c->opt.device));
+  std::lock_guard<std::mutex> lk(c->mu);
+  const int k = c->pending;
+  const uint64_t have = c->raw_count[k];
+  if (c->opt.max_pool_samples && have + count > c->opt.max_pool_samples)
+    return fail(c, GV_ERR_CAPACITY, "pending pool would exceed max_pool_samples");
+  CK(cudaStreamWaitEvent(c->copy_stream, c->raw_free[k], 0));
+  if (have + count > c->raw[k].cap) {
+    // grow, keeping what was already pushed
+    DevBuf<uint2> bigger;
+    CK(bigger.ensure(std::max<uint64_t>(have + count, c->raw[k].cap + c->raw[k].cap / 2)));
+    if (have)
+      CK(cudaMemcpyAsync(bigger.p, c->raw[k].p, have * sizeof(uint2), cudaMemcpyDeviceToDevice,
+                         c->copy_stream));
+    CK(cudaStreamSynchronize(c->copy_stream));
+    c->raw[k].release();
+    c->raw[k] = bigger;
+  }
+  CK(cudaMemcpyAsync(c->raw[k].p + have, pairs, count * sizeof(uint2), kind, c->copy_stream));
+  CK(cudaEventRecord(c->raw_ready[k], c->copy_stream));
+  CK(cudaStreamSynchronize(c->copy_stream));
+  c->raw_count[k] = have + count;
+  return GV_OK;
+}
+
+gv_status gv_push_sample_pool(gv_ctx* c, const uint32_t* pairs, uint64_t count) {
+  return push_impl(c, pairs, count, cudaMemcpyHostToDevice);
+}
+
+gv_status gv_push_sample_pool_device(gv_ctx* c, const uint32_t* pairs_dev, uint64_t count) {
+  return push_impl(c, pairs_dev, count, cudaMemcpyDeviceToDevice);
+}
+
+gv_status gv_replay_pool(gv_ctx* c) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (c->state == PoolState::Prepared || c->last_active < 0 || c->raw_count[c->pending] != 0)
+    return fail(c, GV_ERR_STATE, "no trained pool to replay, or a pool is pending");
+  c->pending = c->last_active;
+  c->raw_count[c->pending] = c->last_count;
+  return GV_OK;
+}
+
+gv_status gv_prepare_episode(gv_ctx* c) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  CK(cudaSetDevice(c->opt.device));
+  return prepare(c);
+}
+
+gv_status gv_train_episode(gv_ctx* c, gv_episode_stats* out) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  CK(cudaSetDevice(c->opt.device));
+  gv_status st = prepare(c);
+  if (st) return st;
+  st = run_steps(c);
+  if (st) return st;
+  if (out) return collect_stats(c, out);
+  return GV_OK;
+}
+
+gv_status gv_synchronize(gv_ctx* c) {
+  if (gv_status s = check_ctx(c, false)) return s;
+  return sync_all(c);
+}
+
+static gv_status embeddings_io(gv_ctx* c, bool context, float* out, const float* in,
+                               uint64_t len) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  if (len != static_cast<uint64_t>(c->nv) * c->dim)
+    return fail(c, GV_ERR_INVALID_ARG, "buffer length must be num_nodes * dim");
+  if (c->state == PoolState::Prepared)
+    return fail(c, GV_ERR_STATE, "a prepared pool is pending training");
+  CK(cudaSetDevice(c->opt.device));
+  gv_status st = sync_all(c);
+  if (st) return st;
+  const uint32_t dim = c->dim, stride = c->stride, m = c->m;
+  std::vector<float> buf;
+  for (auto& r : c->ranks) {
+    // list of (device base row, first new id, rows)
+    struct Span { uint64_t dev_row, id0, rows; };
+    std::vector<Span> spans;
+    float* base = context ? r.context : r.vertex;
+    if (!context) {
+      spans.push_back({0, r.vrow_first, r.vrows});
+    } else if (c->D == 1) {
+      spans.push_back({0, 0, c->nv});
+    } else {
+      for (uint32_t g = 0; g < m; ++g) {
+        const uint32_t j = r.d * m + g;
+        spans.push_back({static_cast<uint64_t>(r.slot_of[j]) * r.slot_rows, c->part.off[j], psize(c, j)});
+      }
+    }
+    for (const Span& sp : spans) {
+      buf.resize(sp.rows * stride);
+      if (out) {
+        CK(cudaMemcpy(buf.data(), base + sp.dev_row * stride, sp.rows * stride * sizeof(float),
+                      cudaMemcpyDeviceToHost));
+        for (uint64_t q = 0; q < sp.rows; ++q)
+          std::memcpy(out + static_cast<uint64_t>(c->part.inv_perm[sp.id0 + q]) * dim,
+                      buf.data() + q * stride, dim * sizeof(float));
+      } else {
+        std::fill(buf.begin(), buf.end(), 0.0f);
+        for (uint64_t q = 0; q < sp.rows; ++q)
+          std::memcpy(buf.data() + q * stride,
+                      in + static_cast<uint64_t>(c->part.inv_perm[sp.id0 + q]) * dim,
+                      dim * sizeof(float));
+        CK(cudaMemcpy(base + sp.dev_row * stride, buf.data(), sp.rows * stride * sizeof(float),
+                      cudaMemcpyHostToDevice));
+      }
+    }
+  }
+  return GV_OK;
+}
+
+gv_status gv_get_vertex_embeddings(gv_ctx* c, float* out, uint64_t len) {
+  if (!out) return fail(c, GV_ERR_INVALID_ARG, "null out");
+  return embeddings_io(c, false, out, nullptr, len);
+}
+gv_status gv_get_context_embeddings(gv_ctx* c, float* out, uint64_t len) {
+  if (!out) return fail(c, GV_ERR_INVALID_ARG, "null out");
+  return embeddings_io(c, true, out, nullptr, len);
+}
+gv_status gv_set_vertex_embeddings(gv_ctx* c, const float* in, uint64_t len) {
+  if (!in) return fail(c, GV_ERR_INVALID_ARG, "null in");
+  return embeddings_io(c, false, nullptr, in, len);
+}
+gv_status gv_set_context_embeddings(gv_ctx* c, const float* in, uint64_t len) {
+  if (!in) return fail(c, GV_ERR_INVALID_ARG, "null in");
+  return embeddings_io(c, true, nullptr, in, len);
+}
+
+gv_status gv_get_stream(gv_ctx* c, int vrank, uintptr_t* stream_out) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  if (vrank < 0 || vrank >= static_cast<int>(c->ranks.size()) || !stream_out)
+    return fail(c, GV_ERR_INVALID_ARG, "bad vrank");
+  *stream_out = reinterpret_cast<uintptr_t>(c->ranks[vrank].compute);
+  return GV_OK;
+}
+
+gv_status gv_augment(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_t threads, uint64_t count,
+                     uint64_t seed, uint32_t* out_pairs) {
+  if (gv_status st = check_ctx(c, true)) return st;
+  if (walk_len == 0 || s == 0 || s > walk_len || threads == 0)
+    return fail(c, GV_ERR_INVALID_ARG, "need walk_len > 0, 0 < s <= walk_len, threads > 0");
+  if (count && !out_pairs) return fail(c, GV_ERR_INVALID_ARG, "null out_pairs");
+  gv::augment(c->walks, walk_len, s, threads, count, seed, out_pairs);
+  return GV_OK;
+}
+
+gv_status gv_get_partition(gv_ctx* c, uint32_t* perm, uint64_t* part_off) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  if (perm) std::memcpy(perm, c->part.perm.data(), sizeof(uint32_t) * c->nv);
+  if (part_off) std::memcpy(part_off, c->part.off.data(), sizeof(uint64_t) * (c->n + 1));
+  return GV_OK;
+}
+
+gv_status gv_get_alias(gv_ctx* c, uint32_t p, uint32_t* prob, uint32_t* alias, uint64_t cap) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  if (p == UINT32_MAX) {
+    if (cap < c->nv) return fail(c, GV_ERR_CAPACITY, "cap < num_nodes");
+    std::memcpy(prob, c->walks.departure.prob.data(), sizeof(uint32_t) * c->nv);
+    std::memcpy(alias, c->walks.departure.alias.data(), sizeof(uint32_t) * c->nv);
+    return GV_OK;
+  }
+  if (p >= c->n) return fail(c, GV_ERR_INVALID_ARG, "bad partition");
+  const uint64_t b = c->part.off[p], sz = psize(c, p);
+  if (cap < sz) return fail(c, GV_ERR_CAPACITY, "cap < partition size");
+  std::memcpy(prob, c->nprob.data() + b, sizeof(uint32_t) * sz);
+  std::memcpy(alias, c->nalias.data() + b, sizeof(uint32_t) * sz);
+  return GV_OK;
+}
+
+gv_status gv_debug_get_buckets(gv_ctx* c, uint32_t* pairs_out, uint64_t cap, uint64_t* block_off) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  if (c->state != PoolState::Prepared) return fail(c, GV_ERR_STATE, "call gv_prepare_episode first");
+  CK(cudaSetDevice(c->opt.device));
+  if (gv_status s = sync_all(c)) return s;
+  const uint32_t n = c->n, m = c->m;
+  std::vector<uint64_t> off(n * n + 1, 0);
+  for (uint32_t b = 0; b < n * n; ++b) off[b + 1] = off[b] + c->global_counts[b];
+  if (block_off) std::memcpy(block_off, off.data(), sizeof(uint64_t) * off.size());
+  if (!pairs_out) return GV_OK;
+  if (cap < off.back()) return fail(c, GV_ERR_CAPACITY, "cap < pool size");
+  for (auto& r : c->ranks) {
+    const uint64_t first = off[r.d * m * n], len = r.final_off.back();
+    CK(cudaMemcpy(pairs_out + 2 * first, r.blocks.p, len * sizeof(uint2), cudaMemcpyDeviceToHost));
+  }
+  return GV_OK;
+}
+
+gv_status gv_debug_get_negatives(gv_ctx* c, uint32_t i, uint32_t j, uint32_t* out, uint64_t cap) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  if (c->state != PoolState::Prepared) return fail(c, GV_ERR_STATE, "call gv_prepare_episode first");
+  if (i >= c->n || j >= c->n) return fail(c, GV_ERR_INVALID_ARG, "bad block");
+  CK(cudaSetDevice(c->opt.device));
+  const uint32_t owner = i / c->m;
+  Rank* r = nullptr;
+  for (auto& x : c->ranks)
+    if (static_cast<uint32_t>(x.d) == owner) r = &x;
+  if (!r) return fail(c, GV_ERR_INVALID_ARG, "block row not owned by this process");
+  const uint32_t g = i - owner * c->m;
+  gv::BlockDesc d{};
+  d.sample_off = r->final_off[g * c->n + j];
+  d.count_lo = static_cast<uint32_t>(r->final_off[g * c->n + j + 1] - d.sample_off);
+  d.alias0 = static_cast<uint32_t>(c->part.off[j]);
+  d.m = static_cast<uint32_t>(psize(c, j));
+  d.ij = (i << 16) | j;
+  if (cap < static_cast<uint64_t>(d.count_lo) * c->K) return fail(c, GV_ERR_CAPACITY, "cap too small");
+  DevBuf<uint32_t> tmp;
+  CK(tmp.ensure(static_cast<size_t>(d.count_lo) * c->K));
+  CK(gv::launch_negatives(d, c->d_alias, static_cast<uint32_t>(c->pool_index),
+                          static_cast<uint32_t>(c->opt.seed), static_cast<uint32_t>(c->opt.seed >> 32),
+                          c->K, tmp.p, r->compute));
+  CK(cudaStreamSynchronize(r->compute));
+  CK(cudaMemcpy(out, tmp.p, sizeof(uint32_t) * d.count_lo * c->K, cudaMemcpyDeviceToHost));
+  tmp.release();
+  return GV_OK;
+}
+
+gv_status gv_train_explicit(gv_ctx* c, const uint32_t* u, const uint32_t* v, const uint32_t* negs,
+                            uint64_t count, float lr) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  if (c->D != 1) return fail(c, GV_ERR_STATE, "gv_train_explicit needs a single rank");
+  if (count == 0) return GV_OK;
+  CK(cudaSetDevice(c->opt.device));
+  const uint32_t K = c->K;
+  std::vector<uint32_t> vrow(count), crow(count * (K + 1));
+  for (uint64_t q = 0; q < count; ++q) {
+    if (u[q] >= c->nv || v[q] >= c->nv) return fail(c, GV_ERR_OUT_OF_RANGE, "id >= num_nodes");
+    vrow[q] = c->part.perm[u[q]];
+    crow[q * (K + 1)] = c->part.perm[v[q]];
+    for (uint32_t k = 0; k < K; ++k) {
+      if (negs[q * K + k] >= c->nv) return fail(c, GV_ERR_OUT_OF_RANGE, "negative id >= num_nodes");
+      crow[q * (K + 1) + 1 + k] = c->part.perm[negs[q * K + k]];
+    }
+  }
+  Rank& r = c->ranks[0];
+  DevBuf<uint32_t> dv, dc;
+  CK(dv.ensure(count));
+  CK(dc.ensure(crow.size()));
+  CK(cudaMemcpy(dv.p, vrow.data(), sizeof(uint32_t) * count, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dc.p, crow.data(), sizeof(uint32_t) * crow.size(), cudaMemcpyHostToDevice));
+  gv::ExplicitArgs a{dv.p, dc.p, count, r.vertex, r.context, c->stride, lr, c->opt.neg_weight};
+  CK(gv::launch_sgd_explicit(a, c->dim, c->K, r.compute));
+  CK(cudaStreamSynchronize(r.compute));
+  dv.release();
+  dc.release();
+  return GV_OK;
+}
+
+gv_status gv_device_bytes(gv_ctx* c, uint64_t* bytes) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  uint64_t b = static_cast<uint64_t>(c->nv) * (4 + 8 + 4);
+  b += c->raw[0].bytes_total() + c->raw[1].bytes_total();
+  for (auto& r : c->ranks) {
+    b += (r.vrows + r.crows) * c->stride * 4;
+    b += r.local_blocks.bytes_total() + r.recv.bytes_total() + r.blocks.bytes_total() +
+         r.scratch.bytes_total();
+  }
+  *bytes = b;
+  return GV_OK;
+}
+
+void gv_destroy(gv_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->opt.device);
+  for (auto& r : c->ranks) {
+    if (r.compute) cudaStreamSynchronize(r.compute);
+    if (r.comm) cudaStreamSynchronize(r.comm);
+  }
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  for (auto& r : c->ranks) {
+    cudaFree(r.vertex);
+    cudaFree(r.context);
+    r.local_blocks.release(); r.recv.release(); r.blocks.release(); r.scratch.release();
+    r.counts.release(); r.all_counts.release(); r.desc.release(); r.segs.release(); r.loss.release();
+    if (r.counts_host) cudaFreeHost(r.counts_host);
+    for (cudaEvent_t e : {r.ev_start, r.ev_bucket, r.ev_exch, r.ev_end, r.ev_recv_consumed,
+                          r.ev_exch_sent, r.ev_last_recv})
+      if (e) cudaEventDestroy(e);
+    for (auto* v : {&r.ev_first_done, &r.ev_recv, &r.ev_sent, &r.ev_sgd})
+      for (cudaEvent_t e : *v) cudaEventDestroy(e);
+    if (r.compute) cudaStreamDestroy(r.compute);
+    if (r.comm) cudaStreamDestroy(r.comm);
+  }
+  for (int k = 0; k < 2; ++k) {
+    c->raw[k].release();
+    if (c->raw_ready[k]) cudaEventDestroy(c->raw_ready[k]);
+    if (c->raw_free[k]) cudaEventDestroy(c->raw_free[k]);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  cudaFree(c->d_packed);
+  cudaFree(c->d_alias);
+  cudaFree(c->d_inv_perm);
+  if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
+  delete c;
+}
+
+}  // extern "C"

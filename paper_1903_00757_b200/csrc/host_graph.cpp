@@ -1,0 +1,207 @@
+// host_graph.cpp — graph preparation (ingest, degree, zig-zag, alias).
+// Semantics follow DESIGN.md readings R-INGEST, R-ZIGZAG, R-ALIAS
+// (SURVEY §8(c) steps 1-3). Written independently of oracle/.
+#include "host_graph.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <deque>
+#include <numeric>
+
+#include "../../include/gv.h"
+
+namespace gv {
+
+int default_threads() {
+  unsigned h = std::thread::hardware_concurrency();
+  return h ? static_cast<int>(h) : 1;
+}
+
+uint64_t Partitioning::max_part() const {
+  uint64_t m = 0;
+  for (uint32_t p = 0; p < n; ++p) m = std::max(m, off[p + 1] - off[p]);
+  return m;
+}
+
+// P:392 undirected; self-loops dropped; duplicates summed in input order;
+// rows sorted by neighbour id; degree summed in that order.
+int build_graph(uint32_t nv, const uint32_t* src, const uint32_t* dst, const float* w,
+                uint64_t ne, int threads, HostGraph* g, std::string* msg) {
+  if (nv == 0) return GV_ERR_INVALID_ARG;
+  for (uint64_t k = 0; k < ne; ++k) {
+    if (src[k] >= nv || dst[k] >= nv) {
+      *msg = "edge " + std::to_string(k) + " has a node id >= num_nodes";
+      return GV_ERR_OUT_OF_RANGE;
+    }
+    if (w && (!std::isfinite(w[k]) || w[k] < 0.0f)) {
+      *msg = "edge " + std::to_string(k) + " has a negative or non-finite weight";
+      return GV_ERR_INVALID_ARG;
+    }
+  }
+  // 1) row counts of the symmetrised multigraph
+  std::vector<uint64_t> cnt(static_cast<size_t>(nv) + 1, 0);
+  for (uint64_t k = 0; k < ne; ++k) {
+    if (src[k] == dst[k]) continue;
+    ++cnt[src[k] + 1];
+    ++cnt[dst[k] + 1];
+  }
+  std::partial_sum(cnt.begin(), cnt.end(), cnt.begin());
+  const uint64_t total = cnt[nv];
+  if (total == 0) {
+    *msg = "graph has no edge besides self-loops";
+    return GV_ERR_EMPTY;
+  }
+  // 2) scatter (col, input index) pairs into rows, in input order
+  struct Ent {
+    uint32_t col;
+    uint32_t pad;
+    uint64_t k;
+  };
+  std::vector<Ent> ent(total);
+  {
+    std::vector<uint64_t> fill(cnt.begin(), cnt.end() - 1);
+    for (uint64_t k = 0; k < ne; ++k) {
+      if (src[k] == dst[k]) continue;
+      ent[fill[src[k]]++] = Ent{dst[k], 0, k};
+      ent[fill[dst[k]]++] = Ent{src[k], 0, k};
+    }
+  }
+  // 3) per row: stable sort by column (input order kept among duplicates),
+  //    merge duplicates; rows are independent -> parallel
+  std::vector<uint64_t> merged(nv, 0);
+  parallel_for(nv, threads, [&](uint64_t b, uint64_t e) {
+    for (uint64_t v = b; v < e; ++v) {
+      Ent* first = ent.data() + cnt[v];
+      Ent* last = ent.data() + cnt[v + 1];
+      std::stable_sort(first, last, [](const Ent& a, const Ent& c) { return a.col < c.col; });
+      uint64_t u = 0;
+      for (Ent* it = first; it != last; ++it)
+        if (u == 0 || first[u - 1].col != it->col) ++u;
+      merged[v] = u;
+    }
+  });
+  g->nv = nv;
+  g->off.assign(static_cast<size_t>(nv) + 1, 0);
+  for (uint32_t v = 0; v < nv; ++v) g->off[v + 1] = g->off[v] + merged[v];
+  g->nbr.resize(g->off[nv]);
+  g->w.resize(g->off[nv]);
+  g->deg.assign(nv, 0.0);
+  parallel_for(nv, threads, [&](uint64_t b, uint64_t e) {
+    for (uint64_t v = b; v < e; ++v) {
+      const Ent* first = ent.data() + cnt[v];
+      const Ent* last = ent.data() + cnt[v + 1];
+      uint64_t o = g->off[v] - 1;
+      uint32_t prev = 0;
+      bool have = false;
+      for (const Ent* it = first; it != last; ++it) {
+        const double wk = w ? static_cast<double>(w[it->k]) : 1.0;
+        if (!have || it->col != prev) {
+          ++o;
+          g->nbr[o] = it->col;
+          g->w[o] = wk;
+          prev = it->col;
+          have = true;
+        } else {
+          g->w[o] += wk;
+        }
+      }
+      double s = 0.0;
+      for (uint64_t q = g->off[v]; q < g->off[v + 1]; ++q) s += g->w[q];
+      g->deg[v] = s;
+    }
+  });
+  return GV_OK;
+}
+
+// Zig-zag (R-ZIGZAG): rank nodes by (degree desc, id asc); rank r goes to
+// part r%n on even rounds r/n and n-1-r%n on odd rounds; local id = r/n.
+int build_partitioning(const HostGraph& g, uint32_t n, Partitioning* p, std::string* msg) {
+  const uint32_t nv = g.nv;
+  if (n == 0 || n > nv) {
+    *msg = "n_partitions must be in [1, num_nodes]";
+    return GV_ERR_INVALID_ARG;
+  }
+  std::vector<uint32_t> order(nv);
+  std::iota(order.begin(), order.end(), 0u);
+  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    if (g.deg[a] != g.deg[b]) return g.deg[a] > g.deg[b];
+    return a < b;
+  });
+  p->n = n;
+  p->off.assign(n + 1, 0);
+  for (uint32_t q = 0; q < n; ++q) {
+    // partition q receives ranks r with zig-zag position q: one per full round
+    // plus one in the last partial round if it reaches q
+    const uint64_t rounds = nv / n, rem = nv % n;
+    const uint64_t last_round = rounds;  // index of the partial round
+    const bool even = (last_round % 2) == 0;
+    const uint64_t pos_in_round = even ? q : n - 1 - q;
+    p->off[q + 1] = rounds + (pos_in_round < rem ? 1 : 0);
+  }
+  for (uint32_t q = 0; q < n; ++q) p->off[q + 1] += p->off[q];
+  p->perm.resize(nv);
+  p->inv_perm.resize(nv);
+  for (uint32_t r = 0; r < nv; ++r) {
+    const uint32_t round = r / n, pos = r % n;
+    const uint32_t part = (round & 1u) ? (n - 1 - pos) : pos;
+    const uint32_t nid = static_cast<uint32_t>(p->off[part] + round);
+    p->perm[order[r]] = nid;
+    p->inv_perm[nid] = order[r];
+  }
+  // packed ids: partition in the top pbits bits, local id below
+  uint32_t pbits = 0;
+  while ((1u << pbits) < n) ++pbits;
+  p->pbits = pbits;
+  const uint64_t local_limit = pbits ? (uint64_t(1) << (32 - pbits)) : (uint64_t(1) << 32);
+  if (p->max_part() > local_limit) {
+    *msg = "partition too large for the packed id range";
+    return GV_ERR_CAPACITY;
+  }
+  p->packed.resize(nv);
+  for (uint32_t q = 0; q < n; ++q)
+    for (uint64_t id = p->off[q]; id < p->off[q + 1]; ++id) {
+      const uint32_t local = static_cast<uint32_t>(id - p->off[q]);
+      p->packed[p->inv_perm[id]] = pbits ? ((q << (32 - pbits)) | local) : local;
+    }
+  return GV_OK;
+}
+
+// Integer Vose (R-ALIAS): a_i = trunc(w_i m 2^32 / W); the residual
+// m 2^32 - sum(a) goes to the first maximal a_i; FIFO worklists of
+// under-full (< 2^32) and over-full slots in index order.
+int build_alias(const double* w, uint32_t m, uint32_t* prob, uint32_t* alias) {
+  if (m == 0) return GV_ERR_EMPTY;
+  double total = 0.0;
+  for (uint32_t i = 0; i < m; ++i) total += w[i];
+  if (!(total > 0.0)) return GV_ERR_EMPTY;
+  constexpr uint64_t kOne = uint64_t(1) << 32;
+  const double scale = static_cast<double>(m) * 4294967296.0 / total;
+  std::vector<uint64_t> a(m);
+  uint64_t sum = 0;
+  uint32_t top = 0;
+  for (uint32_t i = 0; i < m; ++i) {
+    a[i] = static_cast<uint64_t>(w[i] * scale);
+    sum += a[i];
+    if (a[i] > a[top]) top = i;
+  }
+  a[top] += (static_cast<uint64_t>(m) << 32) - sum;
+  std::deque<uint32_t> under, over;
+  for (uint32_t i = 0; i < m; ++i) (a[i] < kOne ? under : over).push_back(i);
+  while (!under.empty() && !over.empty()) {
+    const uint32_t s = under.front();
+    under.pop_front();
+    const uint32_t l = over.front();
+    prob[s] = static_cast<uint32_t>(a[s]);
+    alias[s] = l;
+    a[l] -= kOne - a[s];
+    if (a[l] < kOne) {
+      over.pop_front();
+      under.push_back(l);
+    }
+  }
+  for (uint32_t s : under) prob[s] = 0xFFFFFFFFu, alias[s] = s;
+  for (uint32_t l : over) prob[l] = 0xFFFFFFFFu, alias[l] = l;
+  return GV_OK;
+}
+
+}  // namespace gv

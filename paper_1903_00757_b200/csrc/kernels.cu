@@ -1,0 +1,643 @@
+// kernels.cu — sm_100a kernels of the GraphVite hot path.
+//
+//   KB0 init_vertex        Philox init of the vertex shard (R-INIT)
+//   KB1 bucket_*           relabel + histogram + scans + stable scatter into
+//                          the n x n grid (Alg. 3 "Redistribute")
+//   KB2 sgd_hogwild        block-SGD, one warp per sample, Hogwild in-place
+//                          updates ("asynchronous SGD")
+//   KB2v sgd_ordered       the same update, one warp per block, block order
+//   KB2x sgd_explicit      caller-given negatives (hand-derived tests)
+//   KB2d negatives         dump of the negative stream of one block
+//   KC  segmented_copy     block-row exchange placement (a6)
+//
+// Data layout: embedding rows are fp32, row stride a multiple
+// of 4 floats, so lane l of a warp owns float4 columns l, l+32, ... of a row
+// (128-bit coalesced accesses; a 512 B row at d = 128 is one warp load).
+// Rows are read and written with ld/st.global.cg (L2 only): under Hogwild
+// every SM sees the L2-coherent value of a hot row instead of a stale L1 copy.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "philox.cuh"
+
+namespace gv {
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+template <int CH>
+struct Row {
+  float4 v[CH];
+};
+
+template <int CH>
+__device__ __forceinline__ void load_row(Row<CH>& r, const float* base, uint32_t row,
+                                         uint32_t stride, int lane, int dim4) {
+  const float4* p = reinterpret_cast<const float4*>(base + static_cast<uint64_t>(row) * stride);
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int col = lane + 32 * c;
+    r.v[c] = (col < dim4) ? __ldcg(p + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+template <int CH>
+__device__ __forceinline__ void store_row(const Row<CH>& r, float* base, uint32_t row,
+                                          uint32_t stride, int lane, int dim4) {
+  float4* p = reinterpret_cast<float4*>(base + static_cast<uint64_t>(row) * stride);
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int col = lane + 32 * c;
+    if (col < dim4) __stcg(p + col, r.v[c]);
+  }
+}
+
+template <int CH>
+__device__ __forceinline__ float warp_dot(const Row<CH>& a, const Row<CH>& b) {
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    s = fmaf(a.v[c].x, b.v[c].x, s);
+    s = fmaf(a.v[c].y, b.v[c].y, s);
+    s = fmaf(a.v[c].z, b.v[c].z, s);
+    s = fmaf(a.v[c].w, b.v[c].w, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  return s;
+}
+
+template <int CH>
+__device__ __forceinline__ void axpy(Row<CH>& y, float g, const Row<CH>& x) {
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    y.v[c].x = fmaf(g, x.v[c].x, y.v[c].x);
+    y.v[c].y = fmaf(g, x.v[c].y, y.v[c].y);
+    y.v[c].z = fmaf(g, x.v[c].z, y.v[c].z);
+    y.v[c].w = fmaf(g, x.v[c].w, y.v[c].w);
+  }
+}
+
+// -log sigmoid(z) without overflow.
+__device__ __forceinline__ float softplus_neg(float z) {
+  return fmaxf(-z, 0.f) + log1pf(expf(-fabsf(z)));
+}
+
+// Process up to 32 samples whose ids sit one per lane (lane s holds sample s):
+// my_u = vertex row, my_c[0] = positive context row, my_c[1..K] = negative rows.
+// For each sample, in order (LINE convention):
+//   for target t in [v, n_1..n_K]: x = U.C_t; p = s(x);
+//     g = (y_t - p) lr w_t; err += g C_t; C_t += g U
+//   U += err
+// The rows of sample s+1 are loaded before sample s is computed; rows that
+// sample s updates are forwarded in registers (warp-uniform id compares), so
+// the result equals strictly sequential processing of the 32 samples.
+template <int K, int CH>
+__device__ __forceinline__ float run_chunk(int nvalid, uint32_t my_u, const uint32_t* my_c,
+                                           float* __restrict__ vertex,
+                                           float* __restrict__ context, uint32_t stride,
+                                           int dim4, float lr, float neg_weight, int lane) {
+  float loss = 0.f;
+  Row<CH> U, C[K + 1];
+  uint32_t u = __shfl_sync(kFull, my_u, 0);
+  uint32_t c[K + 1];
+#pragma unroll
+  for (int t = 0; t <= K; ++t) c[t] = __shfl_sync(kFull, my_c[t], 0);
+  load_row<CH>(U, vertex, u, stride, lane, dim4);
+#pragma unroll
+  for (int t = 0; t <= K; ++t) load_row<CH>(C[t], context, c[t], stride, lane, dim4);
+
+  for (int s = 0; s < nvalid; ++s) {
+    const bool has_next = (s + 1) < nvalid;
+    uint32_t un = 0, cn[K + 1];
+    Row<CH> Un, Cn[K + 1];
+    if (has_next) {  // prefetch the next sample's rows (warp-uniform branch)
+      un = __shfl_sync(kFull, my_u, s + 1);
+#pragma unroll
+      for (int t = 0; t <= K; ++t) cn[t] = __shfl_sync(kFull, my_c[t], s + 1);
+      load_row<CH>(Un, vertex, un, stride, lane, dim4);
+#pragma unroll
+      for (int t = 0; t <= K; ++t) load_row<CH>(Cn[t], context, cn[t], stride, lane, dim4);
+    }
+    Row<CH> err;
+#pragma unroll
+    for (int q = 0; q < CH; ++q) err.v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int t = 0; t <= K; ++t) {
+      // a target equal to an earlier target of this sample sees its update
+#pragma unroll
+      for (int tp = 0; tp < t; ++tp)
+        if (c[t] == c[tp]) C[t] = C[tp];
+      const float x = warp_dot<CH>(U, C[t]);
+      const float p = 1.0f / (1.0f + expf(-x));
+      const float y = (t == 0) ? 1.0f : 0.0f;
+      const float w = (t == 0) ? 1.0f : neg_weight;
+      const float g = (y - p) * lr * w;
+      axpy<CH>(err, g, C[t]);
+      axpy<CH>(C[t], g, U);
+      loss += softplus_neg(t == 0 ? x : -x);
+    }
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      U.v[q].x += err.v[q].x;
+      U.v[q].y += err.v[q].y;
+      U.v[q].z += err.v[q].z;
+      U.v[q].w += err.v[q].w;
+    }
+    store_row<CH>(U, vertex, u, stride, lane, dim4);
+#pragma unroll
+    for (int t = 0; t <= K; ++t) store_row<CH>(C[t], context, c[t], stride, lane, dim4);
+    if (has_next) {
+      if (un == u) Un = U;
+#pragma unroll
+      for (int t = 0; t <= K; ++t) {
+#pragma unroll
+        for (int tp = 0; tp <= K; ++tp)
+          if (cn[t] == c[tp]) Cn[t] = C[tp];  // last match = final value
+      }
+      U = Un;
+      u = un;
+#pragma unroll
+      for (int t = 0; t <= K; ++t) {
+        C[t] = Cn[t];
+        c[t] = cn[t];
+      }
+    }
+  }
+  return loss;
+}
+
+// Per-lane ids of sample `qg` of a launch stream: block lookup, sample load,
+// K negatives by Philox + alias (P:231 negatives from partition j only).
+template <int K>
+__device__ __forceinline__ void sample_ids(const SgdArgs& a, uint64_t qg, uint32_t& my_u,
+                                           uint32_t* my_c) {
+  int lo = 0, hi = a.nblk - 1;  // last desc with prefix <= qg
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(&a.desc[mid].prefix) <= qg) lo = mid; else hi = mid - 1;
+  }
+  const BlockDesc* d = a.desc + lo;
+  const uint32_t q = static_cast<uint32_t>(qg - __ldg(&d->prefix));
+  const uint2 smp = __ldcs(a.samples + __ldg(&d->sample_off) + q);
+  const uint32_t crow0 = __ldg(&d->crow0), m = __ldg(&d->m), alias0 = __ldg(&d->alias0);
+  const uint32_t ij = __ldg(&d->ij);
+  my_u = __ldg(&d->vrow0) + smp.x;
+  my_c[0] = crow0 + smp.y;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const u32x4 r = philox4x32_10(u32x4{q, ij, a.pool_index, static_cast<uint32_t>(k)}, a.key0,
+                                  a.key1);
+    const uint32_t slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, m);
+    const uint2 pa = __ldg(a.alias + alias0 + slot);
+    my_c[1 + k] = crow0 + alias_pick(pa.x, pa.y, slot, r.z);
+  }
+}
+
+__device__ __forceinline__ void add_loss(double* acc, float loss, int lane) {
+  if (acc != nullptr && lane == 0) atomicAdd(acc, static_cast<double>(loss));
+}
+
+template <int K, int CH>
+__global__ void __launch_bounds__(256) sgd_hogwild_kernel(const SgdArgs a, int dim4) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t nchunks = (a.total + 31) >> 5;
+  float loss = 0.f;
+  for (uint64_t ch = warp; ch < nchunks; ch += nwarps) {
+    const uint64_t base = ch << 5;
+    const int nvalid = static_cast<int>(umin64(32, a.total - base));
+    uint32_t my_u = 0, my_c[K + 1] = {};
+    if (lane < nvalid) sample_ids<K>(a, base + lane, my_u, my_c);
+    loss += run_chunk<K, CH>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4, a.lr,
+                             a.neg_weight, lane);
+  }
+  add_loss(a.loss_acc, loss, lane);
+}
+
+// Ordered verification mode: warp b owns descriptor b and walks its block
+// in order, 32 samples at a time.
+template <int K, int CH>
+__global__ void __launch_bounds__(32) sgd_ordered_kernel(const SgdArgs a, int dim4) {
+  const int lane = threadIdx.x & 31;
+  const BlockDesc* d = a.desc + blockIdx.x;
+  const uint64_t begin = d->prefix, count = d->count_lo;
+  float loss = 0.f;
+  for (uint64_t off = 0; off < count; off += 32) {
+    const int nvalid = static_cast<int>(umin64(32, count - off));
+    uint32_t my_u = 0, my_c[K + 1] = {};
+    if (lane < nvalid) sample_ids<K>(a, begin + off + lane, my_u, my_c);
+    loss += run_chunk<K, CH>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4, a.lr,
+                             a.neg_weight, lane);
+  }
+  add_loss(a.loss_acc, loss, lane);
+}
+
+template <int K, int CH>
+__global__ void __launch_bounds__(32) sgd_explicit_kernel(const ExplicitArgs a, int dim4) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t off = 0; off < a.count; off += 32) {
+    const int nvalid = static_cast<int>(umin64(32, a.count - off));
+    uint32_t my_u = 0, my_c[K + 1] = {};
+    if (lane < nvalid) {
+      my_u = a.vrow[off + lane];
+#pragma unroll
+      for (int t = 0; t <= K; ++t) my_c[t] = a.crow[(off + lane) * (K + 1) + t];
+    }
+    run_chunk<K, CH>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4, a.lr,
+                     a.neg_weight, lane);
+  }
+}
+
+__global__ void negatives_kernel(const BlockDesc d, const uint2* __restrict__ alias,
+                                 uint32_t pool_index, uint32_t key0, uint32_t key1, int K,
+                                 uint32_t* __restrict__ out) {
+  const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= d.count_lo) return;
+  for (int k = 0; k < K; ++k) {
+    const u32x4 r = philox4x32_10(
+        u32x4{static_cast<uint32_t>(q), d.ij, pool_index, static_cast<uint32_t>(k)}, key0, key1);
+    const uint32_t slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, d.m);
+    const uint2 pa = alias[d.alias0 + slot];
+    out[q * K + k] = alias_pick(pa.x, pa.y, slot, r.z);
+  }
+}
+
+__global__ void init_vertex_kernel(float* __restrict__ vertex, uint32_t stride, uint32_t dim,
+                                   uint64_t row0, uint64_t rows,
+                                   const uint32_t* __restrict__ inv_perm, uint32_t key0,
+                                   uint32_t key1) {
+  const uint32_t q4 = dim / 4;
+  const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= rows * q4) return;
+  const uint64_t row = idx / q4;
+  const uint32_t c = static_cast<uint32_t>(idx % q4);
+  const uint32_t orig = inv_perm[row0 + row];
+  const u32x4 r = philox4x32_10(u32x4{orig, c, 0u, kTagInit}, key0, key1);
+  const float fd = static_cast<float>(dim);
+  float4 v;
+  v.x = __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(r.x >> 8), 0x1p-24f), 0.5f), fd);
+  v.y = __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(r.y >> 8), 0x1p-24f), 0.5f), fd);
+  v.z = __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(r.z >> 8), 0x1p-24f), 0.5f), fd);
+  v.w = __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(r.w >> 8), 0x1p-24f), 0.5f), fd);
+  reinterpret_cast<float4*>(vertex + row * stride)[c] = v;
+}
+
+// ---------------------------------------------------------------- bucketing
+
+struct BinCtx {
+  const uint32_t* packed;
+  uint32_t nv, pbits, n;
+};
+
+// bin of a sample and its local ids; out-of-range ids raise *err and map to bin 0.
+__device__ __forceinline__ uint32_t bin_of(const BinCtx& b, uint2 p, uint2& local,
+                                           uint32_t* err) {
+  if (p.x >= b.nv || p.y >= b.nv) {
+    *err = 1u;
+    local = make_uint2(0, 0);
+    return 0;
+  }
+  const uint32_t a = __ldg(b.packed + p.x), c = __ldg(b.packed + p.y);
+  if (b.pbits == 0) {
+    local = make_uint2(a, c);
+    return 0;
+  }
+  const uint32_t sh = 32 - b.pbits, mask = (1u << sh) - 1u;
+  local = make_uint2(a & mask, c & mask);
+  return (a >> sh) * b.n + (c >> sh);
+}
+
+__global__ void relabel_kernel(const uint2* __restrict__ in, uint64_t count, BinCtx b,
+                               uint2* __restrict__ out, uint64_t* block_off, uint32_t* err) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += stride) {
+    uint2 loc;
+    bin_of(b, __ldcs(in + i), loc, err);
+    __stcs(out + i, loc);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    block_off[0] = 0;
+    block_off[1] = count;
+  }
+}
+
+__global__ void bucket_hist_kernel(const uint2* __restrict__ in, uint64_t count, BinCtx b,
+                                   uint32_t bins, uint32_t tile, uint64_t tiles,
+                                   uint32_t* __restrict__ cnt, uint32_t* err) {
+  extern __shared__ uint32_t hist[];
+  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (uint32_t q = threadIdx.x; q < bins; q += blockDim.x) hist[q] = 0;
+    __syncthreads();
+    const uint64_t beg = t * tile, end = umin64(count, beg + tile);
+    for (uint64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+      uint2 loc;
+      atomicAdd(&hist[bin_of(b, __ldg(in + i), loc, err)], 1u);
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < bins; q += blockDim.x) cnt[q * tiles + t] = hist[q];
+    __syncthreads();
+  }
+}
+
+// Exclusive scan of the per-tile counts of bin blockIdx.x (in place); the
+// bin total goes to bin_total.
+__global__ void __launch_bounds__(1024) bucket_scan_bins_kernel(uint32_t* cnt, uint64_t tiles,
+                                                                uint64_t* bin_total) {
+  __shared__ uint64_t warp_sum[32];
+  uint32_t* a = cnt + blockIdx.x * tiles;
+  const uint64_t per = (tiles + blockDim.x - 1) / blockDim.x;
+  const uint64_t beg = umin64(tiles, threadIdx.x * per);
+  const uint64_t end = umin64(tiles, beg + per);
+  uint64_t s = 0;
+  for (uint64_t i = beg; i < end; ++i) s += a[i];
+  // block-wide exclusive scan of s
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t x = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t w = warp_sum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    warp_sum[lane] = w;  // inclusive
+  }
+  __syncthreads();
+  uint64_t run = x - s + (wid > 0 ? warp_sum[wid - 1] : 0);
+  for (uint64_t i = beg; i < end; ++i) {
+    const uint32_t v = a[i];
+    a[i] = static_cast<uint32_t>(run);  // offsets within a bin stay < 2^32 (capacity check)
+    run += v;
+  }
+  if (threadIdx.x == blockDim.x - 1) bin_total[blockIdx.x] = run;
+}
+
+__global__ void __launch_bounds__(1024) bucket_scan_totals_kernel(const uint64_t* bin_total,
+                                                                  uint32_t bins,
+                                                                  uint64_t* block_off) {
+  __shared__ uint64_t warp_sum[32];
+  const uint32_t per = (bins + blockDim.x - 1) / blockDim.x;
+  const uint32_t beg = min(bins, threadIdx.x * per), end = min(bins, beg + per);
+  uint64_t s = 0;
+  for (uint32_t i = beg; i < end; ++i) s += bin_total[i];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t x = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t w = warp_sum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    warp_sum[lane] = w;
+  }
+  __syncthreads();
+  uint64_t run = x - s + (wid > 0 ? warp_sum[wid - 1] : 0);
+  for (uint32_t i = beg; i < end; ++i) {
+    block_off[i] = run;
+    run += bin_total[i];
+  }
+  if (threadIdx.x == blockDim.x - 1) block_off[bins] = run;
+}
+
+// Stable scatter: the tile is split into 8 consecutive warp ranges; a sample's
+// slot = block_off[bin] + (tile's offset in the bin) + (count of the same bin in
+// earlier warps of the tile) + (count in earlier chunks of this warp) + (rank
+// among lower lanes of its chunk, __match_any_sync). Tile order, then warp
+// order, then lane order = pool order, so the scatter is a stable counting sort.
+__global__ void __launch_bounds__(256) bucket_scatter_kernel(
+    const uint2* __restrict__ in, uint64_t count, BinCtx b, uint32_t bins, uint32_t tile,
+    uint64_t tiles, const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ block_off,
+    uint2* __restrict__ out, uint32_t* err) {
+  extern __shared__ uint64_t smem64[];
+  uint64_t* base = smem64;                                  // bins
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(base + bins);  // 8 x bins
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const uint32_t sub = tile / 8;
+  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (uint32_t q = threadIdx.x; q < 8 * bins; q += blockDim.x) wcnt[q] = 0;
+    __syncthreads();
+    const uint64_t wbeg = t * tile + static_cast<uint64_t>(w) * sub;
+    const uint64_t wend = umin64(count, wbeg + sub);
+    for (uint64_t i0 = wbeg; i0 < wend; i0 += 32) {  // pass 1: per-warp bin counts
+      const uint64_t i = i0 + lane;
+      uint32_t bin = 0xFFFFFFFFu;
+      if (i < wend) {
+        uint2 loc;
+        bin = bin_of(b, __ldg(in + i), loc, err);
+      }
+      const uint32_t mask = __match_any_sync(kFull, bin);
+      if (bin != 0xFFFFFFFFu && (__ffs(mask) - 1) == lane) wcnt[w * bins + bin] += __popc(mask);
+      __syncwarp();
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < bins; q += blockDim.x) {
+      uint32_t run = 0;
+      for (int v = 0; v < 8; ++v) {
+        const uint32_t x = wcnt[v * bins + q];
+        wcnt[v * bins + q] = run;
+        run += x;
+      }
+      base[q] = block_off[q] + cnt[q * tiles + t];
+    }
+    __syncthreads();
+    for (uint64_t i0 = wbeg; i0 < wend; i0 += 32) {  // pass 2: place
+      const uint64_t i = i0 + lane;
+      uint32_t bin = 0xFFFFFFFFu;
+      uint2 loc = make_uint2(0, 0);
+      if (i < wend) bin = bin_of(b, __ldg(in + i), loc, err);
+      const uint32_t mask = __match_any_sync(kFull, bin);
+      const bool leader = (__ffs(mask) - 1) == lane;
+      if (bin != 0xFFFFFFFFu) {
+        const uint64_t pos = base[bin] + wcnt[w * bins + bin] + __popc(mask & lt_mask);
+        out[pos] = loc;
+      }
+      __syncwarp();
+      if (bin != 0xFFFFFFFFu && leader) wcnt[w * bins + bin] += __popc(mask);
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void segmented_copy_kernel(const uint2* __restrict__ src, uint2* __restrict__ dst,
+                                      const CopySeg* __restrict__ segs) {
+  const CopySeg s = segs[blockIdx.y];
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < s.len;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    dst[s.dst + i] = src[s.src + i];
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// ------------------------------------------------------------ dispatch table
+using HogFn = void (*)(const SgdArgs, int);
+using ExpFn = void (*)(const ExplicitArgs, int);
+
+template <int K, int CH>
+struct Inst {
+  static constexpr HogFn hog = sgd_hogwild_kernel<K, CH>;
+  static constexpr HogFn ord = sgd_ordered_kernel<K, CH>;
+  static constexpr ExpFn exp = sgd_explicit_kernel<K, CH>;
+};
+
+#define GV_ROW(K) {Inst<K, 1>::hog, Inst<K, 2>::hog, Inst<K, 3>::hog, Inst<K, 4>::hog}
+const HogFn kHog[8][4] = {GV_ROW(1), GV_ROW(2), GV_ROW(3), GV_ROW(4),
+                          GV_ROW(5), GV_ROW(6), GV_ROW(7), GV_ROW(8)};
+#undef GV_ROW
+#define GV_ROW(K) {Inst<K, 1>::ord, Inst<K, 2>::ord, Inst<K, 3>::ord, Inst<K, 4>::ord}
+const HogFn kOrd[8][4] = {GV_ROW(1), GV_ROW(2), GV_ROW(3), GV_ROW(4),
+                          GV_ROW(5), GV_ROW(6), GV_ROW(7), GV_ROW(8)};
+#undef GV_ROW
+#define GV_ROW(K) {Inst<K, 1>::exp, Inst<K, 2>::exp, Inst<K, 3>::exp, Inst<K, 4>::exp}
+const ExpFn kExp[8][4] = {GV_ROW(1), GV_ROW(2), GV_ROW(3), GV_ROW(4),
+                          GV_ROW(5), GV_ROW(6), GV_ROW(7), GV_ROW(8)};
+#undef GV_ROW
+
+int ch_of(int dim) { return (dim / 4 + 31) / 32; }
+
+}  // namespace
+
+int sgd_supported(int dim, int K) {
+  return dim > 0 && dim % 4 == 0 && dim <= 512 && K >= 1 && K <= 8;
+}
+
+cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaStream_t s) {
+  if (a.total == 0 || a.nblk == 0) return cudaSuccess;
+  HogFn f = kHog[K - 1][ch_of(dim) - 1];
+  static int occ[8][4] = {};
+  int& o = occ[K - 1][ch_of(dim) - 1];
+  if (o == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, 256, 0);
+    if (e != cudaSuccess || o <= 0) o = 1;
+  }
+  const uint64_t chunks = (a.total + 31) / 32;
+  uint64_t grid = static_cast<uint64_t>(sms > 0 ? sms : num_sms()) * o;
+  grid = umin64(grid, (chunks + 7) / 8);
+  f<<<static_cast<unsigned>(grid), 256, 0, s>>>(a, dim / 4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sgd_ordered(const SgdArgs& a, int dim, int K, cudaStream_t s) {
+  if (a.nblk == 0) return cudaSuccess;
+  kOrd[K - 1][ch_of(dim) - 1]<<<a.nblk, 32, 0, s>>>(a, dim / 4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sgd_explicit(const ExplicitArgs& a, int dim, int K, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  kExp[K - 1][ch_of(dim) - 1]<<<1, 32, 0, s>>>(a, dim / 4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_negatives(const BlockDesc& d, const uint2* alias, uint32_t pool_index,
+                             uint32_t key0, uint32_t key1, int K, uint32_t* out,
+                             cudaStream_t s) {
+  if (d.count_lo == 0) return cudaSuccess;
+  const unsigned grid = (d.count_lo + 255) / 256;
+  negatives_kernel<<<grid, 256, 0, s>>>(d, alias, pool_index, key0, key1, K, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_vertex(float* vertex, uint32_t stride, uint32_t dim, uint64_t row0,
+                               uint64_t rows, const uint32_t* inv_perm, uint32_t key0,
+                               uint32_t key1, cudaStream_t s) {
+  const uint64_t n = rows * (dim / 4);
+  if (n == 0) return cudaSuccess;
+  init_vertex_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+      vertex, stride, dim, row0, rows, inv_perm, key0, key1);
+  return cudaGetLastError();
+}
+
+BucketPlan make_bucket_plan(uint32_t n, uint64_t count) {
+  BucketPlan p;
+  p.n = n;
+  p.bins = n * n;
+  uint32_t tile = std::max<uint32_t>(2048, 16 * p.bins);
+  tile = (tile + 255) / 256 * 256;
+  p.tile = tile;
+  p.tiles = (count + tile - 1) / tile;
+  return p;
+}
+
+size_t bucket_scratch_bytes(const BucketPlan& p) {
+  const size_t cnt = static_cast<size_t>(p.bins) * std::max<uint64_t>(p.tiles, 1) * 4;
+  return (cnt + 255) / 256 * 256 + static_cast<size_t>(p.bins) * 8;
+}
+
+cudaError_t launch_bucket(const uint2* in, uint64_t count, const uint32_t* packed, uint32_t nv,
+                          uint32_t pbits, const BucketPlan& plan, void* scratch, uint2* out,
+                          uint64_t* block_off, uint32_t* err, cudaStream_t s, int* launches) {
+  BinCtx b{packed, nv, pbits, plan.n};
+  const int sms = num_sms();
+  if (plan.n == 1) {
+    uint64_t grid = umin64((count + 255) / 256, static_cast<uint64_t>(sms) * 8);
+    if (grid == 0) grid = 1;
+    relabel_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(in, count, b, out, block_off, err);
+    if (launches) *launches += 1;
+    return cudaGetLastError();
+  }
+  uint32_t* cnt = static_cast<uint32_t*>(scratch);
+  const size_t cnt_bytes = static_cast<size_t>(plan.bins) * std::max<uint64_t>(plan.tiles, 1) * 4;
+  uint64_t* bin_total =
+      reinterpret_cast<uint64_t*>(static_cast<char*>(scratch) + (cnt_bytes + 255) / 256 * 256);
+  if (plan.tiles == 0) {
+    cudaMemsetAsync(block_off, 0, (plan.bins + 1) * sizeof(uint64_t), s);
+    return cudaGetLastError();
+  }
+  const unsigned grid =
+      static_cast<unsigned>(umin64(plan.tiles, static_cast<uint64_t>(sms) * 4));
+  bucket_hist_kernel<<<grid, 256, plan.bins * 4, s>>>(in, count, b, plan.bins, plan.tile,
+                                                      plan.tiles, cnt, err);
+  bucket_scan_bins_kernel<<<plan.bins, 1024, 0, s>>>(cnt, plan.tiles, bin_total);
+  bucket_scan_totals_kernel<<<1, 1024, 0, s>>>(bin_total, plan.bins, block_off);
+  const size_t smem = static_cast<size_t>(plan.bins) * (8 + 8 * 4);
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    smem_set = smem;
+  }
+  bucket_scatter_kernel<<<grid, 256, smem, s>>>(in, count, b, plan.bins, plan.tile, plan.tiles,
+                                                cnt, block_off, out, err);
+  if (launches) *launches += 4;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_segmented_copy(const uint2* src, uint2* dst, const CopySeg* segs, int nseg,
+                                  cudaStream_t s) {
+  if (nseg == 0) return cudaSuccess;
+  dim3 grid(64, static_cast<unsigned>(nseg));
+  segmented_copy_kernel<<<grid, 256, 0, s>>>(src, dst, segs);
+  return cudaGetLastError();
+}
+
+}  // namespace gv

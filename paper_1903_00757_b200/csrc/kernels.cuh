@@ -1,0 +1,90 @@
+// kernels.cuh — launchers of the sm_100a kernels of the hot path.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gv {
+
+// One block (i, j) of an offset step as seen by one rank.
+struct BlockDesc {
+  uint64_t sample_off;  // first sample of the block in the rank's block buffer
+  uint64_t prefix;      // first index of the block in the launch's sample stream
+  uint32_t count_lo;    // block size (< 2^32, GV_ERR_CAPACITY otherwise)
+  uint32_t vrow0;       // row of local vertex id 0 of partition i in the rank's vertex shard
+  uint32_t crow0;       // row of local context id 0 of partition j in the rank's context store
+  uint32_t alias0;      // first entry of partition j's alias table
+  uint32_t m;           // size of context partition j
+  uint32_t ij;          // (i << 16) | j  -- Philox counter word 1
+};
+
+struct SgdArgs {
+  const uint2* samples;   // block buffer (u_local, v_local)
+  const BlockDesc* desc;  // nblk descriptors, prefix ascending
+  int nblk;
+  uint64_t total;         // samples in this launch
+  float* vertex;
+  float* context;
+  const uint2* alias;     // {prob, alias} per relabelled node
+  uint32_t stride;        // row stride in floats (multiple of 4)
+  float lr;
+  float neg_weight;
+  uint32_t pool_index;    // e
+  uint32_t key0, key1;    // negative-stream Philox key
+  double* loss_acc;       // nullable
+};
+
+struct ExplicitArgs {
+  const uint32_t* vrow;   // per sample: vertex row
+  const uint32_t* crow;   // per sample: [v, n_1..n_K] context rows ((K+1) per sample)
+  uint64_t count;
+  float* vertex;
+  float* context;
+  uint32_t stride;
+  float lr;
+  float neg_weight;
+};
+
+int sgd_supported(int dim, int K);  // 1 if a kernel instance exists
+
+// Hogwild block-SGD over all blocks of `a` (persistent grid).
+cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int num_sms, cudaStream_t s);
+// Ordered verification: one warp per descriptor, samples in block order.
+cudaError_t launch_sgd_ordered(const SgdArgs& a, int dim, int K, cudaStream_t s);
+// Ordered explicit-negative updates (hand-derived tests): one warp.
+cudaError_t launch_sgd_explicit(const ExplicitArgs& a, int dim, int K, cudaStream_t s);
+// Negative stream of one block: out[q*K + k] (local ids in partition j).
+cudaError_t launch_negatives(const BlockDesc& d, const uint2* alias, uint32_t pool_index,
+                             uint32_t key0, uint32_t key1, int K, uint32_t* out, cudaStream_t s);
+
+// Vertex init (R-INIT): rows [row0, row0+rows) of the relabelled order.
+cudaError_t launch_init_vertex(float* vertex, uint32_t stride, uint32_t dim, uint64_t row0,
+                               uint64_t rows, const uint32_t* inv_perm, uint32_t key0,
+                               uint32_t key1, cudaStream_t s);
+
+// ---- bucketing ----
+struct BucketPlan {
+  uint32_t n;         // partitions
+  uint32_t bins;      // n*n
+  uint32_t tile;      // samples per tile
+  uint64_t tiles;     // ceil(P / tile)
+};
+BucketPlan make_bucket_plan(uint32_t n, uint64_t count);
+size_t bucket_scratch_bytes(const BucketPlan& p);  // tile counts + bin totals
+
+// Full pipeline: range check + relabel + histogram + scans + stable scatter.
+// in: (u, v) ORIGINAL ids; packed[orig] = (part << (32-pbits)) | local.
+// out: local ids in bin-major order; block_off_dev[bins+1] (uint64);
+// err_dev: set to 1 if an id >= nv is met (contents of out undefined then).
+cudaError_t launch_bucket(const uint2* in, uint64_t count, const uint32_t* packed,
+                          uint32_t nv, uint32_t pbits, const BucketPlan& plan, void* scratch,
+                          uint2* out, uint64_t* block_off_dev, uint32_t* err_dev,
+                          cudaStream_t s, int* launches);
+
+// Segmented copy (block-row exchange, a6): copy[k] moves len samples.
+struct CopySeg {
+  uint64_t src, dst, len;
+};
+cudaError_t launch_segmented_copy(const uint2* src, uint2* dst, const CopySeg* segs, int nseg,
+                                  cudaStream_t s);
+
+}  // namespace gv

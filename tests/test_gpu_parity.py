@@ -1,0 +1,229 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle on
+the same seeded inputs (synth/). Bars (BASELINE.json north_star):
+bit-exact for partitions, alias tables, init, buckets, negative streams and
+augmentation; <= 1e-5 relative Frobenius per matrix in ordered mode; Hogwild
+link-prediction AUC within 0.01 of the oracle's."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+from paper_1903_00757_b200 import gv as G  # noqa: E402  (fails loudly if libgv.so is missing)
+
+
+def _graph(nv=2000, ne=10_000, seed=1, wmax=None):
+    return synth.chung_lu(nv, ne, gamma=2.1, wmax=wmax or nv / 10, seed=seed)
+
+
+def _pair(nv, src, dst, d=16, n=1, K=1, lr0=0.025, total=0, lr_kind=1, vranks=1, ordered=1,
+          seed=5, init_seed=4, neg_weight=5.0):
+    """(product, oracle) trainers over the same graph and hyper-parameters."""
+    p = G.GraphVite(nv, d, n, K, lr0, total_samples=total, lr_kind=lr_kind, seed=seed,
+                    init_seed=init_seed, neg_weight=neg_weight, virtual_ranks=vranks,
+                    ordered=ordered)
+    p.load_edges(src, dst)
+    o = O.Trainer(nv, d, n, K=K, lr0=lr0, lr_kind=lr_kind, total_samples=total, seed=seed,
+                  init_seed=init_seed, neg_weight=neg_weight)
+    o.load_edges(src, dst)
+    return p, o
+
+
+def _rel(a, b):
+    return np.linalg.norm(a.astype(np.float64) - b) / max(np.linalg.norm(b.astype(np.float64)), 1e-30)
+
+
+@pytest.mark.parametrize("n", [1, 3, 8])
+def test_partition_alias_init_bitexact(n):
+    src, dst = _graph()
+    p, o = _pair(2000, src, dst, d=16, n=n)
+    perm_p, off_p = p.partition()
+    perm_o, off_o = o.partition()
+    assert np.array_equal(perm_p, perm_o) and np.array_equal(off_p, off_o)
+    for q in range(n):
+        prob_p, al_p = G.gv_get_alias(p.ctx, q, int(off_p[q + 1] - off_p[q]))
+        prob_o, al_o = o.alias(q)
+        assert np.array_equal(prob_p, prob_o) and np.array_equal(al_p, al_o)
+    assert np.array_equal(p.vertex(), o.get("vertex"))  # Philox init, bit-exact
+    assert not p.context().any()
+
+
+@pytest.mark.parametrize("n,vr,count", [(1, 1, 0), (1, 1, 1), (1, 1, 100_003), (2, 1, 77_777),
+                                        (4, 1, 4096 * 3 + 5), (8, 1, 250_001), (5, 1, 31),
+                                        (4, 2, 100_001), (8, 4, 123_457), (8, 8, 64_000)])
+def test_bucketing_bitexact(n, vr, count):
+    """a3-a6: blocks (after the block-row exchange for vr > 1) equal the
+    oracle's stable counting sort, byte for byte, ragged tails included."""
+    src, dst = _graph()
+    p, o = _pair(2000, src, dst, d=8, n=n, vranks=vr)
+    pool = synth.edge_pool(src, dst, count, seed=count + 11)
+    if count == 0:
+        with pytest.raises(G.GVError):
+            G.gv_prepare_episode(p.ctx)
+        return
+    p.push(pool)
+    G.gv_prepare_episode(p.ctx)
+    got, boff = G.gv_debug_get_buckets(p.ctx, n, count)
+    perm, off = o.partition()
+    exp, eoff = O.bucket(pool, 2000, perm, off, n)
+    assert np.array_equal(boff, eoff)
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("n,vr", [(1, 1), (4, 1), (4, 4)])
+def test_negative_stream_bitexact(n, vr):
+    src, dst = _graph()
+    p, o = _pair(2000, src, dst, d=8, n=n, K=3, vranks=vr)
+    pool = synth.edge_pool(src, dst, 50_000, seed=3)
+    for e in range(2):
+        p.push(pool)
+        G.gv_prepare_episode(p.ctx)
+        _, boff = G.gv_debug_get_buckets(p.ctx, n, len(pool))
+        for i in range(n):
+            for j in range(n):
+                cnt = int(boff[i * n + j + 1] - boff[i * n + j])
+                got = G.gv_debug_get_negatives(p.ctx, i, j, cnt, 3)
+                assert np.array_equal(got, o.negatives(cnt, i, j, e)), (i, j, e)
+        p.train_episode()  # advances the pool counter e
+
+
+def test_out_of_range_rejected_before_any_update():
+    src, dst = _graph()
+    p, _ = _pair(2000, src, dst, d=8, n=4)
+    v0 = p.vertex()
+    bad = synth.edge_pool(src, dst, 1000, seed=1)
+    bad[500, 1] = 2000
+    p.push(bad)
+    with pytest.raises(G.GVError) as ei:
+        p.train_episode()
+    assert ei.value.status == G.GV_ERR_OUT_OF_RANGE
+    assert np.array_equal(p.vertex(), v0) and not p.context().any()
+
+
+def test_explicit_hand_derived_example(golden):
+    """tests/golden/sgd_4node.json on the device, d=4 with the
+    example's 2 coordinates padded by zeros (zeros change no dot product)."""
+    ex = golden("sgd_4node.json")
+    g = ex["graph"]
+    p = G.GraphVite(4, 4, 1, 1, ex["lr"], lr_kind=0, neg_weight=ex["neg_weight"])
+    p.load_edges(g["src"], g["dst"])
+    V = np.zeros((4, 4), np.float32)
+    Cm = np.zeros((4, 4), np.float32)
+    V[0, :2] = ex["U0"]
+    Cm[1, :2] = ex["C1"]
+    Cm[2, :2] = ex["C2"]
+    p.set_vertex(V)
+    p.set_context(Cm)
+    G.gv_train_explicit(p.ctx, [0], [1], [[2]], ex["lr"])
+    np.testing.assert_allclose(p.vertex()[0, :2], ex["U1"], rtol=1e-6)
+    np.testing.assert_allclose(p.context()[1, :2], ex["C1_1"], rtol=1e-6)
+    np.testing.assert_allclose(p.context()[2, :2], ex["C2_1"], rtol=1e-6)
+    assert not p.vertex()[0, 2:].any()
+
+
+def test_explicit_repeated_targets_match_oracle():
+    """Negatives equal to the positive / to each other: sequential semantics."""
+    src, dst = _graph(200, 800)
+    p, o = _pair(200, src, dst, d=32, n=1, K=3, lr0=0.1, lr_kind=0)
+    rng = np.random.default_rng(0)
+    V = rng.standard_normal((200, 32)).astype(np.float32) * 0.3
+    Cm = rng.standard_normal((200, 32)).astype(np.float32) * 0.3
+    p.set_vertex(V); p.set_context(Cm); o.set("vertex", V); o.set("context", Cm)
+    u = rng.integers(0, 200, 300)
+    v = rng.integers(0, 200, 300)
+    negs = rng.integers(0, 200, (300, 3))
+    negs[::3, 0] = v[::3]
+    negs[1::3, 2] = negs[1::3, 1]
+    u[5:40] = 7  # consecutive samples sharing rows (in-warp forwarding)
+    v[5:40] = 9
+    G.gv_train_explicit(p.ctx, u, v, negs, 0.1)
+    o.explicit(u, v, negs, 0.1)
+    assert _rel(p.vertex(), o.get("vertex")) < 1e-5
+    assert _rel(p.context(), o.get("context")) < 1e-5
+
+
+C1 = synth.CONFIGS["C1"]
+
+
+@pytest.fixture(scope="module")
+def c1_graph():
+    src, dst, _ = synth.dcsbm(C1["nv"], C1["ne"], gamma=C1["gamma"], wmax=C1["wmax"], c=C1["c"],
+                              mu=C1["mu"], seed=1)
+    return src, dst
+
+
+@pytest.mark.parametrize("n,vr,pools,count", [(1, 1, 1, C1["pool"]), (1, 1, 3, 200_000),
+                                               (4, 1, 2, 400_000), (4, 2, 2, 400_000),
+                                               (8, 8, 2, 400_000), (8, 4, 1, 400_000)])
+def test_ordered_mode_matches_oracle(c1_graph, n, vr, pools, count):
+    """Ordered verification mode (one warp per block, block order) after
+    whole pools of C1 (BASELINE configs[0]): <= 1e-5 relative Frobenius per
+    matrix (reading R-TOL). vr > 1 runs the multi-rank schedule (block-row
+    exchange, context rotation) on virtual ranks."""
+    src, dst = c1_graph
+    total = pools * count
+    p, o = _pair(C1["nv"], src, dst, d=C1["d"], n=n, vranks=vr, total=total)
+    for k in range(pools):
+        pool = synth.edge_pool(src, dst, count, seed=100 + k)
+        p.push(pool)
+        st = p.train_episode()
+        lo = o.train_pool(pool)
+        assert st["samples_global"] == count
+        assert abs(st["loss_sum"] - lo) <= 1e-4 * abs(lo)
+    assert _rel(p.vertex(), o.get("vertex")) <= 1e-5
+    assert _rel(p.context(), o.get("context")) <= 1e-5
+
+
+def test_replay_advances_pool_counter(c1_graph):
+    src, dst = c1_graph
+    p, o = _pair(C1["nv"], src, dst, d=32, n=2)
+    pool = synth.edge_pool(src, dst, 100_000, seed=1)
+    p.push(pool)
+    p.train_episode()
+    o.train_pool(pool)
+    p.replay()
+    st = p.train_episode()
+    o.train_pool(pool)
+    assert st["pool_index"] == 1
+    assert _rel(p.vertex(), o.get("vertex")) <= 1e-5
+
+
+@pytest.mark.parametrize("threads,s,count", [(1, 1, 5000), (3, 2, 100_003), (16, 5, 1_000_000)])
+def test_augmentation_bitexact(c1_graph, threads, s, count):
+    """Host augmentation (Alg. 2 + pseudo shuffle) == oracle, byte for byte."""
+    src, dst = c1_graph
+    p = G.GraphVite(C1["nv"], 8, 1)
+    p.load_edges(src, dst)
+    got = p.augment(40, s, threads, count, 77)
+    sampler = O.Sampler(O.Graph(C1["nv"], src, dst))
+    assert np.array_equal(got, sampler.augment(40, s, threads, count, 77))
+
+
+def test_hogwild_auc_matches_oracle():
+    """Full Hogwild runs: link-prediction AUC within 0.01 of the
+    oracle trained on the same pools, seeds and schedule; AUC_oracle >= 0.8
+    (SURVEY §8(c) AUC parity spec, scaled to 2e7 samples)."""
+    nv, ne = 100_000, 1_000_000
+    src, dst, _ = synth.dcsbm(nv, ne, gamma=2.1, wmax=1000.0, c=50, mu=0.2, seed=1)
+    tr_s, tr_d, pos, neg = synth.linkpred_split(src, dst, nv, holdout=0.01, seed=6)
+    pools, count = 10, 2_000_000
+    res = {}
+    for n, vr in [(1, 1), (4, 4)]:
+        p = G.GraphVite(nv, 128, n, 1, 0.025, total_samples=pools * count, virtual_ranks=vr,
+                        ordered=0)
+        p.load_edges(tr_s, tr_d)
+        for k in range(pools):
+            p.push(synth.edge_pool(tr_s, tr_d, count, seed=200 + k))
+            p.train_episode(stats=False)
+        res[(n, vr)] = O.linkpred_auc(p.vertex(), pos, neg)
+        assert np.isfinite(p.vertex()).all() and np.isfinite(p.context()).all()
+    o = O.Trainer(nv, 128, 1, K=1, lr0=0.025, lr_kind=1, total_samples=pools * count)
+    o.load_edges(tr_s, tr_d)
+    for k in range(pools):
+        o.train_pool(synth.edge_pool(tr_s, tr_d, count, seed=200 + k))
+    auc_o = O.linkpred_auc(o.get("vertex"), pos, neg)
+    assert auc_o >= 0.8, auc_o
+    for key, auc in res.items():
+        assert abs(auc - auc_o) <= 0.01, (key, auc, auc_o)
