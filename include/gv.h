@@ -281,6 +281,26 @@ gv_status gv_debug_get_negatives(gv_ctx* ctx, uint32_t i, uint32_t j,
 gv_status gv_train_explicit(gv_ctx* ctx, const uint32_t* u, const uint32_t* v,
                             const uint32_t* negs, uint64_t count, float lr);
 
+/* Host-only schedule of rank d (of D) at offset step t for an n x n grid
+ * (Alg. 3 P:244-253 with "partitions > GPUs ... in subgroups", P:233;
+ * DESIGN.md §7): rank d owns vertex partitions [d*m, (d+1)*m), m = n/D,
+ * and trains blocks (vpart[g], cpart[g]) for g = 0..m-1 in this order,
+ * cpart[g] = (vpart[g] + t) mod n. After block 0 it sends context partition
+ * send_part to rank send_to; it receives recv_part from rank recv_from,
+ * which block wait_block of step t+1 needs. D == 1: no transfer
+ * (send_part = recv_part = UINT32_MAX). The engine uses exactly this plan.
+ * Errors: GV_ERR_INVALID_ARG (n == 0, n > 64, D == 0, n % D != 0, d >= D,
+ * t >= n, out == NULL). Needs no GPU. */
+typedef struct {
+  uint32_t n_blocks;
+  uint32_t vpart[64];
+  uint32_t cpart[64];
+  uint32_t send_part, send_to;
+  uint32_t recv_part, recv_from;
+  uint32_t wait_block;
+} gv_step_plan;
+gv_status gv_plan_step(uint32_t n, uint32_t D, uint32_t d, uint32_t t, gv_step_plan* out);
+
 /* Bytes of device memory allocated by this context (all virtual ranks). */
 gv_status gv_device_bytes(gv_ctx* ctx, uint64_t* bytes);
 

@@ -425,8 +425,10 @@ gv_status run_steps(gv_ctx* c) {
     int free_slot = r.free_slot;
     for (uint32_t t = 0; t < n; ++t) {
       uint64_t prefix = 0;
+      gv_step_plan plan;
+      gv_plan_step(n, c->D, r.d, t, &plan);
       for (uint32_t g = 0; g < m; ++g) {
-        const uint32_t i = r.d * m + g, j = (i + t) % n;
+        const uint32_t i = plan.vpart[g], j = plan.cpart[g];
         gv::BlockDesc& d = desc[t * m + g];
         d.sample_off = r.final_off[g * n + j];
         d.count_lo = static_cast<uint32_t>(r.final_off[g * n + j + 1] - r.final_off[g * n + j]);
@@ -439,8 +441,8 @@ gv_status run_steps(gv_ctx* c) {
         d.m = static_cast<uint32_t>(psize(c, j));
         d.ij = (i << 16) | j;
       }
-      if (c->D > 1) {  // after step t: partition (d m + t) leaves, ((d+1) m + t) arrives
-        const uint32_t out_p = (r.d * m + t) % n, in_p = ((r.d + 1) * m + t) % n;
+      if (c->D > 1) {  // after step t: send_part leaves, recv_part arrives
+        const uint32_t out_p = plan.send_part, in_p = plan.recv_part;
         const int s_out = slot_of[out_p];
         slot_of[in_p] = free_slot;
         slot_of[out_p] = -1;
@@ -470,12 +472,14 @@ gv_status run_steps(gv_ctx* c) {
       a.key0 = key0;
       a.key1 = key1;
       a.loss_acc = c->opt.compute_loss ? r.loss.p : nullptr;
+      gv_step_plan plan;
+      gv_plan_step(n, c->D, r.d, t, &plan);
       auto launch = [&](uint32_t g0, uint32_t cnt_blk) -> gv_status {
         a.desc = r.desc.p + t * m + g0;
         a.nblk = static_cast<int>(cnt_blk);
         uint64_t tot = 0;
         for (uint32_t g = g0; g < g0 + cnt_blk; ++g)
-          tot += r.final_off[g * n + (r.d * m + g + t) % n + 1] - r.final_off[g * n + (r.d * m + g + t) % n];
+          tot += r.final_off[g * n + plan.cpart[g] + 1] - r.final_off[g * n + plan.cpart[g]];
         a.total = tot;
         cudaEvent_t eb = r.ev_sgd[2 * r.sgd_launches], ee = r.ev_sgd[2 * r.sgd_launches + 1];
         CK(cudaEventRecord(eb, r.compute));
@@ -494,8 +498,8 @@ gv_status run_steps(gv_ctx* c) {
         continue;
       }
       for (uint32_t g = 0; g < m; ++g) {
-        if (g == m - 1) {
-          // the last block's context arrived by the previous rotation
+        if (g == plan.wait_block) {
+          // this block's context arrived by the previous rotation
           if (t > 0) CK(cudaStreamWaitEvent(r.compute, r.ev_recv[t - 1], 0));
           else if (r.have_last_recv) CK(cudaStreamWaitEvent(r.compute, r.ev_last_recv, 0));
         }
@@ -508,8 +512,10 @@ gv_status run_steps(gv_ctx* c) {
     // rotation of step t (a8): rank d sends partition (d m + t) to rank d-1
     if (c->opt.world_size > 1) {
       Rank& r = c->ranks[0];
-      const uint32_t out_p = (r.d * m + t) % n, in_p = ((r.d + 1) * m + t) % n;
-      const int prev = (r.d + c->D - 1) % c->D, next = (r.d + 1) % c->D;
+      gv_step_plan plan;
+      gv_plan_step(n, c->D, r.d, t, &plan);
+      const uint32_t out_p = plan.send_part, in_p = plan.recv_part;
+      const int prev = static_cast<int>(plan.send_to), next = static_cast<int>(plan.recv_from);
       CK(cudaStreamWaitEvent(r.comm, r.ev_first_done[t], 0));
       NK(nccl().GroupStart());
       NK(nccl().Send(r.context + static_cast<uint64_t>(r.slot_of[out_p]) * r.slot_rows * c->stride,
@@ -525,14 +531,15 @@ gv_status run_steps(gv_ctx* c) {
     } else {
       // device copies between virtual ranks; slot moves computed first
       std::vector<int> dst_slot(c->D), src_slot(c->D);
+      std::vector<gv_step_plan> plans(c->D);
       for (auto& r : c->ranks) {
-        const uint32_t out_p = (r.d * m + t) % n;
-        src_slot[r.d] = r.slot_of[out_p];
+        gv_plan_step(n, c->D, r.d, t, &plans[r.d]);
+        src_slot[r.d] = r.slot_of[plans[r.d].send_part];
         dst_slot[r.d] = r.free_slot;  // where rank r receives
       }
       for (auto& r : c->ranks) {
-        Rank& prev = c->ranks[(r.d + c->D - 1) % c->D];
-        const uint32_t out_p = (r.d * m + t) % n;
+        Rank& prev = c->ranks[plans[r.d].send_to];
+        const uint32_t out_p = plans[r.d].send_part;
         CK(cudaStreamWaitEvent(r.comm, r.ev_first_done[t], 0));
         // prev's free slot was released by prev's own send of step t-1
         if (t > 0) CK(cudaStreamWaitEvent(r.comm, prev.ev_sent[t - 1], 0));
@@ -545,7 +552,7 @@ gv_status run_steps(gv_ctx* c) {
         CK(cudaEventRecord(prev.ev_recv[t], r.comm));
       }
       for (auto& r : c->ranks) {
-        const uint32_t out_p = (r.d * m + t) % n, in_p = ((r.d + 1) * m + t) % n;
+        const uint32_t out_p = plans[r.d].send_part, in_p = plans[r.d].recv_part;
         r.slot_of[in_p] = dst_slot[r.d];
         r.slot_of[out_p] = -1;
         r.free_slot = src_slot[r.d];
@@ -1065,6 +1072,31 @@ gv_status gv_train_explicit(gv_ctx* c, const uint32_t* u, const uint32_t* v, con
   CK(cudaStreamSynchronize(r.compute));
   dv.release();
   dc.release();
+  return GV_OK;
+}
+
+gv_status gv_plan_step(uint32_t n, uint32_t D, uint32_t d, uint32_t t, gv_step_plan* out) {
+  gv_ctx* c = nullptr;
+  if (!out || n == 0 || n > 64 || D == 0 || n % D != 0 || d >= D || t >= n)
+    return fail(c, GV_ERR_INVALID_ARG, "gv_plan_step: bad arguments");
+  const uint32_t m = n / D;
+  std::memset(out, 0, sizeof(*out));
+  out->n_blocks = m;
+  for (uint32_t g = 0; g < m; ++g) {
+    out->vpart[g] = d * m + g;
+    out->cpart[g] = (d * m + g + t) % n;
+  }
+  if (D == 1) {
+    out->send_part = out->recv_part = UINT32_MAX;
+    out->send_to = out->recv_from = 0;
+    out->wait_block = UINT32_MAX;
+  } else {
+    out->send_part = (d * m + t) % n;        // = cpart[0]: free after block 0
+    out->send_to = (d + D - 1) % D;
+    out->recv_part = ((d + 1) * m + t) % n;  // = cpart[m-1] of step t+1
+    out->recv_from = (d + 1) % D;
+    out->wait_block = m - 1;
+  }
   return GV_OK;
 }
 

@@ -57,8 +57,28 @@ __device__ __forceinline__ void store_row(const Row<CH>& r, float* base, uint32_
   }
 }
 
+// Component-wise atomic add of a row delta at L2 (Hogwild write-back):
+// concurrent warps never overwrite each other's updates.
+__device__ __forceinline__ void red_add4(float* p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 template <int CH>
-__device__ __forceinline__ float warp_dot(const Row<CH>& a, const Row<CH>& b) {
+__device__ __forceinline__ void red_row(float* base, uint32_t row, uint32_t stride, int lane,
+                                        int dim4, float g, const Row<CH>& x) {
+  float* p = base + static_cast<uint64_t>(row) * stride;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int col = lane + 32 * c;
+    if (col < dim4)
+      red_add4(p + 4 * col, make_float4(g * x.v[c].x, g * x.v[c].y, g * x.v[c].z, g * x.v[c].w));
+  }
+}
+
+template <int CH>
+__device__ __forceinline__ float lane_dot(const Row<CH>& a, const Row<CH>& b) {
   float s = 0.f;
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
@@ -67,9 +87,27 @@ __device__ __forceinline__ float warp_dot(const Row<CH>& a, const Row<CH>& b) {
     s = fmaf(a.v[c].z, b.v[c].z, s);
     s = fmaf(a.v[c].w, b.v[c].w, s);
   }
+  return s;
+}
+
+__device__ __forceinline__ float warp_sum1(float s) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
   return s;
+}
+
+// Two warp sums with 7 shuffles instead of 10: at the first butterfly stage
+// lanes < 16 keep a and send b, lanes >= 16 keep b and send a; four more
+// stages inside each half; the sums are read from lanes 0 and 16.
+__device__ __forceinline__ void warp_sum2(float& a, float& b, int lane) {
+  const bool hi = (lane & 16) != 0;
+  float keep = hi ? b : a;
+  const float send = hi ? a : b;
+  keep += __shfl_xor_sync(kFull, send, 16);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) keep += __shfl_xor_sync(kFull, keep, o);
+  a = __shfl_sync(kFull, keep, 0);
+  b = __shfl_sync(kFull, keep, 16);
 }
 
 template <int CH>
@@ -83,9 +121,20 @@ __device__ __forceinline__ void axpy(Row<CH>& y, float g, const Row<CH>& x) {
   }
 }
 
-// -log sigmoid(z) without overflow.
-__device__ __forceinline__ float softplus_neg(float z) {
-  return fmaxf(-z, 0.f) + log1pf(expf(-fabsf(z)));
+// One target of a sample: p = s(x) = 1/(1+exp(-x)) (IEEE expf, correctly
+// rounded reciprocal), g = (y - p) lr w, err += g C, C += g U. Returns the
+// target's loss -log s(+-x) = log(1+e^-x) (+ x for a negative) when wanted.
+template <int CH>
+__device__ __forceinline__ float apply_target(float x, bool positive, float lr, float neg_weight,
+                                              const Row<CH>& U, Row<CH>& Ct, Row<CH>& err,
+                                              bool want_loss, float& g_out) {
+  const float e = expf(-x);
+  const float p = __frcp_rn(1.0f + e);
+  const float g = ((positive ? 1.0f : 0.0f) - p) * lr * (positive ? 1.0f : neg_weight);
+  g_out = g;
+  axpy<CH>(err, g, Ct);
+  axpy<CH>(Ct, g, U);
+  return want_loss ? (__logf(1.0f + e) + (positive ? 0.0f : x)) : 0.0f;
 }
 
 // Process up to 32 samples whose ids sit one per lane (lane s holds sample s):
@@ -96,12 +145,20 @@ __device__ __forceinline__ float softplus_neg(float z) {
 //   U += err
 // The rows of sample s+1 are loaded before sample s is computed; rows that
 // sample s updates are forwarded in registers (warp-uniform id compares), so
-// the result equals strictly sequential processing of the 32 samples.
-template <int K, int CH>
+// the result equals strictly sequential processing of the 32 samples. A
+// target equal to an earlier target of the same sample sees its update
+// (R-DUP): then the targets run one after the other (rare slow path);
+// otherwise all dot products are reduced together.
+// ATOMIC (Hogwild): rows are written back as deltas with red.global.add
+// (err for the vertex row, g_t U for context row t), as in Hogwild!'s
+// lock-free component-wise updates (Recht et al., "asynchronous SGD");
+// otherwise (one warp per block) the final rows are stored.
+template <int K, int CH, bool ATOMIC>
 __device__ __forceinline__ float run_chunk(int nvalid, uint32_t my_u, const uint32_t* my_c,
                                            float* __restrict__ vertex,
                                            float* __restrict__ context, uint32_t stride,
-                                           int dim4, float lr, float neg_weight, int lane) {
+                                           int dim4, float lr, float neg_weight, int lane,
+                                           bool want_loss) {
   float loss = 0.f;
   Row<CH> U, C[K + 1];
   uint32_t u = __shfl_sync(kFull, my_u, 0);
@@ -127,20 +184,32 @@ __device__ __forceinline__ float run_chunk(int nvalid, uint32_t my_u, const uint
     Row<CH> err;
 #pragma unroll
     for (int q = 0; q < CH; ++q) err.v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool dup = false;
 #pragma unroll
-    for (int t = 0; t <= K; ++t) {
-      // a target equal to an earlier target of this sample sees its update
+    for (int t = 1; t <= K; ++t)
 #pragma unroll
-      for (int tp = 0; tp < t; ++tp)
-        if (c[t] == c[tp]) C[t] = C[tp];
-      const float x = warp_dot<CH>(U, C[t]);
-      const float p = 1.0f / (1.0f + expf(-x));
-      const float y = (t == 0) ? 1.0f : 0.0f;
-      const float w = (t == 0) ? 1.0f : neg_weight;
-      const float g = (y - p) * lr * w;
-      axpy<CH>(err, g, C[t]);
-      axpy<CH>(C[t], g, U);
-      loss += softplus_neg(t == 0 ? x : -x);
+      for (int tp = 0; tp < t; ++tp) dup |= (c[t] == c[tp]);
+    float g[K + 1];
+    Row<CH> U0 = U;  // the vertex row the context deltas are taken against
+    if (!dup) {
+      float x[K + 1];
+#pragma unroll
+      for (int t = 0; t <= K; ++t) x[t] = lane_dot<CH>(U, C[t]);
+#pragma unroll
+      for (int t = 0; t + 1 <= K; t += 2) warp_sum2(x[t], x[t + 1], lane);
+      if ((K + 1) & 1) x[K] = warp_sum1(x[K]);
+#pragma unroll
+      for (int t = 0; t <= K; ++t)
+        loss += apply_target<CH>(x[t], t == 0, lr, neg_weight, U, C[t], err, want_loss, g[t]);
+    } else {
+#pragma unroll
+      for (int t = 0; t <= K; ++t) {
+#pragma unroll
+        for (int tp = 0; tp < t; ++tp)
+          if (c[t] == c[tp]) C[t] = C[tp];
+        const float x = warp_sum1(lane_dot<CH>(U, C[t]));
+        loss += apply_target<CH>(x, t == 0, lr, neg_weight, U, C[t], err, want_loss, g[t]);
+      }
     }
 #pragma unroll
     for (int q = 0; q < CH; ++q) {
@@ -149,16 +218,30 @@ __device__ __forceinline__ float run_chunk(int nvalid, uint32_t my_u, const uint
       U.v[q].z += err.v[q].z;
       U.v[q].w += err.v[q].w;
     }
-    store_row<CH>(U, vertex, u, stride, lane, dim4);
+    if (ATOMIC) {
+      red_row<CH>(vertex, u, stride, lane, dim4, 1.0f, err);
 #pragma unroll
-    for (int t = 0; t <= K; ++t) store_row<CH>(C[t], context, c[t], stride, lane, dim4);
+      for (int t = 0; t <= K; ++t) red_row<CH>(context, c[t], stride, lane, dim4, g[t], U0);
+    } else {
+      store_row<CH>(U, vertex, u, stride, lane, dim4);
+#pragma unroll
+      for (int t = 0; t <= K; ++t) store_row<CH>(C[t], context, c[t], stride, lane, dim4);
+    }
     if (has_next) {
-      if (un == u) Un = U;
+      // forwarding: rare, so decided once with a warp-uniform mask
+      bool fwd = (un == u);
 #pragma unroll
-      for (int t = 0; t <= K; ++t) {
+      for (int t = 0; t <= K; ++t)
 #pragma unroll
-        for (int tp = 0; tp <= K; ++tp)
-          if (cn[t] == c[tp]) Cn[t] = C[tp];  // last match = final value
+        for (int tp = 0; tp <= K; ++tp) fwd |= (cn[t] == c[tp]);
+      if (fwd) {
+        if (un == u) Un = U;
+#pragma unroll
+        for (int t = 0; t <= K; ++t) {
+#pragma unroll
+          for (int tp = 0; tp <= K; ++tp)
+            if (cn[t] == c[tp]) Cn[t] = C[tp];  // last match = final value
+        }
       }
       U = Un;
       u = un;
@@ -203,38 +286,50 @@ __device__ __forceinline__ void add_loss(double* acc, float loss, int lane) {
   if (acc != nullptr && lane == 0) atomicAdd(acc, static_cast<double>(loss));
 }
 
+// KB2: persistent grid; warp w takes chunks w, w + W, ... of 32 consecutive
+// samples of the launch stream. The ids of the warp's next chunk (sample
+// load, Philox, alias gather) are requested before the current chunk is
+// processed, so their latency hides behind 32 samples of work.
 template <int K, int CH>
-__global__ void __launch_bounds__(256) sgd_hogwild_kernel(const SgdArgs a, int dim4) {
+__global__ void __launch_bounds__(256)
+    sgd_hogwild_kernel(const SgdArgs a, int dim4) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   const uint64_t nchunks = (a.total + 31) >> 5;
+  const bool want_loss = a.loss_acc != nullptr;
   float loss = 0.f;
+  uint32_t cu = 0, cc[K + 1] = {};
+  if (warp < nchunks && (warp << 5) + lane < a.total) sample_ids<K>(a, (warp << 5) + lane, cu, cc);
   for (uint64_t ch = warp; ch < nchunks; ch += nwarps) {
-    const uint64_t base = ch << 5;
+    const uint64_t base = ch << 5, nx = ch + nwarps;
     const int nvalid = static_cast<int>(umin64(32, a.total - base));
-    uint32_t my_u = 0, my_c[K + 1] = {};
-    if (lane < nvalid) sample_ids<K>(a, base + lane, my_u, my_c);
-    loss += run_chunk<K, CH>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4, a.lr,
-                             a.neg_weight, lane);
+    uint32_t nu = 0, nc[K + 1] = {};
+    if (nx < nchunks && (nx << 5) + lane < a.total) sample_ids<K>(a, (nx << 5) + lane, nu, nc);
+    loss += run_chunk<K, CH, true>(nvalid, cu, cc, a.vertex, a.context, a.stride, dim4, a.lr,
+                                   a.neg_weight, lane, want_loss);
+    cu = nu;
+#pragma unroll
+    for (int t = 0; t <= K; ++t) cc[t] = nc[t];
   }
   add_loss(a.loss_acc, loss, lane);
 }
 
 // Ordered verification mode: warp b owns descriptor b and walks its block
-// in order, 32 samples at a time.
+// in order, 32 samples at a time, through the same run_chunk.
 template <int K, int CH>
 __global__ void __launch_bounds__(32) sgd_ordered_kernel(const SgdArgs a, int dim4) {
   const int lane = threadIdx.x & 31;
   const BlockDesc* d = a.desc + blockIdx.x;
   const uint64_t begin = d->prefix, count = d->count_lo;
+  const bool want_loss = a.loss_acc != nullptr;
   float loss = 0.f;
   for (uint64_t off = 0; off < count; off += 32) {
     const int nvalid = static_cast<int>(umin64(32, count - off));
     uint32_t my_u = 0, my_c[K + 1] = {};
     if (lane < nvalid) sample_ids<K>(a, begin + off + lane, my_u, my_c);
-    loss += run_chunk<K, CH>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4, a.lr,
-                             a.neg_weight, lane);
+    loss += run_chunk<K, CH, false>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4,
+                                    a.lr, a.neg_weight, lane, want_loss);
   }
   add_loss(a.loss_acc, loss, lane);
 }
@@ -250,8 +345,8 @@ __global__ void __launch_bounds__(32) sgd_explicit_kernel(const ExplicitArgs a, 
 #pragma unroll
       for (int t = 0; t <= K; ++t) my_c[t] = a.crow[(off + lane) * (K + 1) + t];
     }
-    run_chunk<K, CH>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4, a.lr,
-                     a.neg_weight, lane);
+    run_chunk<K, CH, false>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4, a.lr,
+                            a.neg_weight, lane, false);
   }
 }
 
@@ -532,16 +627,15 @@ int sgd_supported(int dim, int K) {
 
 cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaStream_t s) {
   if (a.total == 0 || a.nblk == 0) return cudaSuccess;
-  HogFn f = kHog[K - 1][ch_of(dim) - 1];
+  const int ki = K - 1, ci = ch_of(dim) - 1;
+  HogFn f = kHog[ki][ci];
   static int occ[8][4] = {};
-  int& o = occ[K - 1][ch_of(dim) - 1];
-  if (o == 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, 256, 0);
-    if (e != cudaSuccess || o <= 0) o = 1;
-  }
+  int& o = occ[ki][ci];
+  if (o == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, 256, 0) != cudaSuccess || o <= 0))
+    o = 1;
   const uint64_t chunks = (a.total + 31) / 32;
   uint64_t grid = static_cast<uint64_t>(sms > 0 ? sms : num_sms()) * o;
-  grid = umin64(grid, (chunks + 7) / 8);
+  grid = std::min<uint64_t>(grid, (chunks + 7) / 8);
   f<<<static_cast<unsigned>(grid), 256, 0, s>>>(a, dim / 4);
   return cudaGetLastError();
 }

@@ -52,6 +52,12 @@ class gv_episode_stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class gv_step_plan(C.Structure):
+    _fields_ = [("n_blocks", C.c_uint32), ("vpart", C.c_uint32 * 64), ("cpart", C.c_uint32 * 64),
+                ("send_part", C.c_uint32), ("send_to", C.c_uint32), ("recv_part", C.c_uint32),
+                ("recv_from", C.c_uint32), ("wait_block", C.c_uint32)]
+
+
 class gv_augment_cfg(C.Structure):
     _fields_ = [("walk_len", C.c_uint32), ("s", C.c_uint32), ("threads", C.c_uint32),
                 ("pool_samples", C.c_uint64), ("seed", C.c_uint64), ("collaborate", C.c_int)]
@@ -100,6 +106,7 @@ SIGNATURES = {
     "gv_debug_get_negatives": (st, [ctx_p, C.c_uint32, C.c_uint32, u32p, C.c_uint64]),
     "gv_train_explicit": (st, [ctx_p, u32p, u32p, u32p, C.c_uint64, C.c_float]),
     "gv_device_bytes": (st, [ctx_p, u64p]),
+    "gv_plan_step": (st, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(gv_step_plan)]),
     "gv_last_error": (C.c_char_p, [ctx_p]),
     "gv_status_string": (C.c_char_p, [C.c_int]),
     "gv_abi_version": (C.c_int, []),
@@ -283,6 +290,18 @@ def gv_train_explicit(ctx, u, v, negs, lr):
     v = _u32(v)
     negs = _u32(negs).reshape(-1)
     _ck(lib.gv_train_explicit(ctx, _ptr(u, u32p), _ptr(v, u32p), _ptr(negs, u32p), len(u), lr), ctx)
+
+
+def gv_plan_step(n, D, d, t):
+    """Host-only schedule of rank d at offset step t (no GPU needed)."""
+    p = gv_step_plan()
+    _ck(lib.gv_plan_step(n, D, d, t, C.byref(p)))
+    m = p.n_blocks
+    none = 0xFFFFFFFF
+    return {"blocks": [(p.vpart[g], p.cpart[g]) for g in range(m)],
+            "send_part": None if p.send_part == none else p.send_part, "send_to": p.send_to,
+            "recv_part": None if p.recv_part == none else p.recv_part, "recv_from": p.recv_from,
+            "wait_block": None if p.wait_block == none else p.wait_block}
 
 
 def gv_device_bytes(ctx):
