@@ -16,8 +16,9 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libgv.so")
+BUILD = os.path.join(PKG, "_build" + os.environ.get("GV_BUILD_TAG", ""))
+LIB = os.environ.get("GV_LIB_OUT", os.path.join(PKG, "libgv.so"))
+EXTRA = os.environ.get("GV_EXTRA_FLAGS", "").split()  # experiments, e.g. -DGV_PREFETCH=8
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -38,7 +39,7 @@ def _compile(src, force, verbose):
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(
             os.path.getmtime(path), _newest_dep()):
         return obj, ""
-    cmd = [NVCC, *ARCH, *COMMON, "-c", path, "-o", obj]
+    cmd = [NVCC, *ARCH, *COMMON, *EXTRA, "-c", path, "-o", obj]
     if verbose and src.endswith(".cu"):
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -77,6 +77,17 @@ __device__ __forceinline__ void red_row(float* base, uint32_t row, uint32_t stri
   }
 }
 
+// L2 prefetch of a row (no register, no scoreboard): lanes 0..(bytes/128)-1
+// each name one 128 B line of the row.
+__device__ __forceinline__ void prefetch_row(const float* base, uint32_t row, uint32_t stride,
+                                             int lane, int dim4) {
+  const int lines = (dim4 * 16 + 127) >> 7;
+  if (lane < lines) {
+    const float* p = base + static_cast<uint64_t>(row) * stride + 32 * lane;
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+  }
+}
+
 template <int CH>
 __device__ __forceinline__ float lane_dot(const Row<CH>& a, const Row<CH>& b) {
   float s = 0.f;
@@ -153,12 +164,16 @@ __device__ __forceinline__ float apply_target(float x, bool positive, float lr, 
 // (err for the vertex row, g_t U for context row t), as in Hogwild!'s
 // lock-free component-wise updates (Recht et al., "asynchronous SGD");
 // otherwise (one warp per block) the final rows are stored.
-template <int K, int CH, bool ATOMIC>
+// PF > 0: the rows of sample s+PF (this chunk, or the next one whose ids are
+// nx_u/nx_c, nx_valid samples) are prefetched into L2 while sample s runs,
+// so the register loads of sample s+1 mostly hit L2.
+template <int K, int CH, bool ATOMIC, int PF>
 __device__ __forceinline__ float run_chunk(int nvalid, uint32_t my_u, const uint32_t* my_c,
                                            float* __restrict__ vertex,
                                            float* __restrict__ context, uint32_t stride,
                                            int dim4, float lr, float neg_weight, int lane,
-                                           bool want_loss) {
+                                           bool want_loss, int nx_valid = 0, uint32_t nx_u = 0,
+                                           const uint32_t* nx_c = nullptr) {
   float loss = 0.f;
   Row<CH> U, C[K + 1];
   uint32_t u = __shfl_sync(kFull, my_u, 0);
@@ -168,9 +183,34 @@ __device__ __forceinline__ float run_chunk(int nvalid, uint32_t my_u, const uint
   load_row<CH>(U, vertex, u, stride, lane, dim4);
 #pragma unroll
   for (int t = 0; t <= K; ++t) load_row<CH>(C[t], context, c[t], stride, lane, dim4);
+  if (PF > 0) {  // prime the prefetch window: samples 1..PF-1
+#pragma unroll
+    for (int j = 1; j < PF; ++j) {
+      if (j < nvalid) {
+        prefetch_row(vertex, __shfl_sync(kFull, my_u, j), stride, lane, dim4);
+#pragma unroll
+        for (int t = 0; t <= K; ++t)
+          prefetch_row(context, __shfl_sync(kFull, my_c[t], j), stride, lane, dim4);
+      }
+    }
+  }
 
   for (int s = 0; s < nvalid; ++s) {
     const bool has_next = (s + 1) < nvalid;
+    if (PF > 0) {
+      const int f = s + PF;
+      if (f < nvalid) {
+        prefetch_row(vertex, __shfl_sync(kFull, my_u, f), stride, lane, dim4);
+#pragma unroll
+        for (int t = 0; t <= K; ++t)
+          prefetch_row(context, __shfl_sync(kFull, my_c[t], f), stride, lane, dim4);
+      } else if (f - 32 >= 0 && f - 32 < nx_valid) {
+        prefetch_row(vertex, __shfl_sync(kFull, nx_u, f - 32), stride, lane, dim4);
+#pragma unroll
+        for (int t = 0; t <= K; ++t)
+          prefetch_row(context, __shfl_sync(kFull, nx_c[t], f - 32), stride, lane, dim4);
+      }
+    }
     uint32_t un = 0, cn[K + 1];
     Row<CH> Un, Cn[K + 1];
     if (has_next) {  // prefetch the next sample's rows (warp-uniform branch)
@@ -286,6 +326,11 @@ __device__ __forceinline__ void add_loss(double* acc, float loss, int lane) {
   if (acc != nullptr && lane == 0) atomicAdd(acc, static_cast<double>(loss));
 }
 
+#ifndef GV_PREFETCH
+#define GV_PREFETCH 0
+#endif
+constexpr int kPrefetch = GV_PREFETCH;  // samples of L2 prefetch look-ahead
+
 // KB2: persistent grid; warp w takes chunks w, w + W, ... of 32 consecutive
 // samples of the launch stream. The ids of the warp's next chunk (sample
 // load, Philox, alias gather) are requested before the current chunk is
@@ -306,8 +351,10 @@ __global__ void __launch_bounds__(256)
     const int nvalid = static_cast<int>(umin64(32, a.total - base));
     uint32_t nu = 0, nc[K + 1] = {};
     if (nx < nchunks && (nx << 5) + lane < a.total) sample_ids<K>(a, (nx << 5) + lane, nu, nc);
-    loss += run_chunk<K, CH, true>(nvalid, cu, cc, a.vertex, a.context, a.stride, dim4, a.lr,
-                                   a.neg_weight, lane, want_loss);
+    const int nx_valid = nx < nchunks ? static_cast<int>(umin64(32, a.total - (nx << 5))) : 0;
+    loss += run_chunk<K, CH, true, kPrefetch>(nvalid, cu, cc, a.vertex, a.context, a.stride, dim4,
+                                              a.lr, a.neg_weight, lane, want_loss, nx_valid, nu,
+                                              nc);
     cu = nu;
 #pragma unroll
     for (int t = 0; t <= K; ++t) cc[t] = nc[t];
@@ -328,8 +375,8 @@ __global__ void __launch_bounds__(32) sgd_ordered_kernel(const SgdArgs a, int di
     const int nvalid = static_cast<int>(umin64(32, count - off));
     uint32_t my_u = 0, my_c[K + 1] = {};
     if (lane < nvalid) sample_ids<K>(a, begin + off + lane, my_u, my_c);
-    loss += run_chunk<K, CH, false>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4,
-                                    a.lr, a.neg_weight, lane, want_loss);
+    loss += run_chunk<K, CH, false, 0>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4,
+                                       a.lr, a.neg_weight, lane, want_loss);
   }
   add_loss(a.loss_acc, loss, lane);
 }
@@ -345,8 +392,8 @@ __global__ void __launch_bounds__(32) sgd_explicit_kernel(const ExplicitArgs a, 
 #pragma unroll
       for (int t = 0; t <= K; ++t) my_c[t] = a.crow[(off + lane) * (K + 1) + t];
     }
-    run_chunk<K, CH, false>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4, a.lr,
-                            a.neg_weight, lane, false);
+    run_chunk<K, CH, false, 0>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4, a.lr,
+                               a.neg_weight, lane, false);
   }
 }
 

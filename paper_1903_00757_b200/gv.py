@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgv.so")
+LIB_PATH = os.environ.get("GV_LIB_PATH", os.path.join(_HERE, "libgv.so"))  # override: A/B builds
 
 STATUS = ["GV_OK", "GV_ERR_INVALID_ARG", "GV_ERR_STATE", "GV_ERR_OUT_OF_RANGE", "GV_ERR_EMPTY",
           "GV_ERR_CAPACITY", "GV_ERR_NOMEM", "GV_ERR_CUDA", "GV_ERR_COMM"]
