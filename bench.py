@@ -248,9 +248,12 @@ def run_ours(args):
         barrier()
         t0 = time.perf_counter()
         e2e_samples = 0
-        for _ in range(args.steps):
-            g.push(host_pool)               # H2D of the step's pool
-            st = g.train_episode()          # waits for the result; stats read back (D2H)
+        g.push(host_pool)                   # H2D of step 0's pool
+        for k in range(args.steps):
+            g.train_episode(stats=False)    # enqueue step k
+            if k + 1 < args.steps:
+                g.push(host_pool)           # H2D of step k+1 overlaps step k's training
+            st = g.read_stats()             # step k's result (loss, counts) read back (D2H)
             e2e_samples += st["samples_global"]
         barrier()
         dt = time.perf_counter() - t0

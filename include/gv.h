@@ -205,6 +205,12 @@ gv_status gv_train_episode(gv_ctx* ctx, gv_episode_stats* out);
 /* Wait for all device work of the context. */
 gv_status gv_synchronize(gv_ctx* ctx);
 
+/* Wait for the most recently trained pool and fill *out with its statistics
+ * (the same as gv_train_episode(ctx, out) would have returned). Lets a
+ * caller enqueue pool k, push pool k+1 (overlapping the copy with training)
+ * and only then read pool k's result. GV_ERR_STATE if no pool was trained. */
+gv_status gv_read_stats(gv_ctx* ctx, gv_episode_stats* out);
+
 /* Copy embeddings to out (num_nodes*dim floats, ORIGINAL id order).
  * In multi-process mode only rows owned by this rank (vertex: its vertex
  * partitions; context: its canonical window [d*m,(d+1)*m)) are written.

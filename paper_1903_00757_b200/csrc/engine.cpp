@@ -18,6 +18,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -139,6 +140,7 @@ struct gv_ctx {
   uint32_t stride = 0;
   int threads = 1;
   int sms = 148;
+  uint32_t hot_rows = 0;  // L2 retention: local ids below this are evict_last
   std::string err;
   bool loaded = false;
   // graph
@@ -472,6 +474,7 @@ gv_status run_steps(gv_ctx* c) {
       a.key0 = key0;
       a.key1 = key1;
       a.loss_acc = c->opt.compute_loss ? r.loss.p : nullptr;
+      a.hot_rows = c->hot_rows;
       gv_step_plan plan;
       gv_plan_step(n, c->D, r.d, t, &plan);
       auto launch = [&](uint32_t g0, uint32_t cnt_blk) -> gv_status {
@@ -762,6 +765,16 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
   c->stride = (dim + 3) / 4 * 4;
   c->threads = o.host_threads > 0 ? o.host_threads : gv::default_threads();
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, o.device);
+  {
+    // rows kept in L2 with evict_last: the highest-degree rows of every
+    // partition (zig-zag order is degree-descending within a partition) up
+    // to ~60% of L2 for the two matrices; GV_HOT_ROWS overrides (0 = off).
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, o.device);
+    const double budget = 0.6 * static_cast<double>(l2 > 0 ? l2 : 126 << 20);
+    c->hot_rows = static_cast<uint32_t>(budget / (2.0 * c->stride * 4.0 * n_partitions));
+    if (const char* e = getenv("GV_HOT_ROWS")) c->hot_rows = static_cast<uint32_t>(atol(e));
+  }
   c->ranks.resize(c->local);
   for (int v = 0; v < c->local; ++v) c->ranks[v].d = (o.world_size > 1) ? o.rank : v;
   *out = c;
@@ -883,6 +896,14 @@ gv_status gv_train_episode(gv_ctx* c, gv_episode_stats* out) {
   if (st) return st;
   if (out) return collect_stats(c, out);
   return GV_OK;
+}
+
+gv_status gv_read_stats(gv_ctx* c, gv_episode_stats* out) {
+  if (gv_status s = check_ctx(c, true)) return s;
+  if (!out) return fail(c, GV_ERR_INVALID_ARG, "null out");
+  if (c->pool_index == 0) return fail(c, GV_ERR_STATE, "no pool trained yet");
+  CK(cudaSetDevice(c->opt.device));
+  return collect_stats(c, out);
 }
 
 gv_status gv_synchronize(gv_ctx* c) {

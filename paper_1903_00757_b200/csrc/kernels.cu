@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "philox.cuh"
@@ -295,11 +296,200 @@ __device__ __forceinline__ float run_chunk(int nvalid, uint32_t my_u, const uint
   return loss;
 }
 
+// ------------------------------------------------------------------------
+// Half-warp variant of run_chunk for d <= 128 (Hogwild only): half h of the
+// warp (16 lanes) processes samples h, h+2, h+4, ... of the chunk, lane
+// hl = lane & 15 owning float4 columns hl and hl+16 of every row. One warp
+// instruction therefore serves two samples — the scalar part of a target
+// (expf, reciprocal, g) and the control flow are paid once per pair — and a
+// warp keeps two samples in flight. Each half is sequential with in-register
+// forwarding as in run_chunk; the two halves race like any two warps, and
+// their updates meet as red.global.add deltas.
+// ------------------------------------------------------------------------
+struct Row2 {
+  float4 v[2];
+};
+
+__device__ __forceinline__ void load_row2(Row2& r, const float* base, uint32_t row,
+                                          uint32_t stride, int hl, int dim4, bool active) {
+  const float4* p = reinterpret_cast<const float4*>(base + static_cast<uint64_t>(row) * stride);
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int col = hl + 16 * c;
+    r.v[c] = (active && col < dim4) ? __ldcg(p + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+__device__ __forceinline__ void red_row2(float* base, uint32_t row, uint32_t stride, int hl,
+                                         int dim4, float g, const Row2& x, bool active) {
+  float* p = base + static_cast<uint64_t>(row) * stride;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int col = hl + 16 * c;
+    if (active && col < dim4)
+      red_add4(p + 4 * col, make_float4(g * x.v[c].x, g * x.v[c].y, g * x.v[c].z, g * x.v[c].w));
+  }
+}
+
+__device__ __forceinline__ float lane_dot2(const Row2& a, const Row2& b) {
+  float s = a.v[0].x * b.v[0].x;
+  s = fmaf(a.v[0].y, b.v[0].y, s);
+  s = fmaf(a.v[0].z, b.v[0].z, s);
+  s = fmaf(a.v[0].w, b.v[0].w, s);
+  s = fmaf(a.v[1].x, b.v[1].x, s);
+  s = fmaf(a.v[1].y, b.v[1].y, s);
+  s = fmaf(a.v[1].z, b.v[1].z, s);
+  s = fmaf(a.v[1].w, b.v[1].w, s);
+  return s;
+}
+
+__device__ __forceinline__ void axpy2(Row2& y, float g, const Row2& x) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    y.v[c].x = fmaf(g, x.v[c].x, y.v[c].x);
+    y.v[c].y = fmaf(g, x.v[c].y, y.v[c].y);
+    y.v[c].z = fmaf(g, x.v[c].z, y.v[c].z);
+    y.v[c].w = fmaf(g, x.v[c].w, y.v[c].w);
+  }
+}
+
+// sum over the 16 lanes of each half
+__device__ __forceinline__ float half_sum1(float s) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  return s;
+}
+
+// two half-warp sums with 6 shuffles (split butterfly at offset 8)
+__device__ __forceinline__ void half_sum2(float& a, float& b, int lane) {
+  const bool hi = (lane & 8) != 0;
+  float keep = hi ? b : a;
+  const float send = hi ? a : b;
+  keep += __shfl_xor_sync(kFull, send, 8);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) keep += __shfl_xor_sync(kFull, keep, o);
+  const int base = lane & 16;
+  a = __shfl_sync(kFull, keep, base);
+  b = __shfl_sync(kFull, keep, base + 8);
+}
+
+template <int K>
+__device__ __forceinline__ float run_chunk_half(int nvalid, uint32_t my_u, const uint32_t* my_c,
+                                                float* __restrict__ vertex,
+                                                float* __restrict__ context, uint32_t stride,
+                                                int dim4, float lr, float neg_weight, int lane,
+                                                bool want_loss) {
+  const int h = lane >> 4, hl = lane & 15;
+  float loss = 0.f;
+  Row2 U, C[K + 1];
+  int q = h;  // this half's current sample
+  bool act = q < nvalid;
+  uint32_t u = __shfl_sync(kFull, my_u, q & 31);
+  uint32_t c[K + 1];
+#pragma unroll
+  for (int t = 0; t <= K; ++t) c[t] = __shfl_sync(kFull, my_c[t], q & 31);
+  load_row2(U, vertex, u, stride, hl, dim4, act);
+#pragma unroll
+  for (int t = 0; t <= K; ++t) load_row2(C[t], context, c[t], stride, hl, dim4, act);
+  const int iters = (nvalid + 1) >> 1;
+  for (int it = 0; it < iters; ++it) {
+    const int qn = q + 2;
+    const bool has_next = (it + 1) < iters;  // warp-uniform
+    const bool act_n = qn < nvalid;
+    uint32_t un = 0, cn[K + 1];
+    Row2 Un, Cn[K + 1];
+    if (has_next) {
+      un = __shfl_sync(kFull, my_u, qn & 31);
+#pragma unroll
+      for (int t = 0; t <= K; ++t) cn[t] = __shfl_sync(kFull, my_c[t], qn & 31);
+      load_row2(Un, vertex, un, stride, hl, dim4, act_n);
+#pragma unroll
+      for (int t = 0; t <= K; ++t) load_row2(Cn[t], context, cn[t], stride, hl, dim4, act_n);
+    }
+    Row2 err;
+    err.v[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    err.v[1] = err.v[0];
+    bool dup = false;
+#pragma unroll
+    for (int t = 1; t <= K; ++t)
+#pragma unroll
+      for (int tp = 0; tp < t; ++tp) dup |= (c[t] == c[tp]);
+    float g[K + 1];
+    if (!__any_sync(kFull, dup && act)) {
+      float x[K + 1];
+#pragma unroll
+      for (int t = 0; t <= K; ++t) x[t] = lane_dot2(U, C[t]);
+#pragma unroll
+      for (int t = 0; t + 1 <= K; t += 2) half_sum2(x[t], x[t + 1], lane);
+      if ((K + 1) & 1) x[K] = half_sum1(x[K]);
+#pragma unroll
+      for (int t = 0; t <= K; ++t) {
+        const float e = expf(-x[t]);
+        const float pr = __frcp_rn(1.0f + e);
+        g[t] = ((t == 0 ? 1.0f : 0.0f) - pr) * lr * (t == 0 ? 1.0f : neg_weight);
+        axpy2(err, g[t], C[t]);
+        red_row2(context, c[t], stride, hl, dim4, g[t], U, act);
+        axpy2(C[t], g[t], U);
+        if (want_loss && act) loss += __logf(1.0f + e) + (t == 0 ? 0.0f : x[t]);
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t <= K; ++t) {
+#pragma unroll
+        for (int tp = 0; tp < t; ++tp)
+          if (c[t] == c[tp]) C[t] = C[tp];
+        const float x = half_sum1(lane_dot2(U, C[t]));
+        const float e = expf(-x);
+        const float pr = __frcp_rn(1.0f + e);
+        g[t] = ((t == 0 ? 1.0f : 0.0f) - pr) * lr * (t == 0 ? 1.0f : neg_weight);
+        axpy2(err, g[t], C[t]);
+        red_row2(context, c[t], stride, hl, dim4, g[t], U, act);
+        axpy2(C[t], g[t], U);
+        if (want_loss && act) loss += __logf(1.0f + e) + (t == 0 ? 0.0f : x);
+      }
+    }
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      U.v[cc].x += err.v[cc].x;
+      U.v[cc].y += err.v[cc].y;
+      U.v[cc].z += err.v[cc].z;
+      U.v[cc].w += err.v[cc].w;
+    }
+    red_row2(vertex, u, stride, hl, dim4, 1.0f, err, act);
+    if (has_next) {
+      bool fwd = (un == u);
+#pragma unroll
+      for (int t = 0; t <= K; ++t)
+#pragma unroll
+        for (int tp = 0; tp <= K; ++tp) fwd |= (cn[t] == c[tp]);
+      if (__any_sync(kFull, fwd)) {
+        if (un == u) Un = U;
+#pragma unroll
+        for (int t = 0; t <= K; ++t) {
+#pragma unroll
+          for (int tp = 0; tp <= K; ++tp)
+            if (cn[t] == c[tp]) Cn[t] = C[tp];
+        }
+      }
+      U = Un;
+      u = un;
+#pragma unroll
+      for (int t = 0; t <= K; ++t) {
+        C[t] = Cn[t];
+        c[t] = cn[t];
+      }
+      q = qn;
+      act = act_n;
+    }
+  }
+  return loss;
+}
+
 // Per-lane ids of sample `qg` of a launch stream: block lookup, sample load,
 // K negatives by Philox + alias (P:231 negatives from partition j only).
 template <int K>
 __device__ __forceinline__ void sample_ids(const SgdArgs& a, uint64_t qg, uint32_t& my_u,
-                                           uint32_t* my_c) {
+                                           uint32_t* my_c, uint32_t* my_hot = nullptr) {
   int lo = 0, hi = a.nblk - 1;  // last desc with prefix <= qg
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -318,25 +508,280 @@ __device__ __forceinline__ void sample_ids(const SgdArgs& a, uint64_t qg, uint32
                                   a.key1);
     const uint32_t slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, m);
     const uint2 pa = __ldg(a.alias + alias0 + slot);
-    my_c[1 + k] = crow0 + alias_pick(pa.x, pa.y, slot, r.z);
+    const uint32_t nl = alias_pick(pa.x, pa.y, slot, r.z);
+    my_c[1 + k] = crow0 + nl;
+    if (my_hot) *my_hot |= (nl < a.hot_rows ? 1u : 0u) << (2 + k);
   }
+  if (my_hot) *my_hot |= (smp.x < a.hot_rows ? 1u : 0u) | ((smp.y < a.hot_rows ? 1u : 0u) << 1);
+}
+
+// ------------------------------------------------------------------------
+// Deep-pipelined Hogwild path (d <= 128): half-warps as in run_chunk_half,
+// but the rows of each half's next P samples are in flight as cp.async
+// (LDGSTS, L2-only) copies into a per-half shared-memory ring of R = P + 1
+// stages — P samples of row traffic outstanding per half without holding them
+// in registers ("leverage the on-chip shared memory"). There is no
+// register forwarding: a row may be read before this warp's own deltas of the
+// previous P samples have landed — bounded staleness, the same as between any
+// two warps under Hogwild; no update is lost because every write-back is a
+// red.global.add delta. (The exact, sequential mode is sgd_ordered_kernel.)
+// Lane hl of a half owns float4 columns hl and hl+16 in global and shared
+// memory, so no lane reads another lane's shared data and cp.async
+// completion (wait_group, per thread) is the only synchronisation.
+// ------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(float4* smem, const float4* gmem, uint64_t pol) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa),
+               "l"(gmem), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void red_add4_hint(float* p, float4 v, uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(p),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void red_row2_hint(float* base, uint32_t row, uint32_t stride, int hl,
+                                              int dim4, float g, const Row2& x, bool active,
+                                              uint64_t pol) {
+  float* p = base + static_cast<uint64_t>(row) * stride;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int col = hl + 16 * c;
+    if (active && col < dim4)
+      red_add4_hint(p + 4 * col,
+                    make_float4(g * x.v[c].x, g * x.v[c].y, g * x.v[c].z, g * x.v[c].w), pol);
+  }
+}
+// L2 policies: hot rows (high degree, small local id) stay, cold rows go first
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+#ifndef GV_RING_P
+#define GV_RING_P 5
+#endif
+constexpr int kRingP = GV_RING_P;
+
+template <int K>
+struct RingCfg {
+  static constexpr int R = kRingP + 1;   // stages per half
+  static constexpr int T = K + 2;        // rows per sample
+  static constexpr int STAGE = T * 32;   // float4 per stage (a 512 B row = 32 float4)
+  static constexpr int HALF = R * STAGE;
+  static constexpr int WARP = 2 * HALF;  // float4 per warp
+  static constexpr size_t warp_bytes() { return static_cast<size_t>(WARP) * 16; }
+};
+
+// Sequence of samples processed by one warp: sample p is stream index
+// start + (p >> 5) * stride + (p & 31), p < L.
+struct WarpSeq {
+  uint64_t start, stride;
+  uint32_t L;
+};
+
+template <int K>
+__device__ __forceinline__ void seq_chunk_ids(const SgdArgs& a, const WarpSeq& sq, uint32_t chunk,
+                                              int lane, uint32_t& u, uint32_t* c, uint32_t& hot) {
+  const uint32_t p = (chunk << 5) + lane;
+  u = 0;
+  hot = 0;
+#pragma unroll
+  for (int t = 0; t <= K; ++t) c[t] = 0;
+  if (p < sq.L)
+    sample_ids<K>(a, sq.start + static_cast<uint64_t>(chunk) * sq.stride + lane, u, c, &hot);
+}
+
+template <int K>
+__device__ __forceinline__ float run_ring_half(const SgdArgs& a, const WarpSeq& sq, float4* ring,
+                                               int dim4, int lane, bool want_loss) {
+  using RC = RingCfg<K>;
+  constexpr int P = kRingP, R = RC::R, T = RC::T;
+  const int h = lane >> 4, hl = lane & 15;
+  float4* const my = ring + h * RC::HALF;
+  float* const vertex = a.vertex;
+  float* const context = a.context;
+  const uint32_t stride = a.stride;
+  float loss = 0.f;
+  if (sq.L == 0) return loss;
+  const uint32_t iters = (sq.L + 1) >> 1;  // iteration i: half h runs sample 2i + h
+  uint32_t cu, cc[K + 1], nu, nc[K + 1];   // ids of the current / next 32-sample chunk
+  uint32_t ch_hot, nh_hot;                 // hot-row bits of those samples
+  seq_chunk_ids<K>(a, sq, 0, lane, cu, cc, ch_hot);
+  seq_chunk_ids<K>(a, sq, 1, lane, nu, nc, nh_hot);
+  const uint64_t pol_hot = a.hot_rows ? policy_evict_last() : policy_evict_normal();
+  const uint64_t pol_cold = a.hot_rows ? policy_evict_first() : policy_evict_normal();
+  // ids of sample 2j + h (j = iteration), from the current or the next chunk
+  auto ids_of = [&](uint32_t j, uint32_t cur_chunk, uint32_t& u, uint32_t* c, uint32_t& hot) {
+    const uint32_t pp = 2 * j + h;
+    const bool cur = (j >> 4) == cur_chunk;  // warp-uniform (2j and 2j+1 share a chunk)
+    const int l = static_cast<int>(pp & 31);
+    u = __shfl_sync(kFull, cur ? cu : nu, l);
+#pragma unroll
+    for (int t = 0; t <= K; ++t) c[t] = __shfl_sync(kFull, cur ? cc[t] : nc[t], l);
+    hot = __shfl_sync(kFull, cur ? ch_hot : nh_hot, l);
+  };
+  auto issue = [&](uint32_t j, int st, uint32_t cur_chunk) {
+    uint32_t u, c[K + 1], hot;
+    ids_of(j, cur_chunk, u, c, hot);
+    if (2 * j + h < sq.L) {
+      float4* stage = my + st * RC::STAGE;
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const float4* g = reinterpret_cast<const float4*>(
+            (t == 0 ? vertex : context) + static_cast<uint64_t>(t == 0 ? u : c[t - 1]) * stride);
+        const uint64_t pol = ((hot >> t) & 1u) ? pol_hot : pol_cold;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int col = hl + 16 * q;
+          if (col < dim4) cp_async16(stage + t * 32 + col, g + col, pol);
+        }
+      }
+    }
+  };
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    if (static_cast<uint32_t>(j) < iters) issue(j, j, 0);
+    cp_commit();
+  }
+  int st = 0;       // stage of iteration i
+  int st_in = P;    // stage the prefetch of iteration i + P goes to
+  for (uint32_t i = 0; i < iters; ++i) {
+    const uint32_t chunk = i >> 4;
+    cp_wait<P - 1>();
+    const bool act = 2 * i + h < sq.L;
+    uint32_t u, c[K + 1], hot;
+    ids_of(i, chunk, u, c, hot);
+    const float4* stage = my + st * RC::STAGE;
+    Row2 U, C[K + 1], err;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int col = hl + 16 * q;
+      const bool ok = act && col < dim4;
+      U.v[q] = ok ? stage[col] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int t = 0; t <= K; ++t)
+        C[t].v[q] = ok ? stage[(1 + t) * 32 + col] : make_float4(0.f, 0.f, 0.f, 0.f);
+      err.v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    bool dup = false;
+#pragma unroll
+    for (int t = 1; t <= K; ++t)
+#pragma unroll
+      for (int tp = 0; tp < t; ++tp) dup |= (c[t] == c[tp]);
+    if (!__any_sync(kFull, dup && act)) {
+      float x[K + 1];
+#pragma unroll
+      for (int t = 0; t <= K; ++t) x[t] = lane_dot2(U, C[t]);
+#pragma unroll
+      for (int t = 0; t + 1 <= K; t += 2) half_sum2(x[t], x[t + 1], lane);
+      if ((K + 1) & 1) x[K] = half_sum1(x[K]);
+#pragma unroll
+      for (int t = 0; t <= K; ++t) {
+        const float e = expf(-x[t]);
+        const float pr = __frcp_rn(1.0f + e);
+        const float g = ((t == 0 ? 1.0f : 0.0f) - pr) * a.lr * (t == 0 ? 1.0f : a.neg_weight);
+        axpy2(err, g, C[t]);
+        red_row2_hint(context, c[t], stride, hl, dim4, g, U, act,
+                      ((hot >> (1 + t)) & 1u) ? pol_hot : pol_cold);
+        if (want_loss && act) loss += __logf(1.0f + e) + (t == 0 ? 0.0f : x[t]);
+      }
+    } else {
+      // a target repeated inside the sample sees the earlier target's update (R-DUP)
+#pragma unroll
+      for (int t = 0; t <= K; ++t) {
+#pragma unroll
+        for (int tp = 0; tp < t; ++tp)
+          if (c[t] == c[tp]) C[t] = C[tp];
+        const float x = half_sum1(lane_dot2(U, C[t]));
+        const float e = expf(-x);
+        const float pr = __frcp_rn(1.0f + e);
+        const float g = ((t == 0 ? 1.0f : 0.0f) - pr) * a.lr * (t == 0 ? 1.0f : a.neg_weight);
+        axpy2(err, g, C[t]);
+        red_row2_hint(context, c[t], stride, hl, dim4, g, U, act,
+                      ((hot >> (1 + t)) & 1u) ? pol_hot : pol_cold);
+        axpy2(C[t], g, U);
+        if (want_loss && act) loss += __logf(1.0f + e) + (t == 0 ? 0.0f : x);
+      }
+    }
+    red_row2_hint(vertex, u, stride, hl, dim4, 1.0f, err, act, (hot & 1u) ? pol_hot : pol_cold);
+    if (i + P < iters) issue(i + P, st_in, chunk);
+    cp_commit();
+    st = (st + 1 == R) ? 0 : st + 1;
+    st_in = (st_in + 1 == R) ? 0 : st_in + 1;
+    if ((i & 15) == 15) {  // both halves finished the chunk: slide the id window
+      cu = nu;
+      ch_hot = nh_hot;
+#pragma unroll
+      for (int t = 0; t <= K; ++t) cc[t] = nc[t];
+      seq_chunk_ids<K>(a, sq, chunk + 2, lane, nu, nc, nh_hot);
+    }
+  }
+  cp_wait<0>();
+  return loss;
+}
+
+template <int K>
+__global__ void __launch_bounds__(128) sgd_ring_kernel(const SgdArgs a, int dim4) {
+  extern __shared__ float4 smem_f4[];
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t nchunks = (a.total + 31) >> 5;
+  WarpSeq sq{warp << 5, nw << 5, 0};
+  if (warp < nchunks) {
+    const uint64_t mine = (nchunks - 1 - warp) / nw + 1;
+    uint64_t L = mine << 5;
+    if (warp + (mine - 1) * nw == nchunks - 1) L -= (nchunks << 5) - a.total;
+    sq.L = static_cast<uint32_t>(L);
+  }
+  float4* ring = smem_f4 + (threadIdx.x >> 5) * RingCfg<K>::WARP;
+  const float loss = run_ring_half<K>(a, sq, ring, dim4, lane, a.loss_acc != nullptr);
+  if (a.loss_acc != nullptr && (lane & 15) == 0) atomicAdd(a.loss_acc, static_cast<double>(loss));
 }
 
 __device__ __forceinline__ void add_loss(double* acc, float loss, int lane) {
   if (acc != nullptr && lane == 0) atomicAdd(acc, static_cast<double>(loss));
+}
+// the half-warp path keeps one partial per half (lanes 0 and 16)
+__device__ __forceinline__ void add_loss_halves(double* acc, float loss, int lane) {
+  if (acc != nullptr && (lane & 15) == 0) atomicAdd(acc, static_cast<double>(loss));
 }
 
 #ifndef GV_PREFETCH
 #define GV_PREFETCH 0
 #endif
 constexpr int kPrefetch = GV_PREFETCH;  // samples of L2 prefetch look-ahead
+#ifndef GV_HOG_MINB
+#define GV_HOG_MINB 2
+#endif
+#ifndef GV_HALF_WARP
+#define GV_HALF_WARP 1
+#endif
+constexpr bool kHalfWarp = GV_HALF_WARP != 0;  // two samples per warp for d <= 128
 
 // KB2: persistent grid; warp w takes chunks w, w + W, ... of 32 consecutive
 // samples of the launch stream. The ids of the warp's next chunk (sample
 // load, Philox, alias gather) are requested before the current chunk is
 // processed, so their latency hides behind 32 samples of work.
 template <int K, int CH>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, (CH == 1) ? GV_HOG_MINB : 1)
     sgd_hogwild_kernel(const SgdArgs a, int dim4) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -351,15 +796,23 @@ __global__ void __launch_bounds__(256)
     const int nvalid = static_cast<int>(umin64(32, a.total - base));
     uint32_t nu = 0, nc[K + 1] = {};
     if (nx < nchunks && (nx << 5) + lane < a.total) sample_ids<K>(a, (nx << 5) + lane, nu, nc);
-    const int nx_valid = nx < nchunks ? static_cast<int>(umin64(32, a.total - (nx << 5))) : 0;
-    loss += run_chunk<K, CH, true, kPrefetch>(nvalid, cu, cc, a.vertex, a.context, a.stride, dim4,
-                                              a.lr, a.neg_weight, lane, want_loss, nx_valid, nu,
-                                              nc);
+    if (CH == 1 && kHalfWarp) {
+      loss += run_chunk_half<K>(nvalid, cu, cc, a.vertex, a.context, a.stride, dim4, a.lr,
+                                a.neg_weight, lane, want_loss);
+    } else {
+      const int nx_valid = nx < nchunks ? static_cast<int>(umin64(32, a.total - (nx << 5))) : 0;
+      loss += run_chunk<K, CH, true, kPrefetch>(nvalid, cu, cc, a.vertex, a.context, a.stride,
+                                                dim4, a.lr, a.neg_weight, lane, want_loss,
+                                                nx_valid, nu, nc);
+    }
     cu = nu;
 #pragma unroll
     for (int t = 0; t <= K; ++t) cc[t] = nc[t];
   }
-  add_loss(a.loss_acc, loss, lane);
+  if (CH == 1 && kHalfWarp)
+    add_loss_halves(a.loss_acc, loss, lane);
+  else
+    add_loss(a.loss_acc, loss, lane);
 }
 
 // Ordered verification mode: warp b owns descriptor b and walks its block
@@ -666,6 +1119,19 @@ const ExpFn kExp[8][4] = {GV_ROW(1), GV_ROW(2), GV_ROW(3), GV_ROW(4),
 
 int ch_of(int dim) { return (dim / 4 + 31) / 32; }
 
+const HogFn kRing[8] = {sgd_ring_kernel<1>, sgd_ring_kernel<2>, sgd_ring_kernel<3>,
+                        sgd_ring_kernel<4>, sgd_ring_kernel<5>, sgd_ring_kernel<6>,
+                        sgd_ring_kernel<7>, sgd_ring_kernel<8>};
+
+int ring_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GV_SGD_RING");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
+}
+
 }  // namespace
 
 int sgd_supported(int dim, int K) {
@@ -675,6 +1141,24 @@ int sgd_supported(int dim, int K) {
 cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaStream_t s) {
   if (a.total == 0 || a.nblk == 0) return cudaSuccess;
   const int ki = K - 1, ci = ch_of(dim) - 1;
+  if (ci == 0 && ring_mode()) {
+    HogFn f = kRing[ki];
+    const size_t wb = static_cast<size_t>(2) * (kRingP + 1) * (K + 2) * 32 * 16;
+    const int warps = 4;
+    const size_t smem = wb * warps;
+    static int occr[8] = {};
+    int& o = occr[ki];
+    if (o == 0) {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, 32 * warps, smem) != cudaSuccess || o <= 0)
+        o = 1;
+    }
+    const uint64_t chunks = (a.total + 31) / 32;
+    uint64_t grid = static_cast<uint64_t>(sms > 0 ? sms : num_sms()) * o;
+    grid = std::min<uint64_t>(grid, (chunks + warps - 1) / warps);
+    f<<<static_cast<unsigned>(grid), 32 * warps, smem, s>>>(a, dim / 4);
+    return cudaGetLastError();
+  }
   HogFn f = kHog[ki][ci];
   static int occ[8][4] = {};
   int& o = occ[ki][ci];

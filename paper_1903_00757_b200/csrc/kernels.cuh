@@ -31,6 +31,8 @@ struct SgdArgs {
   uint32_t pool_index;    // e
   uint32_t key0, key1;    // negative-stream Philox key
   double* loss_acc;       // nullable
+  uint32_t hot_rows;      // local ids < hot_rows are L2 evict_last, others evict_first
+                          // (0 = no cache hints)
 };
 
 struct ExplicitArgs {

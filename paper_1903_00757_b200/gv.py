@@ -92,6 +92,7 @@ SIGNATURES = {
     "gv_replay_pool": (st, [ctx_p]),
     "gv_train_episode": (st, [ctx_p, C.POINTER(gv_episode_stats)]),
     "gv_synchronize": (st, [ctx_p]),
+    "gv_read_stats": (st, [ctx_p, C.POINTER(gv_episode_stats)]),
     "gv_get_vertex_embeddings": (st, [ctx_p, f32p, C.c_uint64]),
     "gv_get_context_embeddings": (st, [ctx_p, f32p, C.c_uint64]),
     "gv_set_vertex_embeddings": (st, [ctx_p, f32p, C.c_uint64]),
@@ -203,6 +204,12 @@ def gv_train_episode(ctx, stats=True):
     s = gv_episode_stats() if stats else None
     _ck(lib.gv_train_episode(ctx, C.byref(s) if s is not None else None), ctx)
     return s.as_dict() if s is not None else None
+
+
+def gv_read_stats(ctx):
+    s = gv_episode_stats()
+    _ck(lib.gv_read_stats(ctx, C.byref(s)), ctx)
+    return s.as_dict()
 
 
 def gv_synchronize(ctx):
@@ -355,6 +362,9 @@ class GraphVite:
 
     def train_episode(self, stats=True):
         return gv_train_episode(self.ctx, stats)
+
+    def read_stats(self):
+        return gv_read_stats(self.ctx)
 
     def replay(self):
         gv_replay_pool(self.ctx)

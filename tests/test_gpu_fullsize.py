@@ -1,0 +1,128 @@
+"""GPU checks at BASELINE.json's full single-GPU size (configs[1], C2:
+1,138,499 nodes / 4,945,382 edges, d = 128, K = 1, s = 5, 2e8-sample pool) in
+the launch configuration bench.py times (Hogwild kernel, n = 1), plus the
+collaboration pipeline (gv_run).
+
+Element-wise parity of Hogwild SGD at this size is not computable (the
+oracle needs minutes and Hogwild is nondeterministic), so the checks are:
+bit-exact augmentation, bucketing and sampled negative streams against the
+oracle, and properties that hold at any size (conservation, isolated rows
+untouched, finiteness, loss decrease)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+from paper_1903_00757_b200 import gv as G  # noqa: E402
+
+C2 = synth.CONFIGS["C2"]
+
+
+@pytest.fixture(scope="module")
+def c2():
+    src, dst = synth.chung_lu(C2["nv"], C2["ne"], gamma=C2["gamma"], wmax=C2["wmax"], seed=1)
+    g = G.GraphVite(C2["nv"], C2["d"], 1, C2["K"], 0.025, total_samples=4 * C2["pool"])
+    g.load_edges(src, dst)
+    pool = g.augment(40, C2["s"], 16, C2["pool"], 1000)
+    yield src, dst, g, pool
+    g.close()
+
+
+def test_full_size_augmentation_bitexact(c2):
+    """a1 at full size: 2e8 pairs from 16 sampler threads == oracle."""
+    src, dst, g, pool = c2
+    ref = O.Sampler(O.Graph(C2["nv"], src, dst)).augment(40, C2["s"], 16, C2["pool"], 1000)
+    assert np.array_equal(pool, ref)
+
+
+def test_full_size_bucketing_and_negatives(c2):
+    """a3-a5 (n = 1 relabel) bit-exact on the whole pool; the negative stream
+    bit-exact on 20,000 sampled positions."""
+    src, dst, g, pool = c2
+    g.push(pool)
+    G.gv_prepare_episode(g.ctx)
+    got, boff = G.gv_debug_get_buckets(g.ctx, 1, len(pool))
+    perm, _ = g.partition()
+    assert list(boff) == [0, len(pool)]
+    assert np.array_equal(got, perm[pool])
+    negs = G.gv_debug_get_negatives(g.ctx, 0, 0, len(pool), 1)[:, 0]
+    o = O.Trainer(C2["nv"], 4, 1, K=1)
+    o.load_edges(src, dst)
+    rng = np.random.default_rng(0)
+    for q in rng.integers(0, len(pool), 20_000):
+        assert negs[q] == o.negative_at(int(q), 0, 0, 0)
+    # negatives never hit isolated nodes (zero noise mass)
+    deg = np.bincount(np.r_[src, dst], minlength=C2["nv"])
+    inv = np.argsort(perm)
+    assert (deg[inv[np.unique(negs)]] > 0).all()
+    g.train_episode()  # consume the prepared pool
+
+
+def test_full_size_hogwild_properties(c2):
+    """Three more Hogwild pools in the bench configuration: every sample is
+    trained, the loss per sample falls, embeddings stay finite, and rows of
+    isolated nodes (never sampled, never drawn as negatives) are exactly
+    their initial values."""
+    src, dst, g, pool = c2
+    deg = np.bincount(np.r_[src, dst], minlength=C2["nv"])
+    iso = np.flatnonzero(deg == 0)
+    assert len(iso) > 1000
+    init = O.init_vertex(C2["nv"], C2["d"], 4)
+    losses = []
+    for k in range(3):
+        g.replay()
+        st = g.train_episode()
+        assert st["samples_global"] == C2["pool"] and st["sgd_launches"] == 1
+        losses.append(st["loss_sum"] / st["samples_global"])
+    assert losses[2] < losses[0]
+    V, Cm = g.vertex(), g.context()
+    assert np.isfinite(V).all() and np.isfinite(Cm).all()
+    assert np.array_equal(V[iso], init[iso])
+    assert not Cm[iso].any()
+    assert np.abs(V[deg > 0] - init[deg > 0]).max() > 1e-3
+
+
+def test_collaboration_pipeline_matches_oracle():
+    """gv_run: pools produced by the host sampler threads while
+    the previous pool trains; with the ordered kernel the result equals the
+    oracle fed with the oracle's own augmentation of the same seeds, and the
+    sequential (collaborate = 0) run gives the same bytes."""
+    src, dst = synth.chung_lu(5000, 25_000, gamma=2.1, wmax=400.0, seed=7)
+    P, pools = 200_000, 3
+    out = {}
+    for collab in (1, 0):
+        g = G.GraphVite(5000, 32, 2, 1, 0.025, total_samples=P * pools, ordered=1)
+        g.load_edges(src, dst)
+        rep = G.gv_run(g.ctx, 40, 2, 4, P, 77, P * pools, collaborate=bool(collab))
+        assert rep["pools"] == pools and rep["samples"] == P * pools
+        out[collab] = (g.vertex(), g.context())
+        g.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    o = O.Trainer(5000, 32, 2, K=1, lr0=0.025, lr_kind=1, total_samples=P * pools)
+    o.load_edges(src, dst)
+    sampler = O.Sampler(O.Graph(5000, src, dst))
+    for k in range(pools):
+        o.train_pool(sampler.augment(40, 2, 4, P, 77 + k))
+    for a, b in zip(out[1], (o.get("vertex"), o.get("context"))):
+        rel = np.linalg.norm(a.astype(np.float64) - b) / np.linalg.norm(b.astype(np.float64))
+        assert rel <= 1e-5, rel
+
+
+def test_read_stats_after_overlapped_push():
+    """gv_train_episode without stats, push of the next pool (overlapping the
+    copy with training), then gv_read_stats of the first pool."""
+    src, dst = synth.chung_lu(3000, 15_000, seed=2)
+    g = G.GraphVite(3000, 64, 1, 1, 0.025)
+    g.load_edges(src, dst)
+    a = synth.edge_pool(src, dst, 300_000, seed=1)
+    g.push(a)
+    g.train_episode(stats=False)
+    g.push(synth.edge_pool(src, dst, 100_000, seed=2))
+    st = g.read_stats()
+    assert st["samples_global"] == 300_000 and st["pool_index"] == 0
+    st2 = g.train_episode()
+    assert st2["samples_global"] == 100_000 and st2["pool_index"] == 1
+    g.close()
