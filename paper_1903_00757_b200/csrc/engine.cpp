@@ -765,16 +765,11 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
   c->stride = (dim + 3) / 4 * 4;
   c->threads = o.host_threads > 0 ? o.host_threads : gv::default_threads();
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, o.device);
-  {
-    // rows kept in L2 with evict_last: the highest-degree rows of every
-    // partition (zig-zag order is degree-descending within a partition) up
-    // to ~60% of L2 for the two matrices; GV_HOT_ROWS overrides (0 = off).
-    int l2 = 0;
-    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, o.device);
-    const double budget = 0.6 * static_cast<double>(l2 > 0 ? l2 : 126 << 20);
-    c->hot_rows = static_cast<uint32_t>(budget / (2.0 * c->stride * 4.0 * n_partitions));
-    if (const char* e = getenv("GV_HOT_ROWS")) c->hot_rows = static_cast<uint32_t>(atol(e));
-  }
+  // L2 retention hints (hot rows evict_last, cold rows evict_first) are OFF:
+  // measured on C2 they evict a cold line between its cp.async read and its
+  // red.global.add write-back (DRAM reads +29%, -19% samples/s; profiles/).
+  // GV_HOT_ROWS=<local-id threshold> enables them for experiments.
+  if (const char* e = getenv("GV_HOT_ROWS")) c->hot_rows = static_cast<uint32_t>(atol(e));
   c->ranks.resize(c->local);
   for (int v = 0; v < c->local; ++v) c->ranks[v].d = (o.world_size > 1) ? o.rank : v;
   *out = c;
