@@ -52,6 +52,7 @@ def parse():
                     help="samples of the bounded oracle run (cpu_baseline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true", help="skip the gv_run pipeline detail")
     ap.add_argument("--ordered", action="store_true", help="ordered verification kernel (slow)")
     return ap.parse_args()
 
@@ -257,8 +258,17 @@ def run_ours(args):
     per_launch_samples = local_samples / max(sgd_launches, 1)
     achieved = per_launch_samples * bps / (avg_launch_ms / 1e3) / 1e9
     peak, peak_kind = peaks()
+    traffic = None
+    try:  # DRAM bytes of the same kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "sgd_traffic.json")) as f:
+            tr = json.load(f)
+        traffic = tr["dram_bytes_per_sample"] * per_launch_samples
+    except Exception:
+        pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "kernel": "sgd_ring_kernel<1> (d<=128 Hogwild)",
+            "frac": achieved / peak, "traffic": traffic,
+            "traffic_source": "profiles/sgd_traffic.json (ncu dram__bytes_read+write per sample x "
+                              "samples per launch)", "kernel": "sgd_ring_kernel<1> (d<=128 Hogwild)",
             "peak_source": peak_kind, "sgd_share_of_step": sgd_ms / sum(tot_ms),
             "bytes_per_sample": bps}
     # end to end through the C ABI from pinned host memory
@@ -283,6 +293,29 @@ def run_ours(args):
         e2e = {"value": e2e_samples / dt, "unit": "samples/s",
                "h2d_bytes_per_step": P * 8,
                "d2h_bytes_per_step": 8 * (n * n + 2) + 8}
+    # collaboration pipelines (NEXT-1/NEXT-2): wall clock of
+    # gv_run over `pipe_pools` pools, pools produced by the host sampler threads
+    # (collaborate on / off, tab:main_components) or on the GPU (NEXT-1)
+    pipeline = None
+    if world == 1 and not args.no_pipeline:
+        pipe_pools = 4
+        total = P * pipe_pools
+        pipeline = {"pools": pipe_pools, "pool": P}
+        g.synchronize()
+        t0 = time.perf_counter()
+        g.augment_device(CFG["walk"], CFG["s"], 1184, P, 5000)
+        g.synchronize()
+        pipeline["gpu_augment_ms_per_pool"] = 1e3 * (time.perf_counter() - t0)
+        g.train_episode(stats=False)  # consume it
+        g.synchronize()
+        for name, kw in [("gpu_augment", dict(threads=1184, device=True)),
+                         ("host_collaborate", dict(threads=threads, collaborate=True)),
+                         ("host_sequential", dict(threads=threads, collaborate=False))]:
+            rep = G.gv_run(g.ctx, CFG["walk"], CFG["s"], kw.pop("threads"), P, 6000, total, **kw)
+            pipeline[name + "_samples_per_s"] = total / (rep["wall_ms"] / 1e3)
+            if not name.startswith("gpu"):
+                pipeline[name + "_produce_ms"] = rep["produce_ms"]
+                pipeline[name + "_train_wait_ms"] = rep["train_wait_ms"]
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(src, dst, args.cpu_sample, threads, 1000)
@@ -299,7 +332,7 @@ def run_ours(args):
                        "partitions": n, "pool_per_rank": P, "l2": "inputs > L2 (no flush)",
                        "mode": "ordered" if args.ordered else "hogwild"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk,
+            "clocks": clk, "pipeline": pipeline,
             "detail": {"ms_total_per_pool": tot_ms, "sgd_ms_per_pool": sgd_ms / args.steps,
                        "bucket_ms": stats["ms_bucket"], "load_edges_s": t_load,
                        "augment_s": t_aug, "augment_threads": threads,

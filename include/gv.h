@@ -239,6 +239,22 @@ gv_status gv_augment(gv_ctx* ctx, uint32_t walk_len, uint32_t s,
                      uint32_t threads, uint64_t count, uint64_t seed,
                      uint32_t* out_pairs);
 
+/* NEXT-1: online augmentation ON THE DEVICE. The same pool
+ * as gv_augment(walk_len, s, threads = segments, count, seed) — byte for byte
+ * (reading R-AUG) — generated by one CTA per segment from a device copy of
+ * the graph's CSR and alias tables (uploaded on first use), and APPENDED to
+ * the pending device pool (no host buffer, no H2D copy). Runs on the copy
+ * stream, so it overlaps the training of the previous pool.
+ * Errors: GV_ERR_STATE (no graph), GV_ERR_INVALID_ARG (walk_len == 0,
+ * s == 0, s > walk_len, segments == 0, walk_len > 1000), GV_ERR_CAPACITY
+ * (max_pool_samples), GV_ERR_CUDA. Single-rank contexts only (D == 1). */
+gv_status gv_augment_device(gv_ctx* ctx, uint32_t walk_len, uint32_t s, uint32_t segments,
+                            uint64_t count, uint64_t seed);
+
+/* Copy the pending (not yet trained) pool to the host: out_pairs[2*cap],
+ * *count = its size. Tests. */
+gv_status gv_debug_get_pending(gv_ctx* ctx, uint32_t* out_pairs, uint64_t cap, uint64_t* count);
+
 /* Collaboration strategy: two pinned host pools; producer
  * threads fill one with gv_augment while the trainer pushes and trains the
  * other; pools swap when both sides are done. Trains ceil(total/pool) pools.
@@ -252,6 +268,8 @@ typedef struct {
   uint64_t pool_samples;  /* samples per pool         */
   uint64_t seed;          /* augmentation Philox key (pool k uses seed + k) */
   int collaborate;        /* 1 = double-buffered      */
+  int device;             /* 1 = augment on the GPU (gv_augment_device, segments =
+                             threads); pool k+1 is generated while pool k trains */
 } gv_augment_cfg;
 typedef struct {
   uint64_t pools, samples;

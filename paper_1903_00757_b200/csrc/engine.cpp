@@ -148,6 +148,11 @@ struct gv_ctx {
   gv::Partitioning part;
   std::vector<uint32_t> nprob, nalias;  // negative tables, new-id order
   gv::WalkTables walks;
+  // device copy of the walk tables (gv_augment_device), lazily uploaded
+  uint64_t* d_woff = nullptr;
+  uint32_t* d_wnbr = nullptr;
+  uint2* d_walias = nullptr;
+  uint2* d_dalias = nullptr;
   // shared device tables
   uint32_t* d_packed = nullptr;
   uint2* d_alias = nullptr;
@@ -990,6 +995,67 @@ gv_status gv_augment(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_t threads,
   return GV_OK;
 }
 
+gv_status gv_augment_device(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_t segments,
+                            uint64_t count, uint64_t seed) {
+  if (gv_status st = check_ctx(c, true)) return st;
+  if (walk_len == 0 || walk_len > 1000 || s == 0 || s > walk_len || segments == 0)
+    return fail(c, GV_ERR_INVALID_ARG, "need 0 < walk_len <= 1000, 0 < s <= walk_len, segments > 0");
+  if (c->D != 1) return fail(c, GV_ERR_STATE, "gv_augment_device needs a single rank");
+  if (count == 0) return GV_OK;
+  if (count > (UINT64_MAX / segments)) return fail(c, GV_ERR_CAPACITY, "count * segments overflows");
+  CK(cudaSetDevice(c->opt.device));
+  if (!c->d_woff) {  // upload the CSR and the alias tables the host sampler uses
+    const gv::HostGraph& g = c->graph;
+    const size_t ne = g.nbr.size();
+    CK(cudaMalloc(&c->d_woff, sizeof(uint64_t) * (g.nv + 1)));
+    CK(cudaMalloc(&c->d_wnbr, sizeof(uint32_t) * std::max<size_t>(ne, 1)));
+    CK(cudaMalloc(&c->d_walias, sizeof(uint2) * std::max<size_t>(ne, 1)));
+    CK(cudaMalloc(&c->d_dalias, sizeof(uint2) * g.nv));
+    std::vector<uint2> ea(ne), da(g.nv);
+    for (size_t q = 0; q < ne; ++q) ea[q] = make_uint2(c->walks.eprob[q], c->walks.ealias[q]);
+    for (uint32_t q = 0; q < g.nv; ++q)
+      da[q] = make_uint2(c->walks.departure.prob[q], c->walks.departure.alias[q]);
+    CK(cudaMemcpy(c->d_woff, g.off.data(), sizeof(uint64_t) * (g.nv + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_wnbr, g.nbr.data(), sizeof(uint32_t) * ne, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_walias, ea.data(), sizeof(uint2) * ne, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_dalias, da.data(), sizeof(uint2) * g.nv, cudaMemcpyHostToDevice));
+  }
+  std::lock_guard<std::mutex> lk(c->mu);
+  const int k = c->pending;
+  const uint64_t have = c->raw_count[k];
+  if (c->opt.max_pool_samples && have + count > c->opt.max_pool_samples)
+    return fail(c, GV_ERR_CAPACITY, "pending pool would exceed max_pool_samples");
+  CK(cudaStreamWaitEvent(c->copy_stream, c->raw_free[k], 0));
+  if (have + count > c->raw[k].cap) {
+    DevBuf<uint2> bigger;
+    CK(bigger.ensure(std::max<uint64_t>(have + count, c->raw[k].cap + c->raw[k].cap / 2)));
+    if (have)
+      CK(cudaMemcpyAsync(bigger.p, c->raw[k].p, have * sizeof(uint2), cudaMemcpyDeviceToDevice,
+                         c->copy_stream));
+    CK(cudaStreamSynchronize(c->copy_stream));
+    c->raw[k].release();
+    c->raw[k] = bigger;
+  }
+  gv::WalkDev wd{c->d_woff, c->d_wnbr, c->d_walias, c->d_dalias, c->nv};
+  CK(gv::launch_augment(wd, walk_len, s, segments, count, seed, c->raw[k].p + have, c->copy_stream));
+  CK(cudaEventRecord(c->raw_ready[k], c->copy_stream));
+  c->raw_count[k] = have + count;
+  return GV_OK;
+}
+
+gv_status gv_debug_get_pending(gv_ctx* c, uint32_t* out, uint64_t cap, uint64_t* count) {
+  if (gv_status st = check_ctx(c, true)) return st;
+  CK(cudaSetDevice(c->opt.device));
+  std::lock_guard<std::mutex> lk(c->mu);
+  const int k = c->pending;
+  if (count) *count = c->raw_count[k];
+  if (!out) return GV_OK;
+  if (cap < c->raw_count[k]) return fail(c, GV_ERR_CAPACITY, "cap < pending pool size");
+  CK(cudaStreamSynchronize(c->copy_stream));
+  CK(cudaMemcpy(out, c->raw[k].p, sizeof(uint2) * c->raw_count[k], cudaMemcpyDeviceToHost));
+  return GV_OK;
+}
+
 gv_status gv_get_partition(gv_ctx* c, uint32_t* perm, uint64_t* part_off) {
   if (gv_status s = check_ctx(c, true)) return s;
   if (perm) std::memcpy(perm, c->part.perm.data(), sizeof(uint32_t) * c->nv);
@@ -1159,6 +1225,10 @@ void gv_destroy(gv_ctx* c) {
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   cudaFree(c->d_packed);
   cudaFree(c->d_alias);
+  cudaFree(c->d_woff);
+  cudaFree(c->d_wnbr);
+  cudaFree(c->d_walias);
+  cudaFree(c->d_dalias);
   cudaFree(c->d_inv_perm);
   if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
   delete c;

@@ -884,6 +884,98 @@ __global__ void init_vertex_kernel(float* __restrict__ vertex, uint32_t stride, 
   reinterpret_cast<float4*>(vertex + row * stride)[c] = v;
 }
 
+// ------------------------------------------------ online augmentation (NEXT-1)
+// One CTA per pool segment t (the device analogue of a sampler thread, Alg. 2
+// P:176-196). The CTA generates walks w = base + tid of segment t in batches
+// of kAugBlock: departure ∝ degree, then walk_len steps ∝ edge weight, with
+// the Philox counter {w, step, t, 'WALK'} (R-AUG) — the same walks the host
+// sampler and the oracle draw. Each thread counts its walk's pairs
+// (0 < b-a <= s, w_a != w_b); a block scan gives each walk's offset k in the
+// segment, and pair k is written straight to its pseudo-shuffled position
+// (sub-block k mod s, index k div s). Batches stop once the
+// segment holds cap pairs, the last walk truncated as on the host.
+constexpr int kAugBlock = 128;
+
+__global__ void __launch_bounds__(kAugBlock) augment_kernel(WalkDev g, uint32_t L, uint32_t s,
+                                                            uint32_t T, uint64_t count,
+                                                            uint32_t key0, uint32_t key1,
+                                                            uint2* __restrict__ out) {
+  extern __shared__ uint32_t sh[];
+  uint32_t* walks = sh;                                  // [kAugBlock][L+1]
+  uint64_t* sub_start =  // [s], 8-byte aligned after the walks
+      reinterpret_cast<uint64_t*>(sh + ((kAugBlock * (L + 1) + 1) & ~1u));
+  __shared__ uint32_t warp_tot[kAugBlock / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t W = L + 1;
+  uint32_t* my = walks + tid * W;  // stride L+1 (odd when L is even: few bank conflicts)
+  for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
+    const uint64_t b = count * t / T, e = count * (t + 1) / T, cap = e - b;
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t acc = 0;
+      for (uint32_t j = 0; j < s; ++j) {
+        sub_start[j] = acc;
+        acc += (cap > j) ? (cap - j + s - 1) / s : 0;
+      }
+    }
+    __syncthreads();
+    uint64_t filled = 0;
+    for (uint32_t base = 0; filled < cap; base += kAugBlock) {
+      const uint32_t w = base + tid;
+      // the walk (departure + L steps)
+      u32x4 r = philox4x32_10(u32x4{w, 0u, t, kTagWalk}, key0, key1);
+      uint32_t slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, g.nv);
+      uint2 pa = __ldg(g.dalias + slot);
+      uint32_t x = alias_pick(pa.x, pa.y, slot, r.z);
+      my[0] = x;
+      for (uint32_t k = 1; k <= L; ++k) {
+        const uint64_t o = __ldg(g.off + x);
+        const uint32_t m = static_cast<uint32_t>(__ldg(g.off + x + 1) - o);
+        r = philox4x32_10(u32x4{w, k, t, kTagWalk}, key0, key1);
+        slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, m);
+        pa = __ldg(g.ealias + o + slot);
+        x = __ldg(g.nbr + o + alias_pick(pa.x, pa.y, slot, r.z));
+        my[k] = x;
+      }
+      // its pair count
+      uint32_t c = 0;
+      for (uint32_t a = 0; a < L; ++a) {
+        const uint32_t xa = my[a], last = min(a + s, L);
+        for (uint32_t bb = a + 1; bb <= last; ++bb) c += (my[bb] != xa);
+      }
+      // block exclusive scan of the counts
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) warp_tot[wid] = incl;
+      __syncthreads();
+      uint32_t before = 0, total = 0;
+#pragma unroll
+      for (int q = 0; q < kAugBlock / 32; ++q) {
+        if (q < wid) before += warp_tot[q];
+        total += warp_tot[q];
+      }
+      uint64_t k = filled + before + (incl - c);
+      // write this walk's pairs at their pseudo-shuffled positions
+      for (uint32_t a = 0; a < L && k < cap; ++a) {
+        const uint32_t xa = my[a], last = min(a + s, L);
+        for (uint32_t bb = a + 1; bb <= last && k < cap; ++bb) {
+          const uint32_t xb = my[bb];
+          if (xb == xa) continue;
+          const uint32_t j = static_cast<uint32_t>(k % s);
+          out[b + sub_start[j] + k / s] = make_uint2(xa, xb);
+          ++k;
+        }
+      }
+      filled += total;
+      __syncthreads();  // warp_tot reuse
+    }
+  }
+}
+
 // ---------------------------------------------------------------- bucketing
 
 struct BinCtx {
@@ -1262,6 +1354,23 @@ cudaError_t launch_segmented_copy(const uint2* src, uint2* dst, const CopySeg* s
   if (nseg == 0) return cudaSuccess;
   dim3 grid(64, static_cast<unsigned>(nseg));
   segmented_copy_kernel<<<grid, 256, 0, s>>>(src, dst, segs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_augment(const WalkDev& g, uint32_t walk_len, uint32_t s, uint32_t segments,
+                           uint64_t count, uint64_t seed, uint2* out, cudaStream_t st) {
+  if (count == 0 || segments == 0) return cudaSuccess;
+  const size_t smem = static_cast<size_t>(kAugBlock) * (walk_len + 1) * 4 + 8 + 8 * s;
+  static size_t set = 0;
+  if (smem > 48 * 1024 && smem > set) {
+    cudaFuncSetAttribute(augment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    set = smem;
+  }
+  const unsigned grid = std::min<uint32_t>(segments, static_cast<uint32_t>(num_sms()) * 16);
+  augment_kernel<<<grid, kAugBlock, smem, st>>>(g, walk_len, s, segments, count,
+                                                static_cast<uint32_t>(seed),
+                                                static_cast<uint32_t>(seed >> 32), out);
   return cudaGetLastError();
 }
 

@@ -63,6 +63,19 @@ cudaError_t launch_init_vertex(float* vertex, uint32_t stride, uint32_t dim, uin
                                uint64_t rows, const uint32_t* inv_perm, uint32_t key0,
                                uint32_t key1, cudaStream_t s);
 
+// ---- online augmentation on the device (NEXT-1) ----
+struct WalkDev {
+  const uint64_t* off;   // CSR offsets over ORIGINAL ids (nv + 1)
+  const uint32_t* nbr;   // neighbours
+  const uint2* ealias;   // per CSR entry {prob, alias}: neighbour tables
+  const uint2* dalias;   // per node {prob, alias}: departure table (weight = degree)
+  uint32_t nv;
+};
+// Appends `count` pairs (ORIGINAL ids) to out: `segments` pool segments as in
+// gv_augment with threads = segments (reading R-AUG), one CTA per segment.
+cudaError_t launch_augment(const WalkDev& g, uint32_t walk_len, uint32_t s, uint32_t segments,
+                           uint64_t count, uint64_t seed, uint2* out, cudaStream_t st);
+
 // ---- bucketing ----
 struct BucketPlan {
   uint32_t n;         // partitions

@@ -36,6 +36,28 @@ extern "C" gv_status gv_run(gv_ctx* c, const gv_augment_cfg* cfg, uint64_t total
   const uint64_t npools = (total_samples + P - 1) / P;
   gv_run_report rep;
   std::memset(&rep, 0, sizeof(rep));
+  auto pool_count = [&](uint64_t k) { return std::min<uint64_t>(P, total_samples - k * P); };
+  const auto t0 = Clock::now();
+  gv_status status = GV_OK;
+  gv_episode_stats st;
+  if (cfg->device) {
+    // GPU-resident pipeline (NEXT-1): pool k+1 is generated on the copy
+    // stream while pool k trains on the compute stream.
+    status = gv_augment_device(c, cfg->walk_len, cfg->s, cfg->threads, pool_count(0), cfg->seed);
+    for (uint64_t k = 0; k < npools && status == GV_OK; ++k) {
+      status = gv_train_episode(c, nullptr);
+      if (status == GV_OK && k + 1 < npools)
+        status = gv_augment_device(c, cfg->walk_len, cfg->s, cfg->threads, pool_count(k + 1),
+                                   cfg->seed + k + 1);
+      if (status == GV_OK && !cfg->collaborate) status = gv_synchronize(c);
+    }
+    if (status == GV_OK) status = gv_synchronize(c);
+    rep.pools = npools;
+    rep.samples = total_samples;
+    rep.wall_ms = ms_since(t0);
+    if (report) *report = rep;
+    return status;
+  }
   HostPool pool[2];
   for (auto& p : pool)
     if (cudaMallocHost(&p.pairs, 2 * P * sizeof(uint32_t)) != cudaSuccess) {
@@ -43,10 +65,6 @@ extern "C" gv_status gv_run(gv_ctx* c, const gv_augment_cfg* cfg, uint64_t total
         if (q.pairs) cudaFreeHost(q.pairs);
       return GV_ERR_NOMEM;
     }
-  auto pool_count = [&](uint64_t k) { return std::min<uint64_t>(P, total_samples - k * P); };
-  const auto t0 = Clock::now();
-  gv_status status = GV_OK;
-  gv_episode_stats st;
   if (!cfg->collaborate) {
     for (uint64_t k = 0; k < npools && status == GV_OK; ++k) {
       const auto tp = Clock::now();

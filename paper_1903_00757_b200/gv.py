@@ -60,7 +60,8 @@ class gv_step_plan(C.Structure):
 
 class gv_augment_cfg(C.Structure):
     _fields_ = [("walk_len", C.c_uint32), ("s", C.c_uint32), ("threads", C.c_uint32),
-                ("pool_samples", C.c_uint64), ("seed", C.c_uint64), ("collaborate", C.c_int)]
+                ("pool_samples", C.c_uint64), ("seed", C.c_uint64), ("collaborate", C.c_int),
+                ("device", C.c_int)]
 
 
 class gv_run_report(C.Structure):
@@ -100,6 +101,8 @@ SIGNATURES = {
     "gv_get_stream": (st, [ctx_p, C.c_int, C.POINTER(C.c_size_t)]),
     "gv_augment": (st, [ctx_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, u32p]),
     "gv_run": (st, [ctx_p, C.POINTER(gv_augment_cfg), C.c_uint64, C.POINTER(gv_run_report)]),
+    "gv_augment_device": (st, [ctx_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64]),
+    "gv_debug_get_pending": (st, [ctx_p, u32p, C.c_uint64, u64p]),
     "gv_get_partition": (st, [ctx_p, u32p, u64p]),
     "gv_get_alias": (st, [ctx_p, C.c_uint32, u32p, u32p, C.c_uint64]),
     "gv_prepare_episode": (st, [ctx_p]),
@@ -254,8 +257,23 @@ def gv_augment(ctx, walk_len, s, threads, count, seed, out=None):
     return out
 
 
-def gv_run(ctx, walk_len, s, threads, pool_samples, seed, total_samples, collaborate=True):
-    cfg = gv_augment_cfg(walk_len, s, threads, pool_samples, seed, 1 if collaborate else 0)
+def gv_augment_device(ctx, walk_len, s, segments, count, seed):
+    """Generate a pool on the GPU and append it to the pending pool (NEXT-1)."""
+    _ck(lib.gv_augment_device(ctx, walk_len, s, segments, count, seed), ctx)
+
+
+def gv_debug_get_pending(ctx):
+    n = C.c_uint64(0)
+    _ck(lib.gv_debug_get_pending(ctx, None, 0, C.byref(n)), ctx)
+    out = np.empty((max(n.value, 1), 2), np.uint32)
+    _ck(lib.gv_debug_get_pending(ctx, _ptr(out, u32p), n.value, C.byref(n)), ctx)
+    return out[:n.value]
+
+
+def gv_run(ctx, walk_len, s, threads, pool_samples, seed, total_samples, collaborate=True,
+           device=False):
+    cfg = gv_augment_cfg(walk_len, s, threads, pool_samples, seed, 1 if collaborate else 0,
+                         1 if device else 0)
     rep = gv_run_report()
     _ck(lib.gv_run(ctx, C.byref(cfg), total_samples, C.byref(rep)), ctx)
     return rep.as_dict()
@@ -363,6 +381,9 @@ class GraphVite:
     def train_episode(self, stats=True):
         return gv_train_episode(self.ctx, stats)
 
+    def synchronize(self):
+        gv_synchronize(self.ctx)
+
     def read_stats(self):
         return gv_read_stats(self.ctx)
 
@@ -383,6 +404,9 @@ class GraphVite:
 
     def augment(self, walk_len, s, threads, count, seed, out=None):
         return gv_augment(self.ctx, walk_len, s, threads, count, seed, out)
+
+    def augment_device(self, walk_len, s, segments, count, seed):
+        gv_augment_device(self.ctx, walk_len, s, segments, count, seed)
 
     def partition(self):
         return gv_get_partition(self.ctx, self.nv, self.n)

@@ -235,3 +235,43 @@ def test_hogwild_auc_matches_oracle():
     assert min(auc_o.values()) >= 0.8, auc_o
     for (n, vr), auc in res.items():
         assert abs(auc - auc_o[n]) <= 0.01, (n, vr, auc, auc_o[n])
+
+
+@pytest.mark.parametrize("segments,s,count,L", [(1, 1, 1000, 40), (7, 2, 100_003, 40),
+                                                (1184, 5, 2_000_000, 40), (64, 3, 50_000, 10),
+                                                (3, 5, 17, 5)])
+def test_device_augmentation_bitexact(c1_graph, segments, s, count, L):
+    """NEXT-1: the pool generated on the GPU (one CTA per segment) equals the
+    oracle's augmentation with threads = segments, byte for byte, ragged
+    segment sizes and truncated last walks included."""
+    src, dst = c1_graph
+    p = G.GraphVite(C1["nv"], 8, 1)
+    p.load_edges(src, dst)
+    p.augment_device(L, s, segments, count, 4242)
+    got = G.gv_debug_get_pending(p.ctx)
+    ref = O.Sampler(O.Graph(C1["nv"], src, dst)).augment(L, s, segments, count, 4242)
+    assert np.array_equal(got, ref)
+    # appending a second pool keeps the first intact
+    p.augment_device(L, s, segments, 1000, 7)
+    got2 = G.gv_debug_get_pending(p.ctx)
+    assert np.array_equal(got2[:count], ref) and len(got2) == count + 1000
+    p.close()
+
+
+def test_device_pipeline_matches_oracle(c1_graph):
+    """gv_run with device augmentation (pool k+1 generated while pool k
+    trains), ordered kernel: equals the oracle fed with its own augmentation."""
+    src, dst = c1_graph
+    P, pools, segs = 300_000, 3, 96
+    g = G.GraphVite(C1["nv"], 64, 2, 1, 0.025, total_samples=P * pools, ordered=1)
+    g.load_edges(src, dst)
+    rep = G.gv_run(g.ctx, 40, 2, segs, P, 99, P * pools, device=True)
+    assert rep["pools"] == pools
+    o = O.Trainer(C1["nv"], 64, 2, K=1, lr0=0.025, lr_kind=1, total_samples=P * pools)
+    o.load_edges(src, dst)
+    sampler = O.Sampler(O.Graph(C1["nv"], src, dst))
+    for k in range(pools):
+        o.train_pool(sampler.augment(40, 2, segs, P, 99 + k))
+    assert _rel(g.vertex(), o.get("vertex")) <= 1e-5
+    assert _rel(g.context(), o.get("context")) <= 1e-5
+    g.close()
