@@ -98,6 +98,9 @@ typedef struct {
   int compute_loss;       /* 1 = accumulate the per-sample loss (default 1)       */
   int host_threads;       /* threads for host graph preparation (0 = all cores)   */
   uint64_t max_pool_samples; /* per rank; 0 = grow on demand                      */
+  int transport;          /* world_size > 1: 0 = CUDA IPC peer copies with a shared-
+                             memory handshake (default; also runs several ranks on
+                             one GPU), 1 = NCCL send/recv                          */
 } gv_options;
 
 /* Per-pool statistics of THIS process (all its virtual ranks). Times are
@@ -123,7 +126,7 @@ typedef struct {
 
 /* Fills *opt with defaults: seed 5, init_seed 4 (SURVEY §8(d) seeds),
  * neg_weight 5, device 0, rank 0, world_size 1, virtual_ranks 1, ordered 0,
- * compute_loss 1, host_threads 0, max_pool_samples 0. */
+ * compute_loss 1, host_threads 0, max_pool_samples 0, transport 0. */
 void gv_default_options(gv_options* opt);
 
 /* Create a trainer for |V| = num_nodes nodes with dim-dimensional vertex and
@@ -144,7 +147,9 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
 
 /* Multi-process only (world_size > 1): rank 0 calls gv_comm_unique_id, the
  * caller broadcasts the 128 bytes to every rank (e.g. torch.distributed),
- * then every rank calls gv_comm_init before gv_load_edges. */
+ * then every rank calls gv_comm_init before gv_load_edges. With the IPC
+ * transport gv_load_edges also waits until every rank has loaded the graph
+ * (peers map each other's context buffers). Errors: GV_ERR_COMM. */
 gv_status gv_comm_unique_id(uint8_t id_out[128]);
 gv_status gv_comm_init(gv_ctx* ctx, const uint8_t id[128]);
 

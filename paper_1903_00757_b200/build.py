@@ -24,8 +24,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3,-Wall",
           "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
-SOURCES = ["kernels.cu", "engine.cpp", "host_graph.cpp", "augment.cpp", "run.cpp"]
-HEADERS = ["kernels.cuh", "philox.cuh", "host_graph.hpp", "augment.hpp"]
+SOURCES = ["kernels.cu", "engine.cpp", "host_graph.cpp", "augment.cpp", "run.cpp", "ipc.cpp"]
+HEADERS = ["kernels.cuh", "philox.cuh", "host_graph.hpp", "augment.hpp", "ipc.hpp"]
 
 
 def _newest_dep():
@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if log:
                 print(log, file=sys.stderr)
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-ldl", "-lpthread"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-ldl", "-lpthread", "-lrt"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -11,6 +11,7 @@
 // With m = 1 this is Alg. 3's train -> rotate -> train ring.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/mman.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -29,6 +30,7 @@
 #include "../../include/gv.h"
 #include "augment.hpp"
 #include "host_graph.hpp"
+#include "ipc.hpp"
 #include "kernels.cuh"
 
 namespace {
@@ -74,7 +76,8 @@ NcclApi& nccl() {
 template <class T>
 struct DevBuf {
   T* p = nullptr;
-  size_t cap = 0;  // elements
+  size_t cap = 0;     // elements
+  uint64_t gen = 0;   // bumped by every (re)allocation
   size_t bytes_total() const { return cap * sizeof(T); }
   cudaError_t ensure(size_t n) {
     if (n <= cap) return cudaSuccess;
@@ -82,7 +85,10 @@ struct DevBuf {
     p = nullptr;
     cap = 0;
     cudaError_t e = cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T));
-    if (e == cudaSuccess) cap = std::max<size_t>(n, 1);
+    if (e == cudaSuccess) {
+      cap = std::max<size_t>(n, 1);
+      ++gen;
+    }
     return e;
   }
   void release() {
@@ -178,6 +184,22 @@ struct gv_ctx {
   std::vector<Rank> ranks;
   ncclComm_t comm = nullptr;
   bool comm_ready = false;
+  // CUDA-IPC transport (world_size > 1, transport 0)
+  gv::IpcShm* shm = nullptr;
+  std::string shm_name;
+  float* peer_ctx[gv::kIpcMaxRanks] = {};
+  uint2* peer_blocks[gv::kIpcMaxRanks] = {};
+  uint64_t peer_blocks_gen[gv::kIpcMaxRanks] = {};
+  cudaEvent_t peer_ev_pull[gv::kIpcMaxRanks][2] = {};
+  cudaEvent_t peer_ev_first[gv::kIpcMaxRanks][gv::kIpcEvRing] = {};
+  cudaEvent_t peer_ev_rot[gv::kIpcMaxRanks][gv::kIpcEvRing] = {};
+  cudaEvent_t my_ev_pull[2] = {};
+  cudaEvent_t my_ev_first[gv::kIpcEvRing] = {};
+  cudaEvent_t my_ev_rot[gv::kIpcEvRing] = {};
+  uint64_t exported_blocks_gen = 0;
+  double ipc_timeout = 300.0;
+  bool ipc() const { return opt.world_size > 1 && opt.transport == 0; }
+  bool use_nccl() const { return opt.world_size > 1 && opt.transport == 1; }
 };
 
 namespace {
@@ -271,6 +293,19 @@ gv_status prepare(gv_ctx* c) {
     const gv::BucketPlan plan = gv::make_bucket_plan(n, r.seg_count);
     CK(r.scratch.ensure(gv::bucket_scratch_bytes(plan)));
     DevBuf<uint2>& out = (c->D == 1) ? r.blocks : r.local_blocks;
+    if (c->ipc() && c->pool_index > 0) {
+      // peers pulled their chunks of the previous pool out of local_blocks
+      const uint64_t e = c->pool_index;
+      const bool realloc = out.cap < r.seg_count;
+      for (int q = 0; q < c->D; ++q) {
+        if (q == r.d) continue;
+        if (!gv::ipc_wait(c->shm->rank[q].pull_epoch, e, c->ipc_timeout))
+          return fail(c, GV_ERR_COMM, "IPC timeout waiting for a peer's block pulls");
+        cudaEvent_t ev = c->peer_ev_pull[q][(e - 1) & 1];
+        if (realloc) CK(cudaEventSynchronize(ev));  // the old buffer is freed below
+        else CK(cudaStreamWaitEvent(r.compute, ev, 0));
+      }
+    }
     CK(out.ensure(r.seg_count));
     CK(cudaMemsetAsync(r.counts.p + bins + 1, 0, sizeof(uint64_t), r.compute));
     CK(gv::launch_bucket(c->raw[a].p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
@@ -289,7 +324,26 @@ gv_status prepare(gv_ctx* c) {
   }
   // 2) counts to the host (NCCL: all-gather first)
   std::vector<std::vector<uint64_t>> cnt(c->D, std::vector<uint64_t>(bins + 2, 0));
-  if (c->opt.world_size > 1) {
+  if (c->ipc()) {
+    Rank& r = c->ranks[0];
+    const uint64_t e = c->pool_index;
+    CK(cudaMemcpyAsync(r.counts_host, r.counts.p, sizeof(uint64_t) * (bins + 2),
+                       cudaMemcpyDeviceToHost, r.compute));
+    CK(cudaStreamSynchronize(r.compute));
+    gv::IpcRankShm& me = c->shm->rank[r.d];
+    std::memcpy(me.counts[e & 1], r.counts_host, sizeof(uint64_t) * (bins + 2));
+    if (c->exported_blocks_gen != r.local_blocks.gen) {  // (re)allocated: export again
+      CK(cudaIpcGetMemHandle(&me.blocks_handle, r.local_blocks.p));
+      me.blocks_gen = me.blocks_gen + 1;
+      c->exported_blocks_gen = r.local_blocks.gen;
+    }
+    me.counts_epoch.store(e + 1, std::memory_order_release);
+    for (int q = 0; q < c->D; ++q) {
+      if (!gv::ipc_wait(c->shm->rank[q].counts_epoch, e + 1, c->ipc_timeout))
+        return fail(c, GV_ERR_COMM, "IPC timeout waiting for a peer's bucket counts");
+      std::memcpy(cnt[q].data(), c->shm->rank[q].counts[e & 1], sizeof(uint64_t) * (bins + 2));
+    }
+  } else if (c->use_nccl()) {
     Rank& r = c->ranks[0];
     NK(nccl().AllGather(r.counts.p, r.all_counts.p, bins + 2, ncclUint64, c->comm, r.compute));
     CK(cudaMemcpyAsync(r.counts_host, r.all_counts.p, sizeof(uint64_t) * (bins + 2) * c->D,
@@ -347,7 +401,35 @@ gv_status prepare(gv_ctx* c) {
       CK(r.recv.ensure(total));
       CK(r.blocks.ensure(total));
     }
-    if (c->opt.world_size > 1) {
+    if (c->ipc()) {
+      // pull: rank d copies each source's chunk out of the source's local blocks
+      Rank& r = c->ranks[0];
+      const uint64_t e = c->pool_index;
+      uint64_t roff = 0;
+      for (int q = 0; q < c->D; ++q) {
+        const uint64_t len = chunk_len(q, r.d);
+        const uint2* src = nullptr;
+        if (q == r.d) {
+          src = r.local_blocks.p;
+        } else if (len) {
+          gv::IpcRankShm& pr = c->shm->rank[q];
+          if (c->peer_blocks_gen[q] != pr.blocks_gen) {
+            if (c->peer_blocks[q]) CK(cudaIpcCloseMemHandle(c->peer_blocks[q]));
+            void* ptr = nullptr;
+            CK(cudaIpcOpenMemHandle(&ptr, pr.blocks_handle, cudaIpcMemLazyEnablePeerAccess));
+            c->peer_blocks[q] = static_cast<uint2*>(ptr);
+            c->peer_blocks_gen[q] = pr.blocks_gen;
+          }
+          src = c->peer_blocks[q];
+        }
+        if (len)
+          CK(cudaMemcpyAsync(r.recv.p + roff, src + chunk_begin(q, r.d), len * sizeof(uint2),
+                             cudaMemcpyDeviceToDevice, r.compute));
+        roff += len;
+      }
+      CK(cudaEventRecord(c->my_ev_pull[e & 1], r.compute));
+      c->shm->rank[r.d].pull_epoch.store(e + 1, std::memory_order_release);
+    } else if (c->use_nccl()) {
       Rank& r = c->ranks[0];
       NK(nccl().GroupStart());
       uint64_t roff = 0;
@@ -513,12 +595,50 @@ gv_status run_steps(gv_ctx* c) {
         }
         gv_status st = launch(g, 1);
         if (st) return st;
-        if (g == 0) CK(cudaEventRecord(r.ev_first_done[t], r.compute));
+        if (g == 0) {
+          CK(cudaEventRecord(r.ev_first_done[t], r.compute));
+          if (c->ipc()) {  // publish "block 0 of global step gs done" and the slot to pull
+            const uint64_t gs = c->pool_index * n + t;
+            CK(cudaEventRecord(c->my_ev_first[gs % gv::kIpcEvRing], r.compute));
+            gv::IpcRankShm& me = c->shm->rank[r.d];
+            me.first_slot[gs % gv::kIpcSlotRing] = static_cast<uint32_t>(r.slot_of[plan.send_part]);
+            me.first_epoch.store(gs + 1, std::memory_order_release);
+          }
+        }
       }
     }
     if (c->D == 1) continue;
     // rotation of step t (a8): rank d sends partition (d m + t) to rank d-1
-    if (c->opt.world_size > 1) {
+    if (c->ipc()) {
+      // receiver pulls: rank d copies recv_part out of rank d+1's context slots
+      Rank& r = c->ranks[0];
+      gv_step_plan plan;
+      gv_plan_step(n, c->D, r.d, t, &plan);
+      const uint64_t gs = c->pool_index * n + t;
+      const int src = static_cast<int>(plan.recv_from), prev = static_cast<int>(plan.send_to);
+      gv::IpcRankShm& ps = c->shm->rank[src];
+      if (!gv::ipc_wait(ps.first_epoch, gs + 1, c->ipc_timeout))
+        return fail(c, GV_ERR_COMM, "IPC timeout waiting for the successor's first block");
+      const uint32_t peer_slot = ps.first_slot[gs % gv::kIpcSlotRing];
+      CK(cudaStreamWaitEvent(r.comm, c->peer_ev_first[src][gs % gv::kIpcEvRing], 0));
+      if (gs > 0) {  // our free slot was pulled by the predecessor at the previous step
+        if (!gv::ipc_wait(c->shm->rank[prev].rot_epoch, gs, c->ipc_timeout))
+          return fail(c, GV_ERR_COMM, "IPC timeout waiting for the predecessor's rotation");
+        CK(cudaStreamWaitEvent(r.comm, c->peer_ev_rot[prev][(gs - 1) % gv::kIpcEvRing], 0));
+      }
+      const uint32_t out_p = plan.send_part, in_p = plan.recv_part;
+      CK(cudaMemcpyAsync(
+          r.context + static_cast<uint64_t>(r.free_slot) * r.slot_rows * c->stride,
+          c->peer_ctx[src] + static_cast<uint64_t>(peer_slot) * r.slot_rows * c->stride,
+          psize(c, in_p) * c->stride * sizeof(float), cudaMemcpyDeviceToDevice, r.comm));
+      CK(cudaEventRecord(c->my_ev_rot[gs % gv::kIpcEvRing], r.comm));
+      c->shm->rank[r.d].rot_epoch.store(gs + 1, std::memory_order_release);
+      CK(cudaEventRecord(r.ev_recv[t], r.comm));
+      const int s_out = r.slot_of[out_p];
+      r.slot_of[in_p] = r.free_slot;
+      r.slot_of[out_p] = -1;
+      r.free_slot = s_out;
+    } else if (c->use_nccl()) {
       Rank& r = c->ranks[0];
       gv_step_plan plan;
       gv_plan_step(n, c->D, r.d, t, &plan);
@@ -681,7 +801,46 @@ gv_status setup_device(gv_ctx* c) {
     r.ev_exch_sent = new_event(false);
     CK(cudaEventRecord(r.ev_recv_consumed, r.compute));
   }
-  return sync_all(c);
+  gv_status st = sync_all(c);
+  if (st || !c->ipc()) return st;
+  // IPC transport: export the context buffer and the events, map the peers'
+  Rank& r = c->ranks[0];
+  gv::IpcRankShm& me = c->shm->rank[r.d];
+  const unsigned fl = cudaEventInterprocess | cudaEventDisableTiming;
+  for (int k = 0; k < 2; ++k) {
+    CK(cudaEventCreateWithFlags(&c->my_ev_pull[k], fl));
+    CK(cudaIpcGetEventHandle(&me.ev_pull[k], c->my_ev_pull[k]));
+  }
+  for (int k = 0; k < gv::kIpcEvRing; ++k) {
+    CK(cudaEventCreateWithFlags(&c->my_ev_first[k], fl));
+    CK(cudaEventCreateWithFlags(&c->my_ev_rot[k], fl));
+    CK(cudaIpcGetEventHandle(&me.ev_first[k], c->my_ev_first[k]));
+    CK(cudaIpcGetEventHandle(&me.ev_rot[k], c->my_ev_rot[k]));
+  }
+  CK(cudaIpcGetMemHandle(&me.ctx_handle, r.context));
+  me.joined.store(1, std::memory_order_release);
+  for (int q = 0; q < c->D; ++q) {
+    if (!gv::ipc_wait(c->shm->rank[q].joined, 1, c->ipc_timeout))
+      return fail(c, GV_ERR_COMM, "IPC timeout waiting for the peers to load the graph");
+    if (q == r.d) continue;
+    gv::IpcRankShm& pr = c->shm->rank[q];
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, pr.ctx_handle, cudaIpcMemLazyEnablePeerAccess));
+    c->peer_ctx[q] = static_cast<float*>(ptr);
+    for (int k = 0; k < 2; ++k) CK(cudaIpcOpenEventHandle(&c->peer_ev_pull[q][k], pr.ev_pull[k]));
+    for (int k = 0; k < gv::kIpcEvRing; ++k) {
+      CK(cudaIpcOpenEventHandle(&c->peer_ev_first[q][k], pr.ev_first[k]));
+      CK(cudaIpcOpenEventHandle(&c->peer_ev_rot[q][k], pr.ev_rot[k]));
+    }
+  }
+  me.joined.store(2, std::memory_order_release);
+  if (r.d == 0) {  // everyone mapped everything: the name is no longer needed
+    for (int q = 0; q < c->D; ++q)
+      if (!gv::ipc_wait(c->shm->rank[q].joined, 2, c->ipc_timeout))
+        return fail(c, GV_ERR_COMM, "IPC timeout in the init handshake");
+    shm_unlink(c->shm_name.c_str());
+  }
+  return GV_OK;
 }
 
 gv_status check_ctx(gv_ctx* c, bool need_loaded) {
@@ -708,6 +867,7 @@ void gv_default_options(gv_options* o) {
   o->compute_loss = 1;
   o->host_threads = 0;
   o->max_pool_samples = 0;
+  o->transport = 0;
 }
 
 int gv_abi_version(void) { return GV_ABI_VERSION; }
@@ -749,6 +909,8 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
   const int D = o.world_size * o.virtual_ranks;
   if (n_partitions % D != 0)
     return fail(nullptr, GV_ERR_INVALID_ARG, "n_partitions must be a multiple of the rank count");
+  if (o.transport != 0 && o.transport != 1)
+    return fail(nullptr, GV_ERR_INVALID_ARG, "transport must be 0 (CUDA IPC) or 1 (NCCL)");
   if (alpha && (alpha->kind != GV_LR_CONSTANT && alpha->kind != GV_LR_LINEAR))
     return fail(nullptr, GV_ERR_INVALID_ARG, "bad lr schedule kind");
   int ndev = 0;
@@ -783,10 +945,18 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
 
 gv_status gv_comm_unique_id(uint8_t id_out[128]) {
   gv_ctx* c = nullptr;
-  if (!nccl().ok) return fail(nullptr, GV_ERR_COMM, "libnccl.so.2 not loadable");
-  ncclUniqueId id;
-  NK(nccl().GetUniqueId(&id));
-  std::memcpy(id_out, id.internal, 128);
+  if (nccl().ok) {  // an NCCL id also names the IPC segment (it carries random bytes)
+    ncclUniqueId id;
+    NK(nccl().GetUniqueId(&id));
+    std::memcpy(id_out, id.internal, 128);
+    return GV_OK;
+  }
+  FILE* f = fopen("/dev/urandom", "rb");
+  if (!f || fread(id_out, 1, 128, f) != 128) {
+    if (f) fclose(f);
+    return fail(nullptr, GV_ERR_COMM, "no NCCL and no /dev/urandom for a unique id");
+  }
+  fclose(f);
   return GV_OK;
 }
 
@@ -794,8 +964,18 @@ gv_status gv_comm_init(gv_ctx* c, const uint8_t id[128]) {
   if (gv_status s = check_ctx(c, false)) return s;
   if (c->opt.world_size <= 1) return fail(c, GV_ERR_STATE, "gv_comm_init needs world_size > 1");
   if (c->loaded || c->comm_ready) return fail(c, GV_ERR_STATE, "call gv_comm_init before gv_load_edges, once");
-  if (!nccl().ok) return fail(c, GV_ERR_COMM, "libnccl.so.2 not loadable");
   CK(cudaSetDevice(c->opt.device));
+  if (c->ipc()) {
+    if (c->D > gv::kIpcMaxRanks || c->n * c->n + 2 > static_cast<uint32_t>(gv::kIpcMaxBins))
+      return fail(c, GV_ERR_INVALID_ARG, "IPC transport: at most 16 ranks and 64 partitions");
+    std::string err;
+    c->shm = gv::ipc_open(id, &c->shm_name, &err);
+    if (!c->shm) return fail(c, GV_ERR_COMM, err);
+    if (const char* t = getenv("GV_IPC_TIMEOUT")) c->ipc_timeout = atof(t);
+    c->comm_ready = true;
+    return GV_OK;
+  }
+  if (!nccl().ok) return fail(c, GV_ERR_COMM, "libnccl.so.2 not loadable");
   ncclUniqueId uid;
   std::memcpy(uid.internal, id, 128);
   NK(nccl().CommInitRank(&c->comm, c->opt.world_size, uid, c->opt.rank));
@@ -1231,6 +1411,14 @@ void gv_destroy(gv_ctx* c) {
   cudaFree(c->d_dalias);
   cudaFree(c->d_inv_perm);
   if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
+  for (int q = 0; q < gv::kIpcMaxRanks; ++q) {
+    if (c->peer_ctx[q]) cudaIpcCloseMemHandle(c->peer_ctx[q]);
+    if (c->peer_blocks[q]) cudaIpcCloseMemHandle(c->peer_blocks[q]);
+  }
+  for (cudaEvent_t e : c->my_ev_pull) if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->my_ev_first) if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->my_ev_rot) if (e) cudaEventDestroy(e);
+  if (c->shm) gv::ipc_close(c->shm, c->shm_name, false);
   delete c;
 }
 

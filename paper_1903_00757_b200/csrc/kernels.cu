@@ -133,6 +133,12 @@ __device__ __forceinline__ void axpy(Row<CH>& y, float g, const Row<CH>& x) {
   }
 }
 
+// log(1 + e) for e = exp(-x): -x once e overflows (x < -88), so the
+// monitoring loss stays finite.
+__device__ __forceinline__ float softplus_e(float e, float x) {
+  return e > 1e30f ? -x : __logf(1.0f + e);
+}
+
 // One target of a sample: p = s(x) = 1/(1+exp(-x)) (IEEE expf, correctly
 // rounded reciprocal), g = (y - p) lr w, err += g C, C += g U. Returns the
 // target's loss -log s(+-x) = log(1+e^-x) (+ x for a negative) when wanted.
@@ -146,7 +152,7 @@ __device__ __forceinline__ float apply_target(float x, bool positive, float lr, 
   g_out = g;
   axpy<CH>(err, g, Ct);
   axpy<CH>(Ct, g, U);
-  return want_loss ? (__logf(1.0f + e) + (positive ? 0.0f : x)) : 0.0f;
+  return want_loss ? (softplus_e(e, x) + (positive ? 0.0f : x)) : 0.0f;
 }
 
 // Process up to 32 samples whose ids sit one per lane (lane s holds sample s):
@@ -430,7 +436,7 @@ __device__ __forceinline__ float run_chunk_half(int nvalid, uint32_t my_u, const
         axpy2(err, g[t], C[t]);
         red_row2(context, c[t], stride, hl, dim4, g[t], U, act);
         axpy2(C[t], g[t], U);
-        if (want_loss && act) loss += __logf(1.0f + e) + (t == 0 ? 0.0f : x[t]);
+        if (want_loss && act) loss += softplus_e(e, x[t]) + (t == 0 ? 0.0f : x[t]);
       }
     } else {
 #pragma unroll
@@ -445,7 +451,7 @@ __device__ __forceinline__ float run_chunk_half(int nvalid, uint32_t my_u, const
         axpy2(err, g[t], C[t]);
         red_row2(context, c[t], stride, hl, dim4, g[t], U, act);
         axpy2(C[t], g[t], U);
-        if (want_loss && act) loss += __logf(1.0f + e) + (t == 0 ? 0.0f : x);
+        if (want_loss && act) loss += softplus_e(e, x) + (t == 0 ? 0.0f : x);
       }
     }
 #pragma unroll
@@ -700,7 +706,7 @@ __device__ __forceinline__ float run_ring_half(const SgdArgs& a, const WarpSeq& 
         axpy2(err, g, C[t]);
         red_row2_hint(context, c[t], stride, hl, dim4, g, U, act,
                       ((hot >> (1 + t)) & 1u) ? pol_hot : pol_cold);
-        if (want_loss && act) loss += __logf(1.0f + e) + (t == 0 ? 0.0f : x[t]);
+        if (want_loss && act) loss += softplus_e(e, x[t]) + (t == 0 ? 0.0f : x[t]);
       }
     } else {
       // a target repeated inside the sample sees the earlier target's update (R-DUP)
@@ -717,7 +723,7 @@ __device__ __forceinline__ float run_ring_half(const SgdArgs& a, const WarpSeq& 
         red_row2_hint(context, c[t], stride, hl, dim4, g, U, act,
                       ((hot >> (1 + t)) & 1u) ? pol_hot : pol_cold);
         axpy2(C[t], g, U);
-        if (want_loss && act) loss += __logf(1.0f + e) + (t == 0 ? 0.0f : x);
+        if (want_loss && act) loss += softplus_e(e, x) + (t == 0 ? 0.0f : x);
       }
     }
     red_row2_hint(vertex, u, stride, hl, dim4, 1.0f, err, act, (hot & 1u) ? pol_hot : pol_cold);

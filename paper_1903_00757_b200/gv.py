@@ -38,7 +38,8 @@ class gv_options(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("init_seed", C.c_uint64), ("neg_weight", C.c_float),
                 ("device", C.c_int), ("rank", C.c_int), ("world_size", C.c_int),
                 ("virtual_ranks", C.c_int), ("ordered", C.c_int), ("compute_loss", C.c_int),
-                ("host_threads", C.c_int), ("max_pool_samples", C.c_uint64)]
+                ("host_threads", C.c_int), ("max_pool_samples", C.c_uint64),
+                ("transport", C.c_int)]
 
 
 class gv_episode_stats(C.Structure):

@@ -1,0 +1,76 @@
+"""Multi-process path (world_size > 1, one process per rank) on ONE GPU:
+the ranks are processes sharing cuda:0 and talk through the CUDA-IPC
+transport (peer copies of bucket chunks and context partitions, IPC events,
+a shared-memory handshake). In ordered mode the gathered embeddings must
+equal the serial oracle within 1e-5 (every row sees the oracle's update
+sequence); in Hogwild mode they must be finite and training must progress."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+from paper_1903_00757_b200 import gv as G  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(tmp_path, world, n, pools, count, ordered, nv=4000, ne=20_000):
+    uid = G.gv_comm_unique_id().hex()
+    worker = os.path.join(ROOT, "tests", "_mp_worker.py")
+    outs = [str(tmp_path / f"r{r}.npz") for r in range(world)]
+    env = dict(os.environ, GV_IPC_TIMEOUT="120")
+    procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), uid, str(n), str(pools),
+                               str(count), str(ordered), outs[r], str(nv), str(ne)], env=env)
+             for r in range(world)]
+    codes = [p.wait(timeout=600) for p in procs]
+    assert codes == [0] * world, codes
+    d = 32
+    V = np.full((nv, d), np.nan, np.float32)
+    C = np.full((nv, d), np.nan, np.float32)
+    losses = []
+    for f in outs:
+        z = np.load(f)
+        V[z["ids"]] = z["vertex"]
+        C[z["ids"]] = z["context"]
+        losses.append(z["loss"])
+    assert not np.isnan(V).any() and not np.isnan(C).any()  # the ranks' rows tile the matrix
+    return V, C, np.sum(losses, axis=0)
+
+
+def _oracle(n, pools, count, nv=4000, ne=20_000):
+    src, dst = synth.chung_lu(nv, ne, gamma=2.1, wmax=400.0, seed=11)
+    o = O.Trainer(nv, 32, n, K=1, lr0=0.025, lr_kind=1, total_samples=pools * count)
+    o.load_edges(src, dst)
+    loss = [o.train_pool(synth.edge_pool(src, dst, count, seed=900 + e)) for e in range(pools)]
+    return o.get("vertex"), o.get("context"), np.array(loss)
+
+
+def _rel(a, b):
+    return np.linalg.norm(a.astype(np.float64) - b) / np.linalg.norm(b.astype(np.float64))
+
+
+@pytest.mark.parametrize("world,n", [(2, 2), (2, 4), (4, 4)])
+def test_processes_ordered_match_oracle(tmp_path, world, n):
+    pools, count = 2, 200_001
+    V, C, loss = _run(tmp_path, world, n, pools, count, ordered=1)
+    Vo, Co, lo = _oracle(n, pools, count)
+    assert _rel(V, Vo) <= 1e-5 and _rel(C, Co) <= 1e-5
+    np.testing.assert_allclose(loss, lo, rtol=1e-4)
+
+
+def test_processes_hogwild_runs(tmp_path):
+    """Hogwild over 2 processes on a 10^5-node graph (enough rows for the
+    ~10^4 concurrent samples): finite, learning, loss close to the oracle's."""
+    pools, count, nv, ne = 3, 2_000_000, 100_000, 500_000
+    V, C, loss = _run(tmp_path, 2, 2, pools, count, ordered=0, nv=nv, ne=ne)
+    Vo, Co, lo = _oracle(2, pools, count, nv=nv, ne=ne)
+    assert np.isfinite(V).all() and np.isfinite(C).all() and np.isfinite(loss).all()
+    assert loss[-1] < loss[0]
+    assert abs(loss[-1] - lo[-1]) < 0.05 * lo[-1], (loss, lo)
