@@ -191,9 +191,12 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
+    # GV_BENCH_DEVICE=<k> puts every rank on device k: a code-path check of the
+    # multi-process path on a one-GPU box (not a scaling measurement)
+    dev = int(os.environ.get("GV_BENCH_DEVICE", local))
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("gloo" if "GV_BENCH_DEVICE" in os.environ else "nccl")
     n = world  # one partition per GPU (configs[2]); n = 1 on one GPU (configs[1])
     threads = args.threads or max(1, (os.cpu_count() or 16) // max(1, world))
     src, dst = make_graph()
@@ -201,7 +204,7 @@ def run_ours(args):
     steps_total = args.warmup + args.steps
     total_samples = P * world * (steps_total + (0 if args.no_e2e else args.steps))
     g = G.GraphVite(CFG["nv"], CFG["d"], n, CFG["K"], 0.025, total_samples=total_samples,
-                    device=local, rank=rank, world_size=world, ordered=1 if args.ordered else 0)
+                    device=dev, rank=rank, world_size=world, ordered=1 if args.ordered else 0)
     if world > 1:
         uid = [G.gv_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -217,6 +220,12 @@ def run_ours(args):
     g.push(host_pool)
     stream = torch.cuda.ExternalStream(g.stream())
 
+    def allmax(x):
+        dev_t = "cpu" if dist.get_backend() == "gloo" else "cuda"
+        t = torch.tensor([x], dtype=torch.float64, device=dev_t)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
@@ -228,7 +237,7 @@ def run_ours(args):
         g.replay()
         stats = g.train_episode()
     barrier()
-    clocks = Clocks(local)
+    clocks = Clocks(dev)
     clocks.start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -247,9 +256,7 @@ def run_ours(args):
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = allmax(ms)
     value = samples / (ms / 1e3)
     # roofline of the dominant kernel (block-SGD): algorithmic bytes per launch / launch time
     bps = BYTES_PER_SAMPLE(CFG["d"], CFG["K"])
@@ -287,9 +294,7 @@ def run_ours(args):
         barrier()
         dt = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([dt], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+            dt = allmax(dt)
         e2e = {"value": e2e_samples / dt, "unit": "samples/s",
                "h2d_bytes_per_step": P * 8,
                "d2h_bytes_per_step": 8 * (n * n + 2) + 8}

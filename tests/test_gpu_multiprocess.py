@@ -72,5 +72,7 @@ def test_processes_hogwild_runs(tmp_path):
     V, C, loss = _run(tmp_path, 2, 2, pools, count, ordered=0, nv=nv, ne=ne)
     Vo, Co, lo = _oracle(2, pools, count, nv=nv, ne=ne)
     assert np.isfinite(V).all() and np.isfinite(C).all() and np.isfinite(loss).all()
-    assert loss[-1] < loss[0]
-    assert abs(loss[-1] - lo[-1]) < 0.05 * lo[-1], (loss, lo)
+    # the unweighted monitoring loss need not fall this early (the objective
+    # weighs negatives by 5); it must track the serial oracle's, pool by pool
+    np.testing.assert_allclose(loss, lo, rtol=0.05)
+    assert np.abs(V - Vo).mean() < 0.5 * np.abs(Vo).mean()
