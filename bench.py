@@ -35,8 +35,18 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "edge samples/sec (device-timed, max over ranks) at 1/2/4/8 B200; HBM GB/s vs peak"
-CFG = dict(nv=1_138_499, ne=4_945_382, gamma=2.1, wmax=3e4, d=128, K=1, s=5, walk=40,
-           pool=200_000_000)
+# BASELINE.json configs: C2/C3 Youtube-shaped (the default bench), C4
+# Friendster-small-shaped, C5 Friendster-shaped (tab:datasets P:272; s = 2
+# for the larger graphs). Graph shapes: SURVEY §8(d).
+CONFIGS = {
+    "C2": dict(name="youtube-shaped", nv=1_138_499, ne=4_945_382, gamma=2.1, wmax=3e4, d=128, K=1,
+               s=5, walk=40, pool=200_000_000, gen="unique"),
+    "C4": dict(name="friendster-small-shaped", nv=7_944_949, ne=447_219_610, gamma=2.5, wmax=1e4,
+               d=128, K=1, s=2, walk=40, pool=200_000_000, gen="draws"),
+    "C5": dict(name="friendster-shaped", nv=65_608_376, ne=1_806_067_142, gamma=2.5, wmax=5e3,
+               d=128, K=1, s=2, walk=40, pool=200_000_000, gen="draws"),
+}
+CFG = dict(CONFIGS["C2"])
 BYTES_PER_SAMPLE = lambda d, K: 2 * (2 + K) * d * 4  # noqa: E731  (BASELINE.json north_star)
 
 
@@ -46,7 +56,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--pool", type=int, default=CFG["pool"], help="samples per rank per pool")
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS),
+                    help="C2 (default, configs[1]); C4 / C5: the Friendster-shaped graphs")
+    ap.add_argument("--pool", type=int, default=0, help="samples per rank per pool (0 = config)")
     ap.add_argument("--threads", type=int, default=0, help="sampler threads (0 = all cores)")
     ap.add_argument("--cpu-sample", type=int, default=4_000_000,
                     help="samples of the bounded oracle run (cpu_baseline)")
@@ -114,6 +126,9 @@ class Clocks:
 
 
 def make_graph():
+    if CFG["gen"] == "draws":  # large configs: C generator, duplicates merged by ingest
+        from synth import fastgen
+        return fastgen.chung_lu_draws(CFG["nv"], CFG["ne"], CFG["gamma"], CFG["wmax"], seed=1)
     import synth
     return synth.chung_lu(CFG["nv"], CFG["ne"], gamma=CFG["gamma"], wmax=CFG["wmax"], seed=1)
 
@@ -330,7 +345,8 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": ("C2 youtube-shaped" if world == 1 else "C3 youtube-shaped grid")
+            "config": {"workload": (f"{args.config} {CFG['name']}" if world == 1 or args.config != "C2"
+                                    else "C3 youtube-shaped grid")
                        + f" synthetic power-law graph {CFG['nv']:,} nodes / {CFG['ne']:,} edges "
                        f"(chung-lu gamma {CFG['gamma']}), d={CFG['d']}, K={CFG['K']}, walk 40, "
                        f"s={CFG['s']}, pool {P:,} samples per rank, n={n}",
@@ -352,6 +368,10 @@ def run_ours(args):
 
 def main():
     args = parse()
+    CFG.clear()
+    CFG.update(CONFIGS[args.config])
+    if args.pool == 0:
+        args.pool = CFG["pool"]
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -28,6 +28,10 @@ uint64_t Partitioning::max_part() const {
 int build_graph(uint32_t nv, const uint32_t* src, const uint32_t* dst, const float* w,
                 uint64_t ne, int threads, HostGraph* g, std::string* msg) {
   if (nv == 0) return GV_ERR_INVALID_ARG;
+  if (ne >= (uint64_t(1) << 32)) {
+    *msg = "at most 2^32-1 input edges";
+    return GV_ERR_CAPACITY;
+  }
   for (uint64_t k = 0; k < ne; ++k) {
     if (src[k] >= nv || dst[k] >= nv) {
       *msg = "edge " + std::to_string(k) + " has a node id >= num_nodes";
@@ -52,18 +56,17 @@ int build_graph(uint32_t nv, const uint32_t* src, const uint32_t* dst, const flo
     return GV_ERR_EMPTY;
   }
   // 2) scatter (col, input index) pairs into rows, in input order
-  struct Ent {
+  struct Ent {  // 8 bytes: C5 has 3.6e9 directed entries
     uint32_t col;
-    uint32_t pad;
-    uint64_t k;
+    uint32_t k;  // input index (keeps duplicate summation in input order)
   };
   std::vector<Ent> ent(total);
   {
     std::vector<uint64_t> fill(cnt.begin(), cnt.end() - 1);
     for (uint64_t k = 0; k < ne; ++k) {
       if (src[k] == dst[k]) continue;
-      ent[fill[src[k]]++] = Ent{dst[k], 0, k};
-      ent[fill[dst[k]]++] = Ent{src[k], 0, k};
+      ent[fill[src[k]]++] = Ent{dst[k], static_cast<uint32_t>(k)};
+      ent[fill[dst[k]]++] = Ent{src[k], static_cast<uint32_t>(k)};
     }
   }
   // 3) per row: stable sort by column (input order kept among duplicates),
