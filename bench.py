@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true", help="skip the gv_run pipeline detail")
     ap.add_argument("--ordered", action="store_true", help="ordered verification kernel (slow)")
+    ap.add_argument("--vranks", type=int, default=1,
+                    help="run the N-rank schedule (n = vranks) as virtual ranks on one GPU: "
+                         "measures bucketing / exchange / rotation overheads, not scaling")
     return ap.parse_args()
 
 
@@ -212,14 +215,15 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     if world > 1:
         dist.init_process_group("gloo" if "GV_BENCH_DEVICE" in os.environ else "nccl")
-    n = world  # one partition per GPU (configs[2]); n = 1 on one GPU (configs[1])
+    n = world * args.vranks  # one partition per rank (configs[2]); n = 1 on one GPU (configs[1])
     threads = args.threads or max(1, (os.cpu_count() or 16) // max(1, world))
     src, dst = make_graph()
     P = args.pool
     steps_total = args.warmup + args.steps
-    total_samples = P * world * (steps_total + (0 if args.no_e2e else args.steps))
+    total_samples = P * n * (steps_total + (0 if args.no_e2e else args.steps))
     g = G.GraphVite(CFG["nv"], CFG["d"], n, CFG["K"], 0.025, total_samples=total_samples,
-                    device=dev, rank=rank, world_size=world, ordered=1 if args.ordered else 0)
+                    device=dev, rank=rank, world_size=world, ordered=1 if args.ordered else 0,
+                    virtual_ranks=args.vranks)
     if world > 1:
         uid = [G.gv_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -228,9 +232,9 @@ def run_ours(args):
     g.load_edges(src, dst)
     t_load = time.perf_counter() - t0
     # the rank's pool segment: host augmentation (Alg. 2), pinned host buffer
-    host_pool = torch.empty((P, 2), dtype=torch.int32, pin_memory=True)
+    host_pool = torch.empty((P * args.vranks, 2), dtype=torch.int32, pin_memory=True)
     t0 = time.perf_counter()
-    g.augment(CFG["walk"], CFG["s"], threads, P, 1000 + rank, out=host_pool)
+    g.augment(CFG["walk"], CFG["s"], threads, P * args.vranks, 1000 + rank, out=host_pool)
     t_aug = time.perf_counter() - t0
     g.push(host_pool)
     stream = torch.cuda.ExternalStream(g.stream())
@@ -275,8 +279,9 @@ def run_ours(args):
     value = samples / (ms / 1e3)
     # roofline of the dominant kernel (block-SGD): algorithmic bytes per launch / launch time
     bps = BYTES_PER_SAMPLE(CFG["d"], CFG["K"])
-    local_samples = samples // world
-    avg_launch_ms = sgd_ms / max(sgd_launches, 1)
+    local_samples = samples // world  # all virtual ranks of this process
+    # ms_sgd is per rank (max over virtual ranks); launches are summed over them
+    avg_launch_ms = sgd_ms / max(sgd_launches / args.vranks, 1)
     per_launch_samples = local_samples / max(sgd_launches, 1)
     achieved = per_launch_samples * bps / (avg_launch_ms / 1e3) / 1e9
     peak, peak_kind = peaks()
@@ -311,13 +316,13 @@ def run_ours(args):
         if world > 1:
             dt = allmax(dt)
         e2e = {"value": e2e_samples / dt, "unit": "samples/s",
-               "h2d_bytes_per_step": P * 8,
+               "h2d_bytes_per_step": P * args.vranks * 8,
                "d2h_bytes_per_step": 8 * (n * n + 2) + 8}
     # collaboration pipelines (NEXT-1/NEXT-2): wall clock of
     # gv_run over `pipe_pools` pools, pools produced by the host sampler threads
     # (collaborate on / off, tab:main_components) or on the GPU (NEXT-1)
     pipeline = None
-    if world == 1 and not args.no_pipeline:
+    if world == 1 and args.vranks == 1 and not args.no_pipeline:
         pipe_pools = 4
         total = P * pipe_pools
         pipeline = {"pools": pipe_pools, "pool": P}
@@ -351,11 +356,13 @@ def run_ours(args):
                        f"(chung-lu gamma {CFG['gamma']}), d={CFG['d']}, K={CFG['K']}, walk 40, "
                        f"s={CFG['s']}, pool {P:,} samples per rank, n={n}",
                        "partitions": n, "pool_per_rank": P, "l2": "inputs > L2 (no flush)",
+                       "virtual_ranks": args.vranks,
                        "mode": "ordered" if args.ordered else "hogwild"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk, "pipeline": pipeline,
             "detail": {"ms_total_per_pool": tot_ms, "sgd_ms_per_pool": sgd_ms / args.steps,
-                       "bucket_ms": stats["ms_bucket"], "load_edges_s": t_load,
+                       "bucket_ms": stats["ms_bucket"], "exchange_ms": stats["ms_exchange"],
+                       "rotate_exposed_ms": stats["ms_rotate"], "load_edges_s": t_load,
                        "augment_s": t_aug, "augment_threads": threads,
                        "alg_gbs_step": value / world * bps / 1e9},
         }

@@ -580,6 +580,31 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// The Hogwild kernel's sigmoid: MUFU ex2 / rcp (a few ulp) instead of the
+// IEEE expf and correctly rounded reciprocal of the ordered kernel — under
+// Hogwild the update order is nondeterministic anyway (parity there is the
+// AUC test), and the shorter dependency chain is what the stall profile asks
+// for. GV_RING_IEEE=1 restores the exact functions.
+#ifndef GV_RING_IEEE
+#define GV_RING_IEEE 0
+#endif
+__device__ __forceinline__ float ring_exp(float x) {
+#if GV_RING_IEEE
+  return expf(x);
+#else
+  return __expf(x);
+#endif
+}
+__device__ __forceinline__ float ring_rcp(float x) {
+#if GV_RING_IEEE
+  return __frcp_rn(x);
+#else
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+#endif
+}
+
 #ifndef GV_RING_P
 #define GV_RING_P 5
 #endif
@@ -700,8 +725,8 @@ __device__ __forceinline__ float run_ring_half(const SgdArgs& a, const WarpSeq& 
       if ((K + 1) & 1) x[K] = half_sum1(x[K]);
 #pragma unroll
       for (int t = 0; t <= K; ++t) {
-        const float e = expf(-x[t]);
-        const float pr = __frcp_rn(1.0f + e);
+        const float e = ring_exp(-x[t]);
+        const float pr = ring_rcp(1.0f + e);
         const float g = ((t == 0 ? 1.0f : 0.0f) - pr) * a.lr * (t == 0 ? 1.0f : a.neg_weight);
         axpy2(err, g, C[t]);
         red_row2_hint(context, c[t], stride, hl, dim4, g, U, act,
@@ -716,8 +741,8 @@ __device__ __forceinline__ float run_ring_half(const SgdArgs& a, const WarpSeq& 
         for (int tp = 0; tp < t; ++tp)
           if (c[t] == c[tp]) C[t] = C[tp];
         const float x = half_sum1(lane_dot2(U, C[t]));
-        const float e = expf(-x);
-        const float pr = __frcp_rn(1.0f + e);
+        const float e = ring_exp(-x);
+        const float pr = ring_rcp(1.0f + e);
         const float g = ((t == 0 ? 1.0f : 0.0f) - pr) * a.lr * (t == 0 ? 1.0f : a.neg_weight);
         axpy2(err, g, C[t]);
         red_row2_hint(context, c[t], stride, hl, dim4, g, U, act,
