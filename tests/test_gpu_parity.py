@@ -201,18 +201,38 @@ def test_augmentation_bitexact(c1_graph, threads, s, count):
     assert np.array_equal(got, sampler.augment(40, s, threads, count, 77))
 
 
+def _micro_f1(emb, labels, seed=0, train_frac=0.1):
+    """NEXT-4 protocol ("one-vs-rest linear classifiers over the
+    normalized node embeddings"; tab:performance_youtube): L2-normalised
+    embeddings, one-vs-rest logistic regression on a 10% labelled split,
+    Micro-F1 and Macro-F1 on the rest (single-label DC-SBM communities)."""
+    from sklearn.linear_model import LogisticRegression
+    from sklearn.metrics import f1_score
+    from sklearn.multiclass import OneVsRestClassifier
+    X = emb / np.maximum(np.linalg.norm(emb, axis=1, keepdims=True), 1e-12)
+    rng = np.random.default_rng(seed)
+    idx = rng.permutation(len(X))
+    ntr = int(train_frac * len(X))
+    tr, te = idx[:ntr], idx[ntr:]
+    clf = OneVsRestClassifier(LogisticRegression(max_iter=300)).fit(X[tr], labels[tr])
+    pred = clf.predict(X[te])
+    return f1_score(labels[te], pred, average="micro"), f1_score(labels[te], pred, average="macro")
+
+
 def test_hogwild_auc_matches_oracle():
     """Full Hogwild runs: link-prediction AUC within 0.01 of the
     oracle trained on the same pools, seeds and schedule; AUC_oracle >= 0.8
     (SURVEY §8(c) AUC parity spec: DC-SBM 1e5 nodes / 1e6 edges, d = 128,
     1% held out). 40 epochs (4e7 samples): the paper trains 2000-4000
     epochs; at 20 epochs the embeddings are still in the early phase
-    where the AUC dips below 0.5, so the comparison would be vacuous."""
+    where the AUC dips below 0.5, so the comparison would be vacuous.
+    NEXT-4: node classification (Micro/Macro-F1 of one-vs-rest logistic
+    regression on the community labels) within 0.02 of the oracle's."""
     nv, ne = 100_000, 1_000_000
-    src, dst, _ = synth.dcsbm(nv, ne, gamma=2.1, wmax=1000.0, c=50, mu=0.1, seed=1)
+    src, dst, comm = synth.dcsbm(nv, ne, gamma=2.1, wmax=1000.0, c=50, mu=0.1, seed=1)
     tr_s, tr_d, pos, neg = synth.linkpred_split(src, dst, nv, holdout=0.01, seed=6)
     pools, count = 4, 10_000_000
-    res = {}
+    res, f1 = {}, {}
     for n, vr in [(1, 1), (4, 4)]:
         p = G.GraphVite(nv, 128, n, 1, 0.025, total_samples=pools * count, virtual_ranks=vr,
                         ordered=0)
@@ -220,21 +240,28 @@ def test_hogwild_auc_matches_oracle():
         for k in range(pools):
             p.push(synth.edge_pool(tr_s, tr_d, count, seed=200 + k))
             p.train_episode(stats=False)
-        res[(n, vr)] = O.linkpred_auc(p.vertex(), pos, neg)
-        assert np.isfinite(p.vertex()).all() and np.isfinite(p.context()).all()
+        V = p.vertex()
+        res[(n, vr)] = O.linkpred_auc(V, pos, neg)
+        f1[(n, vr)] = _micro_f1(V, comm)
+        assert np.isfinite(V).all() and np.isfinite(p.context()).all()
         p.close()
-    auc_o = {}
+    auc_o, f1_o = {}, {}
     for n in (1, 4):  # same schedule as the GPU run (n = 4: partition-local negatives)
         o = O.Trainer(nv, 128, n, K=1, lr0=0.025, lr_kind=1, total_samples=pools * count)
         o.load_edges(tr_s, tr_d)
         for k in range(pools):
             o.train_pool(synth.edge_pool(tr_s, tr_d, count, seed=200 + k))
         auc_o[n] = O.linkpred_auc(o.get("vertex"), pos, neg)
+        f1_o[n] = _micro_f1(o.get("vertex"), comm)
         del o
     print("AUC oracle", auc_o, "gpu", res)
+    print("F1 (micro, macro) oracle", f1_o, "gpu", f1)
     assert min(auc_o.values()) >= 0.8, auc_o
     for (n, vr), auc in res.items():
         assert abs(auc - auc_o[n]) <= 0.01, (n, vr, auc, auc_o[n])
+        assert abs(f1[(n, vr)][0] - f1_o[n][0]) <= 0.02, (n, vr, f1[(n, vr)], f1_o[n])
+        assert abs(f1[(n, vr)][1] - f1_o[n][1]) <= 0.02, (n, vr, f1[(n, vr)], f1_o[n])
+    assert min(v[0] for v in f1_o.values()) > 0.5  # far above chance (1/50)
 
 
 @pytest.mark.parametrize("segments,s,count,L", [(1, 1, 1000, 40), (7, 2, 100_003, 40),

@@ -1,0 +1,33 @@
+"""Small workload touching every kernel once, for compute-sanitizer
+(memcheck / racecheck / synccheck). Not a test by itself: the sanitizer's
+exit code is the verdict."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+from paper_1903_00757_b200 import gv as G  # noqa: E402
+
+src, dst = synth.chung_lu(3000, 15_000, gamma=2.1, wmax=300.0, seed=1)
+pool = synth.edge_pool(src, dst, 50_003, seed=3)
+for n, vr, ordered in [(1, 1, 0), (4, 1, 0), (4, 2, 0), (4, 2, 1), (2, 1, 1)]:
+    g = G.GraphVite(3000, 128, n, 1, 0.025, total_samples=200_000, virtual_ranks=vr,
+                    ordered=ordered)
+    g.load_edges(src, dst)
+    g.push(pool)
+    G.gv_prepare_episode(g.ctx)
+    G.gv_debug_get_negatives(g.ctx, 0, 0, 1, 1) if False else None
+    g.train_episode()
+    g.replay()
+    g.train_episode()
+    assert np.isfinite(g.vertex()).all()
+    g.close()
+g = G.GraphVite(3000, 64, 1, 3, 0.025)
+g.load_edges(src, dst)
+g.augment_device(10, 3, 37, 20_011, 5)
+g.train_episode()
+G.gv_train_explicit(g.ctx, [0, 1], [2, 3], [[4, 5, 6], [7, 7, 2]], 0.1)
+g.close()
+print("sanitize drive ok")
