@@ -288,8 +288,9 @@ def run_ours(args):
     traffic = None
     try:  # DRAM bytes of the same kernel from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "sgd_traffic.json")) as f:
-            tr = json.load(f)
-        traffic = tr["dram_bytes_per_sample"] * per_launch_samples
+            tr = json.load(f)[args.config]  # captured for this config (n = 1)
+        if args.vranks == 1 and world == 1:
+            traffic = tr["dram_bytes_per_sample"] * per_launch_samples
     except Exception:
         pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
