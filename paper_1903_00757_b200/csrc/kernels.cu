@@ -610,13 +610,19 @@ __device__ __forceinline__ float ring_rcp(float x) {
 #endif
 constexpr int kRingP = GV_RING_P;
 
-template <int K>
+#ifndef GV_RING_LPS
+#define GV_RING_LPS 16
+#endif
+constexpr int kRingLPS = GV_RING_LPS;  // lanes per sample: 16 (2 samples / warp) or 8 (4)
+
+template <int K, int LPS>
 struct RingCfg {
-  static constexpr int R = kRingP + 1;   // stages per half
+  static constexpr int G = 32 / LPS;     // samples per warp iteration (lane groups)
+  static constexpr int R = kRingP + 1;   // stages per group
   static constexpr int T = K + 2;        // rows per sample
   static constexpr int STAGE = T * 32;   // float4 per stage (a 512 B row = 32 float4)
-  static constexpr int HALF = R * STAGE;
-  static constexpr int WARP = 2 * HALF;  // float4 per warp
+  static constexpr int GROUP = R * STAGE;
+  static constexpr int WARP = G * GROUP; // float4 per warp
   static constexpr size_t warp_bytes() { return static_cast<size_t>(WARP) * 16; }
 };
 
@@ -639,29 +645,66 @@ __device__ __forceinline__ void seq_chunk_ids(const SgdArgs& a, const WarpSeq& s
     sample_ids<K>(a, sq.start + static_cast<uint64_t>(chunk) * sq.stride + lane, u, c, &hot);
 }
 
-template <int K>
-__device__ __forceinline__ float run_ring_half(const SgdArgs& a, const WarpSeq& sq, float4* ring,
-                                               int dim4, int lane, bool want_loss) {
-  using RC = RingCfg<K>;
-  constexpr int P = kRingP, R = RC::R, T = RC::T;
-  const int h = lane >> 4, hl = lane & 15;
-  float4* const my = ring + h * RC::HALF;
+// sums over the LPS lanes of each group
+template <int LPS>
+__device__ __forceinline__ float group_sum1(float s) {
+#pragma unroll
+  for (int o = LPS / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  return s;
+}
+template <int LPS>
+__device__ __forceinline__ void group_sum2(float& a, float& b, int lane) {
+  const bool hi = (lane & (LPS / 2)) != 0;  // split butterfly at the first stage
+  float keep = hi ? b : a;
+  const float send = hi ? a : b;
+  keep += __shfl_xor_sync(kFull, send, LPS / 2);
+#pragma unroll
+  for (int o = LPS / 4; o > 0; o >>= 1) keep += __shfl_xor_sync(kFull, keep, o);
+  const int base = lane & ~(LPS - 1);
+  a = __shfl_sync(kFull, keep, base);
+  b = __shfl_sync(kFull, keep, base + LPS / 2);
+}
+
+template <int CPL>
+__device__ __forceinline__ void red_rowg(float* base, uint32_t row, uint32_t stride, int gl,
+                                         int lps, int dim4, float g, const Row<CPL>& x,
+                                         bool active, uint64_t pol) {
+  float* p = base + static_cast<uint64_t>(row) * stride;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int col = gl + lps * c;
+    if (active && col < dim4)
+      red_add4_hint(p + 4 * col,
+                    make_float4(g * x.v[c].x, g * x.v[c].y, g * x.v[c].z, g * x.v[c].w), pol);
+  }
+}
+
+// The Hogwild ring pipeline with LPS lanes per sample: group g of the warp
+// processes samples g, g+G, g+2G, ... of the warp's sequence; lane gl of a
+// group owns float4 columns gl, gl+LPS, ... of every row.
+template <int K, int LPS>
+__device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, float4* ring,
+                                          int dim4, int lane, bool want_loss) {
+  using RC = RingCfg<K, LPS>;
+  constexpr int P = kRingP, R = RC::R, T = RC::T, G = RC::G, CPL = 32 / LPS;
+  constexpr int ITER_PER_CHUNK = 32 / G;
+  const int h = lane / LPS, gl = lane % LPS;
+  float4* const my = ring + h * RC::GROUP;
   float* const vertex = a.vertex;
   float* const context = a.context;
   const uint32_t stride = a.stride;
   float loss = 0.f;
   if (sq.L == 0) return loss;
-  const uint32_t iters = (sq.L + 1) >> 1;  // iteration i: half h runs sample 2i + h
-  uint32_t cu, cc[K + 1], nu, nc[K + 1];   // ids of the current / next 32-sample chunk
-  uint32_t ch_hot, nh_hot;                 // hot-row bits of those samples
+  const uint32_t iters = (sq.L + G - 1) / G;  // iteration i: group h runs sample G i + h
+  uint32_t cu, cc[K + 1], nu, nc[K + 1];      // ids of the current / next 32-sample chunk
+  uint32_t ch_hot, nh_hot;
   seq_chunk_ids<K>(a, sq, 0, lane, cu, cc, ch_hot);
   seq_chunk_ids<K>(a, sq, 1, lane, nu, nc, nh_hot);
   const uint64_t pol_hot = a.hot_rows ? policy_evict_last() : policy_evict_normal();
   const uint64_t pol_cold = a.hot_rows ? policy_evict_first() : policy_evict_normal();
-  // ids of sample 2j + h (j = iteration), from the current or the next chunk
   auto ids_of = [&](uint32_t j, uint32_t cur_chunk, uint32_t& u, uint32_t* c, uint32_t& hot) {
-    const uint32_t pp = 2 * j + h;
-    const bool cur = (j >> 4) == cur_chunk;  // warp-uniform (2j and 2j+1 share a chunk)
+    const uint32_t pp = G * j + h;
+    const bool cur = (j / ITER_PER_CHUNK) == cur_chunk;  // warp-uniform
     const int l = static_cast<int>(pp & 31);
     u = __shfl_sync(kFull, cur ? cu : nu, l);
 #pragma unroll
@@ -671,7 +714,7 @@ __device__ __forceinline__ float run_ring_half(const SgdArgs& a, const WarpSeq& 
   auto issue = [&](uint32_t j, int st, uint32_t cur_chunk) {
     uint32_t u, c[K + 1], hot;
     ids_of(j, cur_chunk, u, c, hot);
-    if (2 * j + h < sq.L) {
+    if (G * j + h < sq.L) {
       float4* stage = my + st * RC::STAGE;
 #pragma unroll
       for (int t = 0; t < T; ++t) {
@@ -679,8 +722,8 @@ __device__ __forceinline__ float run_ring_half(const SgdArgs& a, const WarpSeq& 
             (t == 0 ? vertex : context) + static_cast<uint64_t>(t == 0 ? u : c[t - 1]) * stride);
         const uint64_t pol = ((hot >> t) & 1u) ? pol_hot : pol_cold;
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int col = hl + 16 * q;
+        for (int q = 0; q < CPL; ++q) {
+          const int col = gl + LPS * q;
           if (col < dim4) cp_async16(stage + t * 32 + col, g + col, pol);
         }
       }
@@ -691,19 +734,19 @@ __device__ __forceinline__ float run_ring_half(const SgdArgs& a, const WarpSeq& 
     if (static_cast<uint32_t>(j) < iters) issue(j, j, 0);
     cp_commit();
   }
-  int st = 0;       // stage of iteration i
-  int st_in = P;    // stage the prefetch of iteration i + P goes to
+  int st = 0;     // stage of iteration i
+  int st_in = P;  // stage the prefetch of iteration i + P goes to
   for (uint32_t i = 0; i < iters; ++i) {
-    const uint32_t chunk = i >> 4;
+    const uint32_t chunk = i / ITER_PER_CHUNK;
     cp_wait<P - 1>();
-    const bool act = 2 * i + h < sq.L;
+    const bool act = G * i + h < sq.L;
     uint32_t u, c[K + 1], hot;
     ids_of(i, chunk, u, c, hot);
     const float4* stage = my + st * RC::STAGE;
-    Row2 U, C[K + 1], err;
+    Row<CPL> U, C[K + 1], err;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int col = hl + 16 * q;
+    for (int q = 0; q < CPL; ++q) {
+      const int col = gl + LPS * q;
       const bool ok = act && col < dim4;
       U.v[q] = ok ? stage[col] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
@@ -719,17 +762,17 @@ __device__ __forceinline__ float run_ring_half(const SgdArgs& a, const WarpSeq& 
     if (!__any_sync(kFull, dup && act)) {
       float x[K + 1];
 #pragma unroll
-      for (int t = 0; t <= K; ++t) x[t] = lane_dot2(U, C[t]);
+      for (int t = 0; t <= K; ++t) x[t] = lane_dot<CPL>(U, C[t]);
 #pragma unroll
-      for (int t = 0; t + 1 <= K; t += 2) half_sum2(x[t], x[t + 1], lane);
-      if ((K + 1) & 1) x[K] = half_sum1(x[K]);
+      for (int t = 0; t + 1 <= K; t += 2) group_sum2<LPS>(x[t], x[t + 1], lane);
+      if ((K + 1) & 1) x[K] = group_sum1<LPS>(x[K]);
 #pragma unroll
       for (int t = 0; t <= K; ++t) {
         const float e = ring_exp(-x[t]);
         const float pr = ring_rcp(1.0f + e);
         const float g = ((t == 0 ? 1.0f : 0.0f) - pr) * a.lr * (t == 0 ? 1.0f : a.neg_weight);
-        axpy2(err, g, C[t]);
-        red_row2_hint(context, c[t], stride, hl, dim4, g, U, act,
+        axpy<CPL>(err, g, C[t]);
+        red_rowg<CPL>(context, c[t], stride, gl, LPS, dim4, g, U, act,
                       ((hot >> (1 + t)) & 1u) ? pol_hot : pol_cold);
         if (want_loss && act) loss += softplus_e(e, x[t]) + (t == 0 ? 0.0f : x[t]);
       }
@@ -740,23 +783,24 @@ __device__ __forceinline__ float run_ring_half(const SgdArgs& a, const WarpSeq& 
 #pragma unroll
         for (int tp = 0; tp < t; ++tp)
           if (c[t] == c[tp]) C[t] = C[tp];
-        const float x = half_sum1(lane_dot2(U, C[t]));
+        const float x = group_sum1<LPS>(lane_dot<CPL>(U, C[t]));
         const float e = ring_exp(-x);
         const float pr = ring_rcp(1.0f + e);
         const float g = ((t == 0 ? 1.0f : 0.0f) - pr) * a.lr * (t == 0 ? 1.0f : a.neg_weight);
-        axpy2(err, g, C[t]);
-        red_row2_hint(context, c[t], stride, hl, dim4, g, U, act,
+        axpy<CPL>(err, g, C[t]);
+        red_rowg<CPL>(context, c[t], stride, gl, LPS, dim4, g, U, act,
                       ((hot >> (1 + t)) & 1u) ? pol_hot : pol_cold);
-        axpy2(C[t], g, U);
+        axpy<CPL>(C[t], g, U);
         if (want_loss && act) loss += softplus_e(e, x) + (t == 0 ? 0.0f : x);
       }
     }
-    red_row2_hint(vertex, u, stride, hl, dim4, 1.0f, err, act, (hot & 1u) ? pol_hot : pol_cold);
+    red_rowg<CPL>(vertex, u, stride, gl, LPS, dim4, 1.0f, err, act,
+                  (hot & 1u) ? pol_hot : pol_cold);
     if (i + P < iters) issue(i + P, st_in, chunk);
     cp_commit();
     st = (st + 1 == R) ? 0 : st + 1;
     st_in = (st_in + 1 == R) ? 0 : st_in + 1;
-    if ((i & 15) == 15) {  // both halves finished the chunk: slide the id window
+    if ((i % ITER_PER_CHUNK) == ITER_PER_CHUNK - 1) {  // all groups finished the chunk
       cu = nu;
       ch_hot = nh_hot;
 #pragma unroll
@@ -782,9 +826,10 @@ __global__ void __launch_bounds__(128) sgd_ring_kernel(const SgdArgs a, int dim4
     if (warp + (mine - 1) * nw == nchunks - 1) L -= (nchunks << 5) - a.total;
     sq.L = static_cast<uint32_t>(L);
   }
-  float4* ring = smem_f4 + (threadIdx.x >> 5) * RingCfg<K>::WARP;
-  const float loss = run_ring_half<K>(a, sq, ring, dim4, lane, a.loss_acc != nullptr);
-  if (a.loss_acc != nullptr && (lane & 15) == 0) atomicAdd(a.loss_acc, static_cast<double>(loss));
+  float4* ring = smem_f4 + (threadIdx.x >> 5) * RingCfg<K, kRingLPS>::WARP;
+  const float loss = run_ring<K, kRingLPS>(a, sq, ring, dim4, lane, a.loss_acc != nullptr);
+  if (a.loss_acc != nullptr && (lane % kRingLPS) == 0)
+    atomicAdd(a.loss_acc, static_cast<double>(loss));
 }
 
 __device__ __forceinline__ void add_loss(double* acc, float loss, int lane) {
@@ -1266,7 +1311,7 @@ cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaSt
   const int ki = K - 1, ci = ch_of(dim) - 1;
   if (ci == 0 && ring_mode()) {
     HogFn f = kRing[ki];
-    const size_t wb = static_cast<size_t>(2) * (kRingP + 1) * (K + 2) * 32 * 16;
+    const size_t wb = static_cast<size_t>(32 / kRingLPS) * (kRingP + 1) * (K + 2) * 32 * 16;
     const int warps = 4;
     const size_t smem = wb * warps;
     static int occr[8] = {};
