@@ -226,6 +226,14 @@ gv_status gv_get_context_embeddings(gv_ctx* ctx, float* out, uint64_t out_len);
 gv_status gv_set_vertex_embeddings(gv_ctx* ctx, const float* in, uint64_t in_len);
 gv_status gv_set_context_embeddings(gv_ctx* ctx, const float* in, uint64_t in_len);
 
+/* Training progress (checkpoint / resume): the pool counter e of the
+ * negative-sample Philox stream (R-RNG) and the global sample count S_before
+ * of the lr schedule (R-LR). Saving them with the embeddings and restoring
+ * both into a fresh context resumes a run exactly (ordered mode: bit for bit).
+ * gv_set_progress: GV_ERR_STATE while a prepared pool is pending. */
+gv_status gv_get_progress(gv_ctx* ctx, uint64_t* pool_index, uint64_t* samples_done);
+gv_status gv_set_progress(gv_ctx* ctx, uint64_t pool_index, uint64_t samples_done);
+
 /* Library-owned compute stream of virtual rank r (cudaStream_t as uintptr),
  * so a caller can time device work with its own events on that stream. */
 gv_status gv_get_stream(gv_ctx* ctx, int vrank, uintptr_t* stream_out);

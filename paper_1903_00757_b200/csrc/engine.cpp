@@ -1157,6 +1157,22 @@ gv_status gv_set_context_embeddings(gv_ctx* c, const float* in, uint64_t len) {
   return embeddings_io(c, true, nullptr, in, len);
 }
 
+gv_status gv_get_progress(gv_ctx* c, uint64_t* pool_index, uint64_t* samples_done) {
+  if (gv_status s = check_ctx(c, false)) return s;
+  if (pool_index) *pool_index = c->pool_index;
+  if (samples_done) *samples_done = c->samples_done;
+  return GV_OK;
+}
+
+gv_status gv_set_progress(gv_ctx* c, uint64_t pool_index, uint64_t samples_done) {
+  if (gv_status s = check_ctx(c, false)) return s;
+  if (c->state == PoolState::Prepared) return fail(c, GV_ERR_STATE, "a prepared pool is pending");
+  if (c->ipc()) return fail(c, GV_ERR_STATE, "set progress before the first pool on every rank");
+  c->pool_index = pool_index;
+  c->samples_done = samples_done;
+  return GV_OK;
+}
+
 gv_status gv_get_stream(gv_ctx* c, int vrank, uintptr_t* stream_out) {
   if (gv_status s = check_ctx(c, true)) return s;
   if (vrank < 0 || vrank >= static_cast<int>(c->ranks.size()) || !stream_out)

@@ -606,12 +606,12 @@ __device__ __forceinline__ float ring_rcp(float x) {
 }
 
 #ifndef GV_RING_P
-#define GV_RING_P 5
+#define GV_RING_P 3
 #endif
 constexpr int kRingP = GV_RING_P;
 
 #ifndef GV_RING_LPS
-#define GV_RING_LPS 16
+#define GV_RING_LPS 8
 #endif
 constexpr int kRingLPS = GV_RING_LPS;  // lanes per sample: 16 (2 samples / warp) or 8 (4)
 
@@ -813,7 +813,7 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
 }
 
 template <int K>
-__global__ void __launch_bounds__(128) sgd_ring_kernel(const SgdArgs a, int dim4) {
+__global__ void __launch_bounds__(256) sgd_ring_kernel(const SgdArgs a, int dim4) {
   extern __shared__ float4 smem_f4[];
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1312,7 +1312,13 @@ cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaSt
   if (ci == 0 && ring_mode()) {
     HogFn f = kRing[ki];
     const size_t wb = static_cast<size_t>(32 / kRingLPS) * (kRingP + 1) * (K + 2) * 32 * 16;
-    const int warps = 4;
+    // warps per CTA that fit the most warps per SM in 227 KB of shared memory
+    // (1 KB reserved per CTA); ties go to the larger CTA
+    int warps = 1, best = 0;
+    for (int w = 1; w <= 8; ++w) {
+      const int per_sm = w * static_cast<int>((227 * 1024) / (w * wb + 1024));
+      if (per_sm >= best) best = per_sm, warps = w;
+    }
     const size_t smem = wb * warps;
     static int occr[8] = {};
     int& o = occr[ki];

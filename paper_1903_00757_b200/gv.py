@@ -100,6 +100,8 @@ SIGNATURES = {
     "gv_set_vertex_embeddings": (st, [ctx_p, f32p, C.c_uint64]),
     "gv_set_context_embeddings": (st, [ctx_p, f32p, C.c_uint64]),
     "gv_get_stream": (st, [ctx_p, C.c_int, C.POINTER(C.c_size_t)]),
+    "gv_get_progress": (st, [ctx_p, u64p, u64p]),
+    "gv_set_progress": (st, [ctx_p, C.c_uint64, C.c_uint64]),
     "gv_augment": (st, [ctx_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, u32p]),
     "gv_run": (st, [ctx_p, C.POINTER(gv_augment_cfg), C.c_uint64, C.POINTER(gv_run_report)]),
     "gv_augment_device": (st, [ctx_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64]),
@@ -242,6 +244,17 @@ def gv_set_vertex_embeddings(ctx, arr):
 def gv_set_context_embeddings(ctx, arr):
     a = np.ascontiguousarray(arr, dtype=np.float32)
     _ck(lib.gv_set_context_embeddings(ctx, _ptr(a, f32p), a.size), ctx)
+
+
+def gv_get_progress(ctx):
+    e = C.c_uint64(0)
+    sd = C.c_uint64(0)
+    _ck(lib.gv_get_progress(ctx, C.byref(e), C.byref(sd)), ctx)
+    return e.value, sd.value
+
+
+def gv_set_progress(ctx, pool_index, samples_done):
+    _ck(lib.gv_set_progress(ctx, pool_index, samples_done), ctx)
 
 
 def gv_get_stream(ctx, vrank=0) -> int:
@@ -411,6 +424,16 @@ class GraphVite:
 
     def partition(self):
         return gv_get_partition(self.ctx, self.nv, self.n)
+
+    def checkpoint(self):
+        """(vertex, context, pool_index, samples_done) — everything a resume needs."""
+        e, sd = gv_get_progress(self.ctx)
+        return self.vertex(), self.context(), e, sd
+
+    def restore(self, vertex, context, pool_index, samples_done):
+        self.set_vertex(vertex)
+        self.set_context(context)
+        gv_set_progress(self.ctx, pool_index, samples_done)
 
     def stream(self, vrank=0):
         return gv_get_stream(self.ctx, vrank)

@@ -302,3 +302,31 @@ def test_device_pipeline_matches_oracle(c1_graph):
     assert _rel(g.vertex(), o.get("vertex")) <= 1e-5
     assert _rel(g.context(), o.get("context")) <= 1e-5
     g.close()
+
+
+def test_checkpoint_resume_is_exact(c1_graph):
+    """SURVEY §5 checkpoint/resume: embeddings + progress (pool counter of the
+    negative stream, lr-schedule sample count) restored into a fresh context
+    continue the run bit for bit (ordered mode, n = 2)."""
+    src, dst = c1_graph
+    pools = [synth.edge_pool(src, dst, 150_000, seed=700 + k) for k in range(3)]
+    full = G.GraphVite(C1["nv"], 32, 2, 1, 0.025, total_samples=450_000, ordered=1)
+    full.load_edges(src, dst)
+    for pl in pools:
+        full.push(pl)
+        full.train_episode()
+    part = G.GraphVite(C1["nv"], 32, 2, 1, 0.025, total_samples=450_000, ordered=1)
+    part.load_edges(src, dst)
+    for pl in pools[:2]:
+        part.push(pl)
+        part.train_episode()
+    ck = part.checkpoint()
+    part.close()
+    assert ck[2] == 2 and ck[3] == 300_000
+    resumed = G.GraphVite(C1["nv"], 32, 2, 1, 0.025, total_samples=450_000, ordered=1)
+    resumed.load_edges(src, dst)
+    resumed.restore(*ck)
+    resumed.push(pools[2])
+    resumed.train_episode()
+    assert np.array_equal(resumed.vertex(), full.vertex())
+    assert np.array_equal(resumed.context(), full.context())
