@@ -78,17 +78,6 @@ __device__ __forceinline__ void red_row(float* base, uint32_t row, uint32_t stri
   }
 }
 
-// L2 prefetch of a row (no register, no scoreboard): lanes 0..(bytes/128)-1
-// each name one 128 B line of the row.
-__device__ __forceinline__ void prefetch_row(const float* base, uint32_t row, uint32_t stride,
-                                             int lane, int dim4) {
-  const int lines = (dim4 * 16 + 127) >> 7;
-  if (lane < lines) {
-    const float* p = base + static_cast<uint64_t>(row) * stride + 32 * lane;
-    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-  }
-}
-
 template <int CH>
 __device__ __forceinline__ float lane_dot(const Row<CH>& a, const Row<CH>& b) {
   float s = 0.f;
@@ -171,16 +160,12 @@ __device__ __forceinline__ float apply_target(float x, bool positive, float lr, 
 // (err for the vertex row, g_t U for context row t), as in Hogwild!'s
 // lock-free component-wise updates (Recht et al., "asynchronous SGD");
 // otherwise (one warp per block) the final rows are stored.
-// PF > 0: the rows of sample s+PF (this chunk, or the next one whose ids are
-// nx_u/nx_c, nx_valid samples) are prefetched into L2 while sample s runs,
-// so the register loads of sample s+1 mostly hit L2.
-template <int K, int CH, bool ATOMIC, int PF>
+template <int K, int CH, bool ATOMIC>
 __device__ __forceinline__ float run_chunk(int nvalid, uint32_t my_u, const uint32_t* my_c,
                                            float* __restrict__ vertex,
                                            float* __restrict__ context, uint32_t stride,
                                            int dim4, float lr, float neg_weight, int lane,
-                                           bool want_loss, int nx_valid = 0, uint32_t nx_u = 0,
-                                           const uint32_t* nx_c = nullptr) {
+                                           bool want_loss) {
   float loss = 0.f;
   Row<CH> U, C[K + 1];
   uint32_t u = __shfl_sync(kFull, my_u, 0);
@@ -190,34 +175,9 @@ __device__ __forceinline__ float run_chunk(int nvalid, uint32_t my_u, const uint
   load_row<CH>(U, vertex, u, stride, lane, dim4);
 #pragma unroll
   for (int t = 0; t <= K; ++t) load_row<CH>(C[t], context, c[t], stride, lane, dim4);
-  if (PF > 0) {  // prime the prefetch window: samples 1..PF-1
-#pragma unroll
-    for (int j = 1; j < PF; ++j) {
-      if (j < nvalid) {
-        prefetch_row(vertex, __shfl_sync(kFull, my_u, j), stride, lane, dim4);
-#pragma unroll
-        for (int t = 0; t <= K; ++t)
-          prefetch_row(context, __shfl_sync(kFull, my_c[t], j), stride, lane, dim4);
-      }
-    }
-  }
 
   for (int s = 0; s < nvalid; ++s) {
     const bool has_next = (s + 1) < nvalid;
-    if (PF > 0) {
-      const int f = s + PF;
-      if (f < nvalid) {
-        prefetch_row(vertex, __shfl_sync(kFull, my_u, f), stride, lane, dim4);
-#pragma unroll
-        for (int t = 0; t <= K; ++t)
-          prefetch_row(context, __shfl_sync(kFull, my_c[t], f), stride, lane, dim4);
-      } else if (f - 32 >= 0 && f - 32 < nx_valid) {
-        prefetch_row(vertex, __shfl_sync(kFull, nx_u, f - 32), stride, lane, dim4);
-#pragma unroll
-        for (int t = 0; t <= K; ++t)
-          prefetch_row(context, __shfl_sync(kFull, nx_c[t], f - 32), stride, lane, dim4);
-      }
-    }
     uint32_t un = 0, cn[K + 1];
     Row<CH> Un, Cn[K + 1];
     if (has_next) {  // prefetch the next sample's rows (warp-uniform branch)
@@ -302,195 +262,6 @@ __device__ __forceinline__ float run_chunk(int nvalid, uint32_t my_u, const uint
   return loss;
 }
 
-// ------------------------------------------------------------------------
-// Half-warp variant of run_chunk for d <= 128 (Hogwild only): half h of the
-// warp (16 lanes) processes samples h, h+2, h+4, ... of the chunk, lane
-// hl = lane & 15 owning float4 columns hl and hl+16 of every row. One warp
-// instruction therefore serves two samples — the scalar part of a target
-// (expf, reciprocal, g) and the control flow are paid once per pair — and a
-// warp keeps two samples in flight. Each half is sequential with in-register
-// forwarding as in run_chunk; the two halves race like any two warps, and
-// their updates meet as red.global.add deltas.
-// ------------------------------------------------------------------------
-struct Row2 {
-  float4 v[2];
-};
-
-__device__ __forceinline__ void load_row2(Row2& r, const float* base, uint32_t row,
-                                          uint32_t stride, int hl, int dim4, bool active) {
-  const float4* p = reinterpret_cast<const float4*>(base + static_cast<uint64_t>(row) * stride);
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    const int col = hl + 16 * c;
-    r.v[c] = (active && col < dim4) ? __ldcg(p + col) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-}
-
-__device__ __forceinline__ void red_row2(float* base, uint32_t row, uint32_t stride, int hl,
-                                         int dim4, float g, const Row2& x, bool active) {
-  float* p = base + static_cast<uint64_t>(row) * stride;
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    const int col = hl + 16 * c;
-    if (active && col < dim4)
-      red_add4(p + 4 * col, make_float4(g * x.v[c].x, g * x.v[c].y, g * x.v[c].z, g * x.v[c].w));
-  }
-}
-
-__device__ __forceinline__ float lane_dot2(const Row2& a, const Row2& b) {
-  float s = a.v[0].x * b.v[0].x;
-  s = fmaf(a.v[0].y, b.v[0].y, s);
-  s = fmaf(a.v[0].z, b.v[0].z, s);
-  s = fmaf(a.v[0].w, b.v[0].w, s);
-  s = fmaf(a.v[1].x, b.v[1].x, s);
-  s = fmaf(a.v[1].y, b.v[1].y, s);
-  s = fmaf(a.v[1].z, b.v[1].z, s);
-  s = fmaf(a.v[1].w, b.v[1].w, s);
-  return s;
-}
-
-__device__ __forceinline__ void axpy2(Row2& y, float g, const Row2& x) {
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    y.v[c].x = fmaf(g, x.v[c].x, y.v[c].x);
-    y.v[c].y = fmaf(g, x.v[c].y, y.v[c].y);
-    y.v[c].z = fmaf(g, x.v[c].z, y.v[c].z);
-    y.v[c].w = fmaf(g, x.v[c].w, y.v[c].w);
-  }
-}
-
-// sum over the 16 lanes of each half
-__device__ __forceinline__ float half_sum1(float s) {
-#pragma unroll
-  for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-  return s;
-}
-
-// two half-warp sums with 6 shuffles (split butterfly at offset 8)
-__device__ __forceinline__ void half_sum2(float& a, float& b, int lane) {
-  const bool hi = (lane & 8) != 0;
-  float keep = hi ? b : a;
-  const float send = hi ? a : b;
-  keep += __shfl_xor_sync(kFull, send, 8);
-#pragma unroll
-  for (int o = 4; o > 0; o >>= 1) keep += __shfl_xor_sync(kFull, keep, o);
-  const int base = lane & 16;
-  a = __shfl_sync(kFull, keep, base);
-  b = __shfl_sync(kFull, keep, base + 8);
-}
-
-template <int K>
-__device__ __forceinline__ float run_chunk_half(int nvalid, uint32_t my_u, const uint32_t* my_c,
-                                                float* __restrict__ vertex,
-                                                float* __restrict__ context, uint32_t stride,
-                                                int dim4, float lr, float neg_weight, int lane,
-                                                bool want_loss) {
-  const int h = lane >> 4, hl = lane & 15;
-  float loss = 0.f;
-  Row2 U, C[K + 1];
-  int q = h;  // this half's current sample
-  bool act = q < nvalid;
-  uint32_t u = __shfl_sync(kFull, my_u, q & 31);
-  uint32_t c[K + 1];
-#pragma unroll
-  for (int t = 0; t <= K; ++t) c[t] = __shfl_sync(kFull, my_c[t], q & 31);
-  load_row2(U, vertex, u, stride, hl, dim4, act);
-#pragma unroll
-  for (int t = 0; t <= K; ++t) load_row2(C[t], context, c[t], stride, hl, dim4, act);
-  const int iters = (nvalid + 1) >> 1;
-  for (int it = 0; it < iters; ++it) {
-    const int qn = q + 2;
-    const bool has_next = (it + 1) < iters;  // warp-uniform
-    const bool act_n = qn < nvalid;
-    uint32_t un = 0, cn[K + 1];
-    Row2 Un, Cn[K + 1];
-    if (has_next) {
-      un = __shfl_sync(kFull, my_u, qn & 31);
-#pragma unroll
-      for (int t = 0; t <= K; ++t) cn[t] = __shfl_sync(kFull, my_c[t], qn & 31);
-      load_row2(Un, vertex, un, stride, hl, dim4, act_n);
-#pragma unroll
-      for (int t = 0; t <= K; ++t) load_row2(Cn[t], context, cn[t], stride, hl, dim4, act_n);
-    }
-    Row2 err;
-    err.v[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-    err.v[1] = err.v[0];
-    bool dup = false;
-#pragma unroll
-    for (int t = 1; t <= K; ++t)
-#pragma unroll
-      for (int tp = 0; tp < t; ++tp) dup |= (c[t] == c[tp]);
-    float g[K + 1];
-    if (!__any_sync(kFull, dup && act)) {
-      float x[K + 1];
-#pragma unroll
-      for (int t = 0; t <= K; ++t) x[t] = lane_dot2(U, C[t]);
-#pragma unroll
-      for (int t = 0; t + 1 <= K; t += 2) half_sum2(x[t], x[t + 1], lane);
-      if ((K + 1) & 1) x[K] = half_sum1(x[K]);
-#pragma unroll
-      for (int t = 0; t <= K; ++t) {
-        const float e = expf(-x[t]);
-        const float pr = __frcp_rn(1.0f + e);
-        g[t] = ((t == 0 ? 1.0f : 0.0f) - pr) * lr * (t == 0 ? 1.0f : neg_weight);
-        axpy2(err, g[t], C[t]);
-        red_row2(context, c[t], stride, hl, dim4, g[t], U, act);
-        axpy2(C[t], g[t], U);
-        if (want_loss && act) loss += softplus_e(e, x[t]) + (t == 0 ? 0.0f : x[t]);
-      }
-    } else {
-#pragma unroll
-      for (int t = 0; t <= K; ++t) {
-#pragma unroll
-        for (int tp = 0; tp < t; ++tp)
-          if (c[t] == c[tp]) C[t] = C[tp];
-        const float x = half_sum1(lane_dot2(U, C[t]));
-        const float e = expf(-x);
-        const float pr = __frcp_rn(1.0f + e);
-        g[t] = ((t == 0 ? 1.0f : 0.0f) - pr) * lr * (t == 0 ? 1.0f : neg_weight);
-        axpy2(err, g[t], C[t]);
-        red_row2(context, c[t], stride, hl, dim4, g[t], U, act);
-        axpy2(C[t], g[t], U);
-        if (want_loss && act) loss += softplus_e(e, x) + (t == 0 ? 0.0f : x);
-      }
-    }
-#pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-      U.v[cc].x += err.v[cc].x;
-      U.v[cc].y += err.v[cc].y;
-      U.v[cc].z += err.v[cc].z;
-      U.v[cc].w += err.v[cc].w;
-    }
-    red_row2(vertex, u, stride, hl, dim4, 1.0f, err, act);
-    if (has_next) {
-      bool fwd = (un == u);
-#pragma unroll
-      for (int t = 0; t <= K; ++t)
-#pragma unroll
-        for (int tp = 0; tp <= K; ++tp) fwd |= (cn[t] == c[tp]);
-      if (__any_sync(kFull, fwd)) {
-        if (un == u) Un = U;
-#pragma unroll
-        for (int t = 0; t <= K; ++t) {
-#pragma unroll
-          for (int tp = 0; tp <= K; ++tp)
-            if (cn[t] == c[tp]) Cn[t] = C[tp];
-        }
-      }
-      U = Un;
-      u = un;
-#pragma unroll
-      for (int t = 0; t <= K; ++t) {
-        C[t] = Cn[t];
-        c[t] = cn[t];
-      }
-      q = qn;
-      act = act_n;
-    }
-  }
-  return loss;
-}
-
 // Per-lane ids of sample `qg` of a launch stream: block lookup, sample load,
 // K negatives by Philox + alias (P:231 negatives from partition j only).
 template <int K>
@@ -522,18 +293,22 @@ __device__ __forceinline__ void sample_ids(const SgdArgs& a, uint64_t qg, uint32
 }
 
 // ------------------------------------------------------------------------
-// Deep-pipelined Hogwild path (d <= 128): half-warps as in run_chunk_half,
-// but the rows of each half's next P samples are in flight as cp.async
-// (LDGSTS, L2-only) copies into a per-half shared-memory ring of R = P + 1
-// stages — P samples of row traffic outstanding per half without holding them
-// in registers ("leverage the on-chip shared memory"). There is no
-// register forwarding: a row may be read before this warp's own deltas of the
-// previous P samples have landed — bounded staleness, the same as between any
-// two warps under Hogwild; no update is lost because every write-back is a
-// red.global.add delta. (The exact, sequential mode is sgd_ordered_kernel.)
-// Lane hl of a half owns float4 columns hl and hl+16 in global and shared
-// memory, so no lane reads another lane's shared data and cp.async
-// completion (wait_group, per thread) is the only synchronisation.
+// Deep-pipelined Hogwild path (d <= 128). A warp is split into groups of LPS
+// lanes (default 8: four samples per warp instruction, so the scalar part of
+// an update — exp, reciprocal, g — and the control flow are paid once per
+// four samples). Group h processes samples h, h+G, h+2G, ... of the warp's
+// sequence; the rows of its next P samples are in flight as cp.async
+// (LDGSTS, L2-only) copies into a per-group shared-memory ring of R = P + 1
+// stages — P samples of row traffic outstanding per group without holding
+// them in registers ("leverage the on-chip shared memory"). There is
+// no register forwarding: a row may be read before this warp's own deltas
+// of the previous P samples have landed — bounded staleness, the same as
+// between any two warps under Hogwild; no update is lost because every
+// write-back is a red.global.add delta. (The exact, sequential mode is
+// sgd_ordered_kernel.) Lane gl of a group owns float4 columns gl, gl+LPS, ...
+// in global and shared memory, so no lane reads another lane's shared data
+// and cp.async completion (wait_group, per thread) is the only
+// synchronisation.
 // ------------------------------------------------------------------------
 __device__ __forceinline__ void cp_async16(float4* smem, const float4* gmem, uint64_t pol) {
   const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
@@ -545,18 +320,6 @@ __device__ __forceinline__ void red_add4_hint(float* p, float4 v, uint64_t pol) 
   asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(p),
                "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
                : "memory");
-}
-__device__ __forceinline__ void red_row2_hint(float* base, uint32_t row, uint32_t stride, int hl,
-                                              int dim4, float g, const Row2& x, bool active,
-                                              uint64_t pol) {
-  float* p = base + static_cast<uint64_t>(row) * stride;
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    const int col = hl + 16 * c;
-    if (active && col < dim4)
-      red_add4_hint(p + 4 * col,
-                    make_float4(g * x.v[c].x, g * x.v[c].y, g * x.v[c].z, g * x.v[c].w), pol);
-  }
 }
 // L2 policies: hot rows (high degree, small local id) stay, cold rows go first
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -835,29 +598,14 @@ __global__ void __launch_bounds__(256) sgd_ring_kernel(const SgdArgs a, int dim4
 __device__ __forceinline__ void add_loss(double* acc, float loss, int lane) {
   if (acc != nullptr && lane == 0) atomicAdd(acc, static_cast<double>(loss));
 }
-// the half-warp path keeps one partial per half (lanes 0 and 16)
-__device__ __forceinline__ void add_loss_halves(double* acc, float loss, int lane) {
-  if (acc != nullptr && (lane & 15) == 0) atomicAdd(acc, static_cast<double>(loss));
-}
 
-#ifndef GV_PREFETCH
-#define GV_PREFETCH 0
-#endif
-constexpr int kPrefetch = GV_PREFETCH;  // samples of L2 prefetch look-ahead
-#ifndef GV_HOG_MINB
-#define GV_HOG_MINB 2
-#endif
-#ifndef GV_HALF_WARP
-#define GV_HALF_WARP 1
-#endif
-constexpr bool kHalfWarp = GV_HALF_WARP != 0;  // two samples per warp for d <= 128
 
 // KB2: persistent grid; warp w takes chunks w, w + W, ... of 32 consecutive
 // samples of the launch stream. The ids of the warp's next chunk (sample
 // load, Philox, alias gather) are requested before the current chunk is
 // processed, so their latency hides behind 32 samples of work.
 template <int K, int CH>
-__global__ void __launch_bounds__(256, (CH == 1) ? GV_HOG_MINB : 1)
+__global__ void __launch_bounds__(256)
     sgd_hogwild_kernel(const SgdArgs a, int dim4) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -872,23 +620,13 @@ __global__ void __launch_bounds__(256, (CH == 1) ? GV_HOG_MINB : 1)
     const int nvalid = static_cast<int>(umin64(32, a.total - base));
     uint32_t nu = 0, nc[K + 1] = {};
     if (nx < nchunks && (nx << 5) + lane < a.total) sample_ids<K>(a, (nx << 5) + lane, nu, nc);
-    if (CH == 1 && kHalfWarp) {
-      loss += run_chunk_half<K>(nvalid, cu, cc, a.vertex, a.context, a.stride, dim4, a.lr,
-                                a.neg_weight, lane, want_loss);
-    } else {
-      const int nx_valid = nx < nchunks ? static_cast<int>(umin64(32, a.total - (nx << 5))) : 0;
-      loss += run_chunk<K, CH, true, kPrefetch>(nvalid, cu, cc, a.vertex, a.context, a.stride,
-                                                dim4, a.lr, a.neg_weight, lane, want_loss,
-                                                nx_valid, nu, nc);
-    }
+    loss += run_chunk<K, CH, true>(nvalid, cu, cc, a.vertex, a.context, a.stride, dim4, a.lr,
+                                   a.neg_weight, lane, want_loss);
     cu = nu;
 #pragma unroll
     for (int t = 0; t <= K; ++t) cc[t] = nc[t];
   }
-  if (CH == 1 && kHalfWarp)
-    add_loss_halves(a.loss_acc, loss, lane);
-  else
-    add_loss(a.loss_acc, loss, lane);
+  add_loss(a.loss_acc, loss, lane);
 }
 
 // Ordered verification mode: warp b owns descriptor b and walks its block
@@ -904,8 +642,8 @@ __global__ void __launch_bounds__(32) sgd_ordered_kernel(const SgdArgs a, int di
     const int nvalid = static_cast<int>(umin64(32, count - off));
     uint32_t my_u = 0, my_c[K + 1] = {};
     if (lane < nvalid) sample_ids<K>(a, begin + off + lane, my_u, my_c);
-    loss += run_chunk<K, CH, false, 0>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4,
-                                       a.lr, a.neg_weight, lane, want_loss);
+    loss += run_chunk<K, CH, false>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4,
+                                    a.lr, a.neg_weight, lane, want_loss);
   }
   add_loss(a.loss_acc, loss, lane);
 }
@@ -921,8 +659,8 @@ __global__ void __launch_bounds__(32) sgd_explicit_kernel(const ExplicitArgs a, 
 #pragma unroll
       for (int t = 0; t <= K; ++t) my_c[t] = a.crow[(off + lane) * (K + 1) + t];
     }
-    run_chunk<K, CH, false, 0>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4, a.lr,
-                               a.neg_weight, lane, false);
+    run_chunk<K, CH, false>(nvalid, my_u, my_c, a.vertex, a.context, a.stride, dim4, a.lr,
+                            a.neg_weight, lane, false);
   }
 }
 
@@ -1312,13 +1050,9 @@ cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaSt
   if (ci == 0 && ring_mode()) {
     HogFn f = kRing[ki];
     const size_t wb = static_cast<size_t>(32 / kRingLPS) * (kRingP + 1) * (K + 2) * 32 * 16;
-    // warps per CTA that fit the most warps per SM in 227 KB of shared memory
-    // (1 KB reserved per CTA); ties go to the larger CTA
-    int warps = 1, best = 0;
-    for (int w = 1; w <= 8; ++w) {
-      const int per_sm = w * static_cast<int>((227 * 1024) / (w * wb + 1024));
-      if (per_sm >= best) best = per_sm, warps = w;
-    }
+    // 4-warp CTAs: one warp per SM sub-partition (3-warp CTAs that fit 9
+    // warps/SM measured slower than 4-warp CTAs at 8 warps/SM: uneven SMSPs)
+    const int warps = wb * 4 <= 200 * 1024 ? 4 : 1;
     const size_t smem = wb * warps;
     static int occr[8] = {};
     int& o = occr[ki];

@@ -91,3 +91,36 @@ def test_product_never_imports_the_oracle():
             if f.endswith((".py", ".cpp", ".cu", ".cuh", ".hpp", ".h")):
                 text = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", text).lower() or f == "__init__.py", f
+
+
+@pytest.mark.parametrize("args,kw", [
+    ((0, 128, 1), {}),                     # num_nodes = 0
+    ((100, 0, 1), {}),                     # dim = 0
+    ((100, 6, 1), {}),                     # dim % 4 != 0
+    ((100, 516, 1), {}),                   # dim > 512
+    ((100, 128, 0), {}),                   # n_partitions = 0
+    ((100, 128, 101), {}),                 # n_partitions > num_nodes
+    ((1000, 128, 65), {}),                 # n_partitions > 64
+    ((100, 128, 4, 0), {}),                # K = 0
+    ((100, 128, 4, 9), {}),                # K > 8
+    ((100, 128, 3), {"world_size": 2}),    # n % ranks != 0
+    ((100, 128, 4), {"virtual_ranks": 3}),
+    ((100, 128, 4), {"world_size": 2, "virtual_ranks": 2}),
+    ((100, 128, 4), {"rank": 2, "world_size": 2}),
+    ((100, 128, 4), {"transport": 2, "world_size": 2}),
+])
+def test_create_rejects_bad_arguments_without_a_gpu(args, kw):
+    """gv_create validates every argument before touching the device
+    (include/gv.h: GV_ERR_INVALID_ARG)."""
+    from paper_1903_00757_b200 import gv
+    opt = gv.gv_default_options(**kw)
+    with pytest.raises(gv.GVError) as e:
+        gv.gv_create(*args, opt=opt)
+    assert e.value.status == gv.GV_ERR_INVALID_ARG
+
+
+def test_plan_step_is_host_only():
+    """gv_plan_step runs without a GPU (the gloo multi-rank test relies on it)."""
+    from paper_1903_00757_b200 import gv
+    p = gv.gv_plan_step(8, 4, 3, 5)
+    assert p["blocks"] == [(6, 3), (7, 4)] and p["send_to"] == 2 and p["recv_from"] == 0
