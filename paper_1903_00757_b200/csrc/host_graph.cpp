@@ -4,7 +4,12 @@
 #include "host_graph.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
+#include <memory>
 #include <deque>
 #include <numeric>
 
@@ -27,6 +32,15 @@ uint64_t Partitioning::max_part() const {
 // rows sorted by neighbour id; degree summed in that order.
 int build_graph(uint32_t nv, const uint32_t* src, const uint32_t* dst, const float* w,
                 uint64_t ne, int threads, HostGraph* g, std::string* msg) {
+  const bool timing = getenv("GV_INGEST_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[ingest] %s %.0f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   if (nv == 0) return GV_ERR_INVALID_ARG;
   if (ne >= (uint64_t(1) << 32)) {
     *msg = "at most 2^32-1 input edges";
@@ -42,47 +56,60 @@ int build_graph(uint32_t nv, const uint32_t* src, const uint32_t* dst, const flo
       return GV_ERR_INVALID_ARG;
     }
   }
-  // 1) row counts of the symmetrised multigraph
+  // 1) row counts of the symmetrised multigraph (parallel, atomic counters)
+  std::vector<std::atomic<uint32_t>> deg_cnt(nv);
+  for (auto& x : deg_cnt) x.store(0, std::memory_order_relaxed);
+  parallel_for(ne, threads, [&](uint64_t b, uint64_t e) {
+    for (uint64_t k = b; k < e; ++k) {
+      if (src[k] == dst[k]) continue;
+      deg_cnt[src[k]].fetch_add(1, std::memory_order_relaxed);
+      deg_cnt[dst[k]].fetch_add(1, std::memory_order_relaxed);
+    }
+  });
+  lap("validate + count");
   std::vector<uint64_t> cnt(static_cast<size_t>(nv) + 1, 0);
-  for (uint64_t k = 0; k < ne; ++k) {
-    if (src[k] == dst[k]) continue;
-    ++cnt[src[k] + 1];
-    ++cnt[dst[k] + 1];
-  }
-  std::partial_sum(cnt.begin(), cnt.end(), cnt.begin());
+  for (uint32_t v = 0; v < nv; ++v) cnt[v + 1] = cnt[v] + deg_cnt[v].load(std::memory_order_relaxed);
   const uint64_t total = cnt[nv];
   if (total == 0) {
     *msg = "graph has no edge besides self-loops";
     return GV_ERR_EMPTY;
   }
-  // 2) scatter (col, input index) pairs into rows, in input order
+  // 2) scatter (col, input index) entries into their rows (parallel; the order
+  //    inside a row is arbitrary here and restored by the sort below)
   struct Ent {  // 8 bytes: C5 has 3.6e9 directed entries
     uint32_t col;
-    uint32_t k;  // input index (keeps duplicate summation in input order)
+    uint32_t k;  // input index: duplicates are summed in input order
   };
-  std::vector<Ent> ent(total);
-  {
-    std::vector<uint64_t> fill(cnt.begin(), cnt.end() - 1);
-    for (uint64_t k = 0; k < ne; ++k) {
-      if (src[k] == dst[k]) continue;
-      ent[fill[src[k]]++] = Ent{dst[k], static_cast<uint32_t>(k)};
-      ent[fill[dst[k]]++] = Ent{src[k], static_cast<uint32_t>(k)};
+  std::unique_ptr<Ent[]> ent(new Ent[total]);
+  for (uint32_t v = 0; v < nv; ++v) deg_cnt[v].store(0, std::memory_order_relaxed);
+  parallel_for(ne, threads, [&](uint64_t b, uint64_t e) {
+    for (uint64_t k = b; k < e; ++k) {
+      const uint32_t a = src[k], c = dst[k];
+      if (a == c) continue;
+      ent[cnt[a] + deg_cnt[a].fetch_add(1, std::memory_order_relaxed)] =
+          Ent{c, static_cast<uint32_t>(k)};
+      ent[cnt[c] + deg_cnt[c].fetch_add(1, std::memory_order_relaxed)] =
+          Ent{a, static_cast<uint32_t>(k)};
     }
-  }
-  // 3) per row: stable sort by column (input order kept among duplicates),
-  //    merge duplicates; rows are independent -> parallel
+  });
+  lap("scatter");
+  // 3) per row: sort by (column, input index) — deterministic whatever the
+  //    scatter order — and count the merged entries; rows are independent
   std::vector<uint64_t> merged(nv, 0);
   parallel_for(nv, threads, [&](uint64_t b, uint64_t e) {
     for (uint64_t v = b; v < e; ++v) {
-      Ent* first = ent.data() + cnt[v];
-      Ent* last = ent.data() + cnt[v + 1];
-      std::stable_sort(first, last, [](const Ent& a, const Ent& c) { return a.col < c.col; });
+      Ent* first = ent.get() + cnt[v];
+      Ent* last = ent.get() + cnt[v + 1];
+      std::sort(first, last, [](const Ent& x, const Ent& y) {
+        return x.col != y.col ? x.col < y.col : x.k < y.k;
+      });
       uint64_t u = 0;
       for (Ent* it = first; it != last; ++it)
-        if (u == 0 || first[u - 1].col != it->col) ++u;
+        if (it == first || (it - 1)->col != it->col) ++u;
       merged[v] = u;
     }
   });
+  lap("row sort");
   g->nv = nv;
   g->off.assign(static_cast<size_t>(nv) + 1, 0);
   for (uint32_t v = 0; v < nv; ++v) g->off[v + 1] = g->off[v] + merged[v];
@@ -91,8 +118,8 @@ int build_graph(uint32_t nv, const uint32_t* src, const uint32_t* dst, const flo
   g->deg.assign(nv, 0.0);
   parallel_for(nv, threads, [&](uint64_t b, uint64_t e) {
     for (uint64_t v = b; v < e; ++v) {
-      const Ent* first = ent.data() + cnt[v];
-      const Ent* last = ent.data() + cnt[v + 1];
+      const Ent* first = ent.get() + cnt[v];
+      const Ent* last = ent.get() + cnt[v + 1];
       uint64_t o = g->off[v] - 1;
       uint32_t prev = 0;
       bool have = false;
@@ -113,6 +140,7 @@ int build_graph(uint32_t nv, const uint32_t* src, const uint32_t* dst, const flo
       g->deg[v] = s;
     }
   });
+  lap("merge + degree");
   return GV_OK;
 }
 

@@ -316,6 +316,36 @@ __device__ __forceinline__ void cp_async16(float4* smem, const float4* gmem, uin
                "l"(gmem), "l"(pol)
                : "memory");
 }
+// TMA bulk copy of a whole row into shared memory, completing on an mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(a),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_row(void* smem, const void* gmem, uint32_t bytes,
+                                         uint64_t* bar, uint64_t pol) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;\n" ::"r"(d),
+      "l"(gmem), "r"(bytes), "r"(b), "l"(pol)
+      : "memory");
+}
+
 __device__ __forceinline__ void red_add4_hint(float* p, float4 v, uint64_t pol) {
   asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(p),
                "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
@@ -378,6 +408,11 @@ constexpr int kRingP = GV_RING_P;
 #endif
 constexpr int kRingLPS = GV_RING_LPS;  // lanes per sample: 16 (2 samples / warp) or 8 (4)
 
+#ifndef GV_RING_TMA
+#define GV_RING_TMA 1
+#endif
+constexpr bool kRingTma = GV_RING_TMA != 0;  // rows staged by TMA bulk copies (else LDGSTS)
+
 template <int K, int LPS>
 struct RingCfg {
   static constexpr int G = 32 / LPS;     // samples per warp iteration (lane groups)
@@ -385,8 +420,10 @@ struct RingCfg {
   static constexpr int T = K + 2;        // rows per sample
   static constexpr int STAGE = T * 32;   // float4 per stage (a 512 B row = 32 float4)
   static constexpr int GROUP = R * STAGE;
-  static constexpr int WARP = G * GROUP; // float4 per warp
-  static constexpr size_t warp_bytes() { return static_cast<size_t>(WARP) * 16; }
+  static constexpr int WARP = G * GROUP; // float4 of row stages per warp
+  static constexpr int BARS = (G * R + 1) / 2;  // float4 holding G*R mbarriers (8 B each)
+  static constexpr int WARP_ALL = WARP + BARS;
+  static constexpr size_t warp_bytes() { return static_cast<size_t>(WARP_ALL) * 16; }
 };
 
 // Sequence of samples processed by one warp: sample p is stream index
@@ -453,6 +490,14 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
   constexpr int ITER_PER_CHUNK = 32 / G;
   const int h = lane / LPS, gl = lane % LPS;
   float4* const my = ring + h * RC::GROUP;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(ring + RC::WARP) + h * R;  // this group's
+  uint32_t phases = 0;  // bit r: parity of stage r's next completion
+  if (kRingTma) {
+    if (gl == 0)
+      for (int r = 0; r < R; ++r) mbar_init(bars + r, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncwarp();
+  }
   float* const vertex = a.vertex;
   float* const context = a.context;
   const uint32_t stride = a.stride;
@@ -479,15 +524,28 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
     ids_of(j, cur_chunk, u, c, hot);
     if (G * j + h < sq.L) {
       float4* stage = my + st * RC::STAGE;
+      if (kRingTma) {  // one lane per group: expect the bytes, then one bulk copy per row
+        if (gl == 0) {
+          mbar_expect_tx(bars + st, static_cast<uint32_t>(T * dim4 * 16));
 #pragma unroll
-      for (int t = 0; t < T; ++t) {
-        const float4* g = reinterpret_cast<const float4*>(
-            (t == 0 ? vertex : context) + static_cast<uint64_t>(t == 0 ? u : c[t - 1]) * stride);
-        const uint64_t pol = ((hot >> t) & 1u) ? pol_hot : pol_cold;
+          for (int t = 0; t < T; ++t) {
+            const float* g =
+                (t == 0 ? vertex : context) + static_cast<uint64_t>(t == 0 ? u : c[t - 1]) * stride;
+            bulk_row(stage + t * 32, g, static_cast<uint32_t>(dim4 * 16), bars + st,
+                     ((hot >> t) & 1u) ? pol_hot : pol_cold);
+          }
+        }
+      } else {
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-          const int col = gl + LPS * q;
-          if (col < dim4) cp_async16(stage + t * 32 + col, g + col, pol);
+        for (int t = 0; t < T; ++t) {
+          const float4* g = reinterpret_cast<const float4*>(
+              (t == 0 ? vertex : context) + static_cast<uint64_t>(t == 0 ? u : c[t - 1]) * stride);
+          const uint64_t pol = ((hot >> t) & 1u) ? pol_hot : pol_cold;
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) {
+            const int col = gl + LPS * q;
+            if (col < dim4) cp_async16(stage + t * 32 + col, g + col, pol);
+          }
         }
       }
     }
@@ -495,14 +553,19 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
 #pragma unroll
   for (int j = 0; j < P; ++j) {
     if (static_cast<uint32_t>(j) < iters) issue(j, j, 0);
-    cp_commit();
+    if (!kRingTma) cp_commit();
   }
   int st = 0;     // stage of iteration i
   int st_in = P;  // stage the prefetch of iteration i + P goes to
   for (uint32_t i = 0; i < iters; ++i) {
     const uint32_t chunk = i / ITER_PER_CHUNK;
-    cp_wait<P - 1>();
     const bool act = G * i + h < sq.L;
+    if (kRingTma) {
+      if (act) mbar_wait(bars + st, (phases >> st) & 1u);
+      phases ^= 1u << st;
+    } else {
+      cp_wait<P - 1>();
+    }
     uint32_t u, c[K + 1], hot;
     ids_of(i, chunk, u, c, hot);
     const float4* stage = my + st * RC::STAGE;
@@ -560,7 +623,7 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
     red_rowg<CPL>(vertex, u, stride, gl, LPS, dim4, 1.0f, err, act,
                   (hot & 1u) ? pol_hot : pol_cold);
     if (i + P < iters) issue(i + P, st_in, chunk);
-    cp_commit();
+    if (!kRingTma) cp_commit();
     st = (st + 1 == R) ? 0 : st + 1;
     st_in = (st_in + 1 == R) ? 0 : st_in + 1;
     if ((i % ITER_PER_CHUNK) == ITER_PER_CHUNK - 1) {  // all groups finished the chunk
@@ -571,7 +634,7 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
       seq_chunk_ids<K>(a, sq, chunk + 2, lane, nu, nc, nh_hot);
     }
   }
-  cp_wait<0>();
+  if (!kRingTma) cp_wait<0>();
   return loss;
 }
 
@@ -589,7 +652,7 @@ __global__ void __launch_bounds__(256) sgd_ring_kernel(const SgdArgs a, int dim4
     if (warp + (mine - 1) * nw == nchunks - 1) L -= (nchunks << 5) - a.total;
     sq.L = static_cast<uint32_t>(L);
   }
-  float4* ring = smem_f4 + (threadIdx.x >> 5) * RingCfg<K, kRingLPS>::WARP;
+  float4* ring = smem_f4 + (threadIdx.x >> 5) * RingCfg<K, kRingLPS>::WARP_ALL;
   const float loss = run_ring<K, kRingLPS>(a, sq, ring, dim4, lane, a.loss_acc != nullptr);
   if (a.loss_acc != nullptr && (lane % kRingLPS) == 0)
     atomicAdd(a.loss_acc, static_cast<double>(loss));
@@ -1049,7 +1112,8 @@ cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaSt
   const int ki = K - 1, ci = ch_of(dim) - 1;
   if (ci == 0 && ring_mode()) {
     HogFn f = kRing[ki];
-    const size_t wb = static_cast<size_t>(32 / kRingLPS) * (kRingP + 1) * (K + 2) * 32 * 16;
+    const int G = 32 / kRingLPS, R = kRingP + 1;
+    const size_t wb = (static_cast<size_t>(G) * R * (K + 2) * 32 + (G * R + 1) / 2) * 16;
     // 4-warp CTAs: one warp per SM sub-partition (3-warp CTAs that fit 9
     // warps/SM measured slower than 4-warp CTAs at 8 warps/SM: uneven SMSPs)
     const int warps = wb * 4 <= 200 * 1024 ? 4 : 1;
