@@ -420,3 +420,29 @@ def test_hogwild_shapes_track_oracle(d, K):
         assert abs(lg - lo) <= 0.03 * lo, (k, lg, lo)
     assert np.isfinite(p.vertex()).all() and np.isfinite(p.context()).all()
     p.close()
+
+
+def test_multigraph_ingest_matches_oracle():
+    """Ingest of a weighted multigraph with many duplicates, reversed
+    duplicates and self-loops (R-INGEST): partition, every alias table and the
+    walks (which read the merged CSR) equal the oracle's, byte for byte."""
+    rng = np.random.default_rng(12)
+    nv, ne = 300, 20_000
+    src = rng.integers(0, nv, ne).astype(np.uint32)
+    dst = rng.integers(0, nv, ne).astype(np.uint32)
+    w = rng.integers(1, 8, ne).astype(np.float32) * np.float32(0.25)  # dyadic: exact sums
+    p = G.GraphVite(nv, 8, 3)
+    G.gv_load_edges(p.ctx, src, dst, w)
+    o = O.Trainer(nv, 8, 3)
+    o.load_edges(src, dst, w)
+    perm_p, off_p = p.partition()
+    perm_o, off_o = o.partition()
+    assert np.array_equal(perm_p, perm_o) and np.array_equal(off_p, off_o)
+    for q in range(3):
+        prob, al = G.gv_get_alias(p.ctx, q, int(off_p[q + 1] - off_p[q]))
+        po, ao = o.alias(q)
+        assert np.array_equal(prob, po) and np.array_equal(al, ao)
+    got = p.augment(8, 3, 5, 30_000, 9)
+    ref = O.Sampler(O.Graph(nv, src, dst, w)).augment(8, 3, 5, 30_000, 9)
+    assert np.array_equal(got, ref)
+    p.close()
