@@ -101,6 +101,12 @@ typedef struct {
   int transport;          /* world_size > 1: 0 = CUDA IPC peer copies with a shared-
                              memory handshake (default; also runs several ranks on
                              one GPU), 1 = NCCL send/recv                          */
+  int host_partitions;    /* 1 = out-of-core (NEXT-3, Alg. 3 P:248-252 verbatim):
+                             both matrices live in pinned host memory and only the
+                             current block's vertex and context partitions are on
+                             the device (two slots each, the next block's partitions
+                             load while the current block trains). Single rank,
+                             n_partitions >= 2. Default 0. */
 } gv_options;
 
 /* Per-pool statistics of THIS process (all its virtual ranks). Times are
@@ -126,7 +132,8 @@ typedef struct {
 
 /* Fills *opt with defaults: seed 5, init_seed 4 (SURVEY §8(d) seeds),
  * neg_weight 5, device 0, rank 0, world_size 1, virtual_ranks 1, ordered 0,
- * compute_loss 1, host_threads 0, max_pool_samples 0, transport 0. */
+ * compute_loss 1, host_threads 0, max_pool_samples 0, transport 0,
+ * host_partitions 0. */
 void gv_default_options(gv_options* opt);
 
 /* Create a trainer for |V| = num_nodes nodes with dim-dimensional vertex and

@@ -11,6 +11,7 @@
 // With m = 1 this is Alg. 3's train -> rotate -> train ring.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 #include <sys/mman.h>
 #include <nccl.h>
 
@@ -36,6 +37,12 @@
 namespace {
 
 thread_local std::string g_last_error;
+
+// NVTX ranges around the stages (visible in Nsight Systems timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ------------------------------------------------------------------ NCCL
 // Loaded lazily so that single-process use has no NCCL dependency.
@@ -184,6 +191,15 @@ struct gv_ctx {
   std::vector<Rank> ranks;
   ncclComm_t comm = nullptr;
   bool comm_ready = false;
+  // out-of-core mode (host_partitions): matrices in pinned host memory, two
+  // device slots per matrix
+  float* h_vertex = nullptr;
+  float* h_context = nullptr;
+  int vslot_part[2] = {-1, -1};
+  int cslot_part[2] = {-1, -1};
+  int vslot_prev = 1, cslot_prev = 1;  // slot used by the previous block
+  cudaEvent_t ev_vfree[2] = {}, ev_cfree[2] = {}, ev_vload[2] = {}, ev_cload[2] = {};
+  bool hp() const { return opt.host_partitions != 0; }
   // CUDA-IPC transport (world_size > 1, transport 0)
   gv::IpcShm* shm = nullptr;
   std::string shm_name;
@@ -266,6 +282,7 @@ gv_status sync_all(gv_ctx* c) {
 // a3-a6: bucket every local rank's pool segment, exchange block rows.
 gv_status prepare(gv_ctx* c) {
   if (c->state == PoolState::Prepared) return GV_OK;
+  NvtxRange nv_range("gv:prepare (bucket + exchange)");
   {
     std::lock_guard<std::mutex> lk(c->mu);
     if (c->raw_count[c->pending] == 0) return fail(c, GV_ERR_EMPTY, "no pending samples");
@@ -494,6 +511,7 @@ gv_status prepare(gv_ctx* c) {
 // ---------------------------------------------------------------- steps
 // a7-a8 for the prepared pool.
 gv_status run_steps(gv_ctx* c) {
+  NvtxRange nv_range("gv:offset steps (block-SGD + rotation)");
   const uint32_t n = c->n, m = c->m;
   const uint32_t e = static_cast<uint32_t>(c->pool_index);
   const uint32_t key0 = static_cast<uint32_t>(c->opt.seed), key1 = static_cast<uint32_t>(c->opt.seed >> 32);
@@ -507,6 +525,33 @@ gv_status run_steps(gv_ctx* c) {
   // descriptors: D == 1 -> one launch per step over all n blocks;
   //              D > 1  -> one launch per block (g), so the first block of a
   //              step can release its context partition early.
+  struct HpAct {  // out-of-core: slots of a block and the transfers before it
+    int vs, cs, vload, vevict, cload, cevict;
+  };
+  std::vector<HpAct> hp_acts;
+  if (c->hp()) {
+    auto pick = [](int* part_of_slot, int& prev, int need, int& load, int& evict) {
+      for (int s = 0; s < 2; ++s)
+        if (part_of_slot[s] == need) {
+          prev = s;
+          load = evict = -1;
+          return s;
+        }
+      const int s = prev == 0 ? 1 : 0;  // keep the previous block's slot (it may still run)
+      evict = part_of_slot[s];
+      load = need;
+      part_of_slot[s] = need;
+      prev = s;
+      return s;
+    };
+    hp_acts.resize(static_cast<size_t>(n) * n);
+    for (uint32_t t = 0; t < n; ++t)
+      for (uint32_t i = 0; i < n; ++i) {  // Alg. 3 order: offset step, then vertex partition
+        HpAct& h = hp_acts[t * n + i];
+        h.vs = pick(c->vslot_part, c->vslot_prev, static_cast<int>(i), h.vload, h.vevict);
+        h.cs = pick(c->cslot_part, c->cslot_prev, static_cast<int>((i + t) % n), h.cload, h.cevict);
+      }
+  }
   for (auto& r : c->ranks) {
     std::vector<gv::BlockDesc> desc(static_cast<size_t>(n) * m);
     // slot bookkeeping is simulated here exactly as the rotation will move data
@@ -521,11 +566,15 @@ gv_status run_steps(gv_ctx* c) {
         gv::BlockDesc& d = desc[t * m + g];
         d.sample_off = r.final_off[g * n + j];
         d.count_lo = static_cast<uint32_t>(r.final_off[g * n + j + 1] - r.final_off[g * n + j]);
-        d.prefix = (c->D == 1) ? prefix : 0;
+        d.prefix = (c->D == 1 && !c->hp()) ? prefix : 0;
         prefix += d.count_lo;
         d.vrow0 = static_cast<uint32_t>(c->part.off[i] - r.vrow_first);
         d.crow0 = static_cast<uint32_t>(c->D == 1 ? c->part.off[j]
                                                   : static_cast<uint64_t>(slot_of[j]) * r.slot_rows);
+        if (c->hp()) {
+          d.vrow0 = static_cast<uint32_t>(hp_acts[t * n + i].vs * r.slot_rows);
+          d.crow0 = static_cast<uint32_t>(hp_acts[t * n + i].cs * r.slot_rows);
+        }
         d.alias0 = static_cast<uint32_t>(c->part.off[j]);
         d.m = static_cast<uint32_t>(psize(c, j));
         d.ij = (i << 16) | j;
@@ -543,7 +592,7 @@ gv_status run_steps(gv_ctx* c) {
                        cudaMemcpyHostToDevice, r.compute));
     // (pageable source: the copy is staged before cudaMemcpyAsync returns)
     if (c->opt.compute_loss) CK(cudaMemsetAsync(r.loss.p, 0, sizeof(double), r.compute));
-    const size_t need = static_cast<size_t>(2) * (c->D == 1 ? n : n * m);
+    const size_t need = static_cast<size_t>(2) * (c->D == 1 && !c->hp() ? n : n * m);
     while (r.ev_sgd.size() < need) r.ev_sgd.push_back(new_event(true));
   }
   // enqueue the steps
@@ -582,6 +631,36 @@ gv_status run_steps(gv_ctx* c) {
         r.kernel_launches++;
         return GV_OK;
       };
+      if (c->hp()) {
+        // out-of-core (Alg. 3): before block (i, j), send its vertex
+        // and context partitions to the device (writing back what they evict);
+        // the copy stream runs ahead, so block k+1's transfers overlap block k
+        const size_t row_bytes = sizeof(float) * c->stride;
+        for (uint32_t g = 0; g < m; ++g) {
+          const HpAct& h = hp_acts[t * n + g];
+          struct X { int s, load, evict; float* dev; float* host; cudaEvent_t* fr; cudaEvent_t* ld; };
+          const X xs[2] = {{h.vs, h.vload, h.vevict, r.vertex, c->h_vertex, c->ev_vfree, c->ev_vload},
+                           {h.cs, h.cload, h.cevict, r.context, c->h_context, c->ev_cfree, c->ev_cload}};
+          for (const X& x : xs) {
+            if (x.load < 0) continue;
+            float* slot = x.dev + static_cast<uint64_t>(x.s) * r.slot_rows * c->stride;
+            CK(cudaStreamWaitEvent(c->copy_stream, x.fr[x.s], 0));
+            if (x.evict >= 0)
+              CK(cudaMemcpyAsync(x.host + c->part.off[x.evict] * c->stride, slot,
+                                 row_bytes * psize(c, x.evict), cudaMemcpyDeviceToHost, c->copy_stream));
+            CK(cudaMemcpyAsync(slot, x.host + c->part.off[x.load] * c->stride,
+                               row_bytes * psize(c, x.load), cudaMemcpyHostToDevice, c->copy_stream));
+            CK(cudaEventRecord(x.ld[x.s], c->copy_stream));
+          }
+          CK(cudaStreamWaitEvent(r.compute, c->ev_vload[h.vs], 0));
+          CK(cudaStreamWaitEvent(r.compute, c->ev_cload[h.cs], 0));
+          gv_status st = launch(g, 1);
+          if (st) return st;
+          CK(cudaEventRecord(c->ev_vfree[h.vs], r.compute));
+          CK(cudaEventRecord(c->ev_cfree[h.cs], r.compute));
+        }
+        continue;
+      }
       if (c->D == 1) {
         gv_status st = launch(0, m);
         if (st) return st;
@@ -764,6 +843,36 @@ gv_status setup_device(gv_ctx* c) {
     CK(cudaStreamCreateWithFlags(&r.comm, cudaStreamNonBlocking));
     r.vrow_first = c->part.off[r.d * m];
     r.vrows = c->part.off[(r.d + 1) * m] - r.vrow_first;
+    if (c->hp()) {
+      // out-of-core: host arrays in relabelled order, two device slots each
+      const size_t hbytes = sizeof(float) * static_cast<size_t>(nv) * c->stride;
+      CK(cudaHostAlloc(&c->h_vertex, hbytes, cudaHostAllocDefault));
+      CK(cudaHostAlloc(&c->h_context, hbytes, cudaHostAllocDefault));
+      std::memset(c->h_context, 0, hbytes);
+      r.slot_rows = max_part;
+      r.vrows = 2 * max_part;
+      r.crows = 2 * max_part;
+      CK(cudaMalloc(&r.vertex, sizeof(float) * r.vrows * c->stride));
+      CK(cudaMalloc(&r.context, sizeof(float) * r.crows * c->stride));
+      CK(cudaMemset(r.vertex, 0, sizeof(float) * r.vrows * c->stride));
+      for (uint32_t p = 0; p < n; ++p) {  // Philox init partition by partition
+        CK(gv::launch_init_vertex(r.vertex, c->stride, c->dim, c->part.off[p], psize(c, p),
+                                  c->d_inv_perm, key0, key1, r.compute));
+        CK(cudaMemcpyAsync(c->h_vertex + c->part.off[p] * c->stride, r.vertex,
+                           sizeof(float) * psize(c, p) * c->stride, cudaMemcpyDeviceToHost,
+                           r.compute));
+        CK(cudaStreamSynchronize(r.compute));
+      }
+      for (int k = 0; k < 2; ++k) {
+        c->ev_vfree[k] = new_event(false);
+        c->ev_cfree[k] = new_event(false);
+        c->ev_vload[k] = new_event(false);
+        c->ev_cload[k] = new_event(false);
+        CK(cudaEventRecord(c->ev_vfree[k], r.compute));
+        CK(cudaEventRecord(c->ev_cfree[k], r.compute));
+      }
+      r.vrow_first = 0;
+    } else {
     CK(cudaMalloc(&r.vertex, sizeof(float) * std::max<uint64_t>(r.vrows, 1) * c->stride));
     CK(cudaMemsetAsync(r.vertex, 0, sizeof(float) * r.vrows * c->stride, r.compute));
     CK(gv::launch_init_vertex(r.vertex, c->stride, c->dim, r.vrow_first, r.vrows, c->d_inv_perm,
@@ -789,6 +898,7 @@ gv_status setup_device(gv_ctx* c) {
     }
     CK(cudaMalloc(&r.context, sizeof(float) * r.crows * c->stride));
     CK(cudaMemsetAsync(r.context, 0, sizeof(float) * r.crows * c->stride, r.compute));
+    }  // !hp
     CK(r.counts.ensure(n * n + 2));
     if (c->opt.world_size > 1) CK(r.all_counts.ensure(static_cast<size_t>(n * n + 2) * c->D));
     CK(r.loss.ensure(1));
@@ -868,6 +978,7 @@ void gv_default_options(gv_options* o) {
   o->host_threads = 0;
   o->max_pool_samples = 0;
   o->transport = 0;
+  o->host_partitions = 0;
 }
 
 int gv_abi_version(void) { return GV_ABI_VERSION; }
@@ -909,6 +1020,8 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
   const int D = o.world_size * o.virtual_ranks;
   if (n_partitions % D != 0)
     return fail(nullptr, GV_ERR_INVALID_ARG, "n_partitions must be a multiple of the rank count");
+  if (o.host_partitions && (o.world_size * o.virtual_ranks != 1 || n_partitions < 2))
+    return fail(nullptr, GV_ERR_INVALID_ARG, "host_partitions needs one rank and n_partitions >= 2");
   if (o.transport != 0 && o.transport != 1)
     return fail(nullptr, GV_ERR_INVALID_ARG, "transport must be 0 (CUDA IPC) or 1 (NCCL)");
   if (alpha && (alpha->kind != GV_LR_CONSTANT && alpha->kind != GV_LR_LINEAR))
@@ -990,6 +1103,7 @@ gv_status gv_load_edges(gv_ctx* c, const uint32_t* src, const uint32_t* dst, con
   if (c->opt.world_size > 1 && !c->comm_ready) return fail(c, GV_ERR_STATE, "gv_comm_init first");
   if (num_edges && (!src || !dst)) return fail(c, GV_ERR_INVALID_ARG, "null edge arrays");
   CK(cudaSetDevice(c->opt.device));
+  NvtxRange nv_range("gv:load_edges");
   std::string msg;
   int rc = gv::build_graph(c->nv, src, dst, weight, num_edges, c->threads, &c->graph, &msg);
   if (rc) return fail(c, static_cast<gv_status>(rc), msg);
@@ -1102,6 +1216,29 @@ static gv_status embeddings_io(gv_ctx* c, bool context, float* out, const float*
   gv_status st = sync_all(c);
   if (st) return st;
   const uint32_t dim = c->dim, stride = c->stride, m = c->m;
+  if (c->hp()) {
+    // out-of-core: flush the resident (dirty) partitions, then use the host copy
+    Rank& r = c->ranks[0];
+    float* host = context ? c->h_context : c->h_vertex;
+    float* dev = context ? r.context : r.vertex;
+    int* part_of_slot = context ? c->cslot_part : c->vslot_part;
+    for (int sl = 0; sl < 2; ++sl) {
+      const int p = part_of_slot[sl];
+      if (p < 0) continue;
+      float* slot = dev + static_cast<uint64_t>(sl) * r.slot_rows * stride;
+      if (out)
+        CK(cudaMemcpy(host + c->part.off[p] * stride, slot, sizeof(float) * psize(c, p) * stride,
+                      cudaMemcpyDeviceToHost));
+      else
+        part_of_slot[sl] = -1;  // overwritten below: drop the device copy
+    }
+    for (uint32_t id = 0; id < c->nv; ++id) {
+      const uint64_t o = static_cast<uint64_t>(c->part.inv_perm[id]) * dim;
+      if (out) std::memcpy(out + o, host + static_cast<uint64_t>(id) * stride, dim * sizeof(float));
+      else std::memcpy(host + static_cast<uint64_t>(id) * stride, in + o, dim * sizeof(float));
+    }
+    return GV_OK;
+  }
   std::vector<float> buf;
   for (auto& r : c->ranks) {
     // list of (device base row, first new id, rows)
@@ -1325,7 +1462,8 @@ gv_status gv_debug_get_negatives(gv_ctx* c, uint32_t i, uint32_t j, uint32_t* ou
 gv_status gv_train_explicit(gv_ctx* c, const uint32_t* u, const uint32_t* v, const uint32_t* negs,
                             uint64_t count, float lr) {
   if (gv_status s = check_ctx(c, true)) return s;
-  if (c->D != 1) return fail(c, GV_ERR_STATE, "gv_train_explicit needs a single rank");
+  if (c->D != 1 || c->hp())
+    return fail(c, GV_ERR_STATE, "gv_train_explicit needs a single rank with resident matrices");
   if (count == 0) return GV_OK;
   CK(cudaSetDevice(c->opt.device));
   const uint32_t K = c->K;
@@ -1419,6 +1557,11 @@ void gv_destroy(gv_ctx* c) {
     if (c->raw_free[k]) cudaEventDestroy(c->raw_free[k]);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->h_vertex) cudaFreeHost(c->h_vertex);
+  if (c->h_context) cudaFreeHost(c->h_context);
+  for (int k = 0; k < 2; ++k)
+    for (cudaEvent_t e : {c->ev_vfree[k], c->ev_cfree[k], c->ev_vload[k], c->ev_cload[k]})
+      if (e) cudaEventDestroy(e);
   cudaFree(c->d_packed);
   cudaFree(c->d_alias);
   cudaFree(c->d_woff);

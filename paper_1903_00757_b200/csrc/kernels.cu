@@ -521,7 +521,13 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
   };
   auto issue = [&](uint32_t j, int st, uint32_t cur_chunk) {
     uint32_t u, c[K + 1], hot;
-    ids_of(j, cur_chunk, u, c, hot);
+    ids_of(j, cur_chunk, u, c, hot);  // warp-uniform call: all lanes shuffle
+    if (kRingTma) {
+      // the stage was last read (generic proxy) by every lane of the group:
+      // order those reads before the async-proxy (TMA) write into it
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
     if (G * j + h < sq.L) {
       float4* stage = my + st * RC::STAGE;
       if (kRingTma) {  // one lane per group: expect the bytes, then one bulk copy per row
