@@ -108,6 +108,8 @@ def test_product_never_imports_the_oracle():
     ((100, 128, 4), {"world_size": 2, "virtual_ranks": 2}),
     ((100, 128, 4), {"rank": 2, "world_size": 2}),
     ((100, 128, 4), {"transport": 2, "world_size": 2}),
+    ((100, 128, 1), {"host_partitions": 1}),            # out-of-core needs n >= 2
+    ((100, 128, 4), {"host_partitions": 1, "virtual_ranks": 2}),
 ])
 def test_create_rejects_bad_arguments_without_a_gpu(args, kw):
     """gv_create validates every argument before touching the device

@@ -446,3 +446,35 @@ def test_multigraph_ingest_matches_oracle():
     ref = O.Sampler(O.Graph(nv, src, dst, w)).augment(8, 3, 5, 30_000, 9)
     assert np.array_equal(got, ref)
     p.close()
+
+
+@pytest.mark.parametrize("n,ordered", [(2, 1), (4, 1), (5, 0)])
+def test_out_of_core_partitions(c1_graph, n, ordered):
+    """NEXT-3 (Alg. 3 P:248-252 verbatim): the matrices live in pinned host
+    memory; each block's vertex and context partitions are sent to the device
+    (evicted ones written back) with the next block's transfers overlapping the
+    current block. Ordered mode equals the oracle with the same n; Hogwild
+    tracks its loss; set/get round-trips through the host copy."""
+    src, dst = c1_graph
+    total = 600_000
+    p = G.GraphVite(C1["nv"], 64, n, 1, 0.025, total_samples=total, ordered=ordered,
+                    host_partitions=1)
+    p.load_edges(src, dst)
+    o = O.Trainer(C1["nv"], 64, n, K=1, lr0=0.025, lr_kind=1, total_samples=total)
+    o.load_edges(src, dst)
+    assert np.array_equal(p.vertex(), o.get("vertex"))  # init through the host copy
+    for k in range(2):
+        pool = synth.edge_pool(src, dst, 300_000, seed=800 + k)
+        p.push(pool)
+        lg = p.train_episode()["loss_sum"]
+        lo = o.train_pool(pool)
+        if not ordered:
+            assert abs(lg - lo) <= 0.05 * lo
+    if ordered:
+        assert _rel(p.vertex(), o.get("vertex")) <= 1e-5
+        assert _rel(p.context(), o.get("context")) <= 1e-5
+    V = p.vertex()
+    V[:5] = 0.5
+    p.set_vertex(V)
+    assert np.array_equal(p.vertex(), V)
+    p.close()
