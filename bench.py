@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true", help="skip the gv_run pipeline detail")
     ap.add_argument("--ordered", action="store_true", help="ordered verification kernel (slow)")
+    ap.add_argument("--host-partitions", type=int, default=0,
+                    help="out-of-core (NEXT-3): n host-resident partitions on one GPU")
     ap.add_argument("--vranks", type=int, default=1,
                     help="run the N-rank schedule (n = vranks) as virtual ranks on one GPU: "
                          "measures bucketing / exchange / rotation overheads, not scaling")
@@ -216,6 +218,8 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("gloo" if "GV_BENCH_DEVICE" in os.environ else "nccl")
     n = world * args.vranks  # one partition per rank (configs[2]); n = 1 on one GPU (configs[1])
+    if args.host_partitions:
+        n = args.host_partitions
     threads = args.threads or max(1, (os.cpu_count() or 16) // max(1, world))
     src, dst = make_graph()
     P = args.pool
@@ -223,7 +227,7 @@ def run_ours(args):
     total_samples = P * n * (steps_total + (0 if args.no_e2e else args.steps))
     g = G.GraphVite(CFG["nv"], CFG["d"], n, CFG["K"], 0.025, total_samples=total_samples,
                     device=dev, rank=rank, world_size=world, ordered=1 if args.ordered else 0,
-                    virtual_ranks=args.vranks)
+                    virtual_ranks=args.vranks, host_partitions=1 if args.host_partitions else 0)
     if world > 1:
         uid = [G.gv_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -289,7 +293,7 @@ def run_ours(args):
     try:  # DRAM bytes of the same kernel from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "sgd_traffic.json")) as f:
             tr = json.load(f)[args.config]  # captured for this config (n = 1)
-        if args.vranks == 1 and world == 1:
+        if args.vranks == 1 and world == 1 and not args.host_partitions:
             traffic = tr["dram_bytes_per_sample"] * per_launch_samples
     except Exception:
         pass
@@ -323,7 +327,7 @@ def run_ours(args):
     # gv_run over `pipe_pools` pools, pools produced by the host sampler threads
     # (collaborate on / off, tab:main_components) or on the GPU (NEXT-1)
     pipeline = None
-    if world == 1 and args.vranks == 1 and not args.no_pipeline:
+    if world == 1 and args.vranks == 1 and not args.host_partitions and not args.no_pipeline:
         pipe_pools = 4
         total = P * pipe_pools
         pipeline = {"pools": pipe_pools, "pool": P}
@@ -358,6 +362,7 @@ def run_ours(args):
                        f"s={CFG['s']}, pool {P:,} samples per rank, n={n}",
                        "partitions": n, "pool_per_rank": P, "l2": "inputs > L2 (no flush)",
                        "virtual_ranks": args.vranks,
+                       "host_partitions": bool(args.host_partitions),
                        "mode": "ordered" if args.ordered else "hogwild"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk, "pipeline": pipeline,

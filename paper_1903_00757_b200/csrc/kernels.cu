@@ -409,9 +409,13 @@ constexpr int kRingP = GV_RING_P;
 constexpr int kRingLPS = GV_RING_LPS;  // lanes per sample: 16 (2 samples / warp) or 8 (4)
 
 #ifndef GV_RING_TMA
-#define GV_RING_TMA 1
+#define GV_RING_TMA 0
 #endif
-constexpr bool kRingTma = GV_RING_TMA != 0;  // rows staged by TMA bulk copies (else LDGSTS)
+// Rows staged by TMA bulk copies (cp.async.bulk + one mbarrier per stage)
+// instead of LDGSTS: measured equal on C2 and C4 (profiles/README.md), and
+// compute-sanitizer racecheck cannot verify the async-proxy ordering, so the
+// default is LDGSTS; GV_RING_TMA=1 builds the TMA variant.
+constexpr bool kRingTma = GV_RING_TMA != 0;
 
 template <int K, int LPS>
 struct RingCfg {

@@ -478,3 +478,56 @@ def test_out_of_core_partitions(c1_graph, n, ordered):
     p.set_vertex(V)
     assert np.array_equal(p.vertex(), V)
     p.close()
+
+
+@pytest.mark.parametrize("d,K", [(128, 1), (96, 2), (64, 3)])
+def test_ring_kernel_math_matches_ordered_on_disjoint_rows(d, K):
+    """The bench kernel (sgd_ring_kernel: 8 lanes per sample, cp.async ring,
+    red.global.add deltas, MUFU sigmoid) element-wise against the ordered
+    kernel on a pool whose samples touch pairwise-disjoint rows (distinct u;
+    v's and negatives all distinct — checked through the negative dump), where
+    the Hogwild schedule cannot matter: the two must agree to fp32 rounding
+    (1e-5 relative per touched row), and untouched rows must be unchanged."""
+    nv, deg = 400_000, 10
+    ids = np.arange(nv, dtype=np.uint32)
+    src = np.concatenate([ids] * (deg // 2))
+    dst = np.concatenate([(ids + k + 1) % nv for k in range(deg // 2)]).astype(np.uint32)
+    rng = np.random.default_rng(d + K)
+    count = 128
+    for attempt in range(20):
+        u = rng.choice(nv, count, replace=False).astype(np.uint32)
+        v = rng.choice(nv, count, replace=False).astype(np.uint32)
+        pool = np.stack([u, v], axis=1)
+        ctx = {}
+        for mode in (0, 1):
+            g = G.GraphVite(nv, d, 1, K, 0.05, lr_kind=0, ordered=mode, neg_weight=5.0 / K)
+            g.load_edges(src, dst)
+            g.set_context(rng.standard_normal((nv, d)).astype(np.float32) * 0.1 if mode == 0
+                          else ctx[0][1])
+            g.push(pool)
+            G.gv_prepare_episode(g.ctx)
+            negs = G.gv_debug_get_negatives(g.ctx, 0, 0, count, K)  # local = new ids (n = 1)
+            perm, _ = g.partition()
+            ctx[mode] = (g, g.context() if mode == 0 else None, negs, perm)
+        g0, C0, negs, perm = ctx[0]
+        rows = np.concatenate([perm[v], negs.ravel()])
+        if len(np.unique(rows)) == len(rows):
+            break
+        for m in (0, 1):
+            ctx[m][0].close()
+    else:
+        pytest.skip("no collision-free pool drawn")
+    V0 = ctx[0][0].vertex()
+    for m in (0, 1):
+        ctx[m][0].train_episode()
+    Vh, Ch = ctx[0][0].vertex(), ctx[0][0].context()
+    Vo, Co = ctx[1][0].vertex(), ctx[1][0].context()
+    touched_v = np.zeros(nv, bool); touched_v[u] = True
+    inv = np.argsort(perm)
+    touched_c = np.zeros(nv, bool); touched_c[inv[rows]] = True
+    assert np.array_equal(Vh[~touched_v], V0[~touched_v]) and np.array_equal(Ch[~touched_c], C0[~touched_c])
+    assert _rel(Vh[touched_v], Vo[touched_v]) <= 1e-5
+    assert _rel(Ch[touched_c], Co[touched_c]) <= 1e-5
+    assert _rel(Vh[touched_v], V0[touched_v]) > 1e-4  # the update is not vacuous
+    for m in (0, 1):
+        ctx[m][0].close()

@@ -24,6 +24,12 @@ for n, vr, ordered in [(1, 1, 0), (4, 1, 0), (4, 2, 0), (4, 2, 1), (2, 1, 1)]:
     g.train_episode()
     assert np.isfinite(g.vertex()).all()
     g.close()
+g = G.GraphVite(3000, 128, 3, 1, 0.025, host_partitions=1)
+g.load_edges(src, dst)
+g.push(pool)
+g.train_episode()
+assert np.isfinite(g.vertex()).all()
+g.close()
 g = G.GraphVite(3000, 64, 1, 3, 0.025)
 g.load_edges(src, dst)
 g.augment_device(10, 3, 37, 20_011, 5)
