@@ -494,6 +494,7 @@ def test_ring_kernel_math_matches_ordered_on_disjoint_rows(d, K):
     dst = np.concatenate([(ids + k + 1) % nv for k in range(deg // 2)]).astype(np.uint32)
     rng = np.random.default_rng(d + K)
     count = 128
+    C_init = rng.standard_normal((nv, d)).astype(np.float32) * 0.1
     for attempt in range(20):
         u = rng.choice(nv, count, replace=False).astype(np.uint32)
         v = rng.choice(nv, count, replace=False).astype(np.uint32)
@@ -502,22 +503,23 @@ def test_ring_kernel_math_matches_ordered_on_disjoint_rows(d, K):
         for mode in (0, 1):
             g = G.GraphVite(nv, d, 1, K, 0.05, lr_kind=0, ordered=mode, neg_weight=5.0 / K)
             g.load_edges(src, dst)
-            g.set_context(rng.standard_normal((nv, d)).astype(np.float32) * 0.1 if mode == 0
-                          else ctx[0][1])
+            g.set_context(C_init)
+            V_init = g.vertex()
             g.push(pool)
             G.gv_prepare_episode(g.ctx)
             negs = G.gv_debug_get_negatives(g.ctx, 0, 0, count, K)  # local = new ids (n = 1)
             perm, _ = g.partition()
-            ctx[mode] = (g, g.context() if mode == 0 else None, negs, perm)
-        g0, C0, negs, perm = ctx[0]
+            ctx[mode] = (g, negs, perm)
+        g0, negs, perm = ctx[0]
         rows = np.concatenate([perm[v], negs.ravel()])
         if len(np.unique(rows)) == len(rows):
             break
         for m in (0, 1):
+            ctx[m][0].train_episode()  # consume the prepared pool before closing
             ctx[m][0].close()
     else:
         pytest.skip("no collision-free pool drawn")
-    V0 = ctx[0][0].vertex()
+    C0, V0 = C_init, V_init
     for m in (0, 1):
         ctx[m][0].train_episode()
     Vh, Ch = ctx[0][0].vertex(), ctx[0][0].context()
