@@ -101,12 +101,13 @@ typedef struct {
   int transport;          /* world_size > 1: 0 = CUDA IPC peer copies with a shared-
                              memory handshake (default; also runs several ranks on
                              one GPU), 1 = NCCL send/recv                          */
-  int host_partitions;    /* 1 = out-of-core (NEXT-3, Alg. 3 P:248-252 verbatim):
-                             both matrices live in pinned host memory and only the
-                             current block's vertex and context partitions are on
-                             the device (two slots each, the next block's partitions
-                             load while the current block trains). Single rank,
-                             n_partitions >= 2. Default 0. */
+  int host_partitions;    /* 1 = out-of-core (NEXT-3, Alg. 3): both
+                             matrices live in pinned host memory; the device holds
+                             three partition slots per matrix, loaded and written
+                             back on their own streams while blocks train (block
+                             order: steps in pairs, a reordering with the same
+                             result). Single rank, n_partitions >= 2.
+                             Default 0. */
 } gv_options;
 
 /* Per-pool statistics of THIS process (all its virtual ranks). Times are

@@ -141,6 +141,18 @@ enum class PoolState { Idle, Prepared };
 
 }  // namespace
 
+// Residency of one matrix (vertex or context) in out-of-core mode.
+struct HpMat {
+  static constexpr int S = 3;  // device slots
+  int part[S] = {-1, -1, -1};  // partition held by each slot
+  bool dirty[S] = {};          // device copy newer than the host copy
+  uint64_t stamp[S] = {};      // last use (LRU)
+  int last_block[S] = {-1, -1, -1};  // last block of this episode using the slot
+  int prev = -1;               // slot of the previous block
+  cudaEvent_t free_[S] = {}, saved[S] = {}, loaded[S] = {};
+  std::vector<cudaEvent_t> part_saved;  // per partition: its last write-back done
+};
+
 struct gv_ctx {
   // parameters
   uint32_t nv = 0, dim = 0, n = 1, K = 1;
@@ -191,14 +203,14 @@ struct gv_ctx {
   std::vector<Rank> ranks;
   ncclComm_t comm = nullptr;
   bool comm_ready = false;
-  // out-of-core mode (host_partitions): matrices in pinned host memory, two
-  // device slots per matrix
+  // out-of-core mode (host_partitions): matrices in pinned host memory, three
+  // device slots per matrix; loads (H2D) and write-backs (D2H) run on their
+  // own streams so the two PCIe directions overlap each other and the SGD
   float* h_vertex = nullptr;
   float* h_context = nullptr;
-  int vslot_part[2] = {-1, -1};
-  int cslot_part[2] = {-1, -1};
-  int vslot_prev = 1, cslot_prev = 1;  // slot used by the previous block
-  cudaEvent_t ev_vfree[2] = {}, ev_cfree[2] = {}, ev_vload[2] = {}, ev_cload[2] = {};
+  HpMat hpv, hpc;
+  uint64_t hp_clock = 0;
+  cudaStream_t hp_h2d = nullptr, hp_d2h = nullptr;
   bool hp() const { return opt.host_partitions != 0; }
   // CUDA-IPC transport (world_size > 1, transport 0)
   gv::IpcShm* shm = nullptr;
@@ -275,6 +287,8 @@ gv_status sync_all(gv_ctx* c) {
     CK(cudaStreamSynchronize(r.comm));
   }
   if (c->copy_stream) CK(cudaStreamSynchronize(c->copy_stream));
+  if (c->hp_h2d) CK(cudaStreamSynchronize(c->hp_h2d));
+  if (c->hp_d2h) CK(cudaStreamSynchronize(c->hp_d2h));
   return GV_OK;
 }
 
@@ -525,32 +539,76 @@ gv_status run_steps(gv_ctx* c) {
   // descriptors: D == 1 -> one launch per step over all n blocks;
   //              D > 1  -> one launch per block (g), so the first block of a
   //              step can release its context partition early.
-  struct HpAct {  // out-of-core: slots of a block and the transfers before it
-    int vs, cs, vload, vevict, cload, cevict;
+  struct HpUse {  // out-of-core: one matrix's slot for a block and the load before it
+    int s, load;       // slot; partition to load into it (-1: resident)
+    bool wait_saved;   // the slot's old contents are written back first
   };
-  std::vector<HpAct> hp_acts;
+  struct HpWb { int mat, s, p; };  // write-back of slot s (partition p) of matrix mat
+  std::vector<HpUse> hp_use[2];          // per position in hp_order
+  std::vector<std::vector<HpWb>> hp_wb;  // hp_wb[k + 1]: write-backs issued after the k-th block
+  std::vector<std::pair<uint32_t, uint32_t>> hp_order;  // (offset step t, vertex partition i)
   if (c->hp()) {
-    auto pick = [](int* part_of_slot, int& prev, int need, int& load, int& evict) {
-      for (int s = 0; s < 2; ++s)
-        if (part_of_slot[s] == need) {
-          prev = s;
-          load = evict = -1;
-          return s;
-        }
-      const int s = prev == 0 ? 1 : 0;  // keep the previous block's slot (it may still run)
-      evict = part_of_slot[s];
-      load = need;
-      part_of_slot[s] = need;
-      prev = s;
-      return s;
-    };
-    hp_acts.resize(static_cast<size_t>(n) * n);
-    for (uint32_t t = 0; t < n; ++t)
-      for (uint32_t i = 0; i < n; ++i) {  // Alg. 3 order: offset step, then vertex partition
-        HpAct& h = hp_acts[t * n + i];
-        h.vs = pick(c->vslot_part, c->vslot_prev, static_cast<int>(i), h.vload, h.vevict);
-        h.cs = pick(c->cslot_part, c->cslot_prev, static_cast<int>((i + t) % n), h.cload, h.cevict);
+    // Block order: Alg. 3 orders blocks by offset step; a block (i, i+t)
+    // depends only on the blocks sharing its rows, (i, i+t-1) and (i+1, i+t)
+    // of step t-1, so any order respecting those edges gives the same result.
+    // Steps are taken in pairs (t, t+1) as A_{n-1}, A_{n-2}, B_{n-2}, ...,
+    // A_0, B_0, B_{n-1} (A_i = (i, i+t), B_i = (i, i+t+1)): B_i shares its
+    // vertex partition with A_i and its context partition with A_{i+1}, so
+    // with three slots per matrix a block loads one partition instead of two.
+    for (uint32_t t = 0; t < n; t += 2) {
+      if (t + 1 == n) {
+        for (uint32_t i = 0; i < n; ++i) hp_order.push_back({t, i});
+        break;
       }
+      hp_order.push_back({t, n - 1});
+      for (uint32_t i = n - 1; i-- > 0;) {
+        hp_order.push_back({t, i});
+        hp_order.push_back({t + 1, i});
+      }
+      hp_order.push_back({t + 1, n - 1});
+    }
+    // LRU over three slots, never the previous block's slot (it may still
+    // run). A victim's write-back is issued right after its last use, so it
+    // runs during the next block while another slot loads (PCIe duplex).
+    hp_wb.assign(static_cast<size_t>(n) * n + 1, {});
+    HpMat* mats[2] = {&c->hpv, &c->hpc};
+    for (HpMat* M : mats)
+      for (int sl = 0; sl < HpMat::S; ++sl) M->last_block[sl] = -1;
+    for (int mt = 0; mt < 2; ++mt) hp_use[mt].resize(static_cast<size_t>(n) * n);
+    for (size_t k = 0; k < hp_order.size(); ++k) {
+        const uint32_t t = hp_order[k].first, i = hp_order[k].second;
+        const int b = static_cast<int>(k);
+        const int need[2] = {static_cast<int>(i), static_cast<int>((i + t) % n)};
+        for (int mt = 0; mt < 2; ++mt) {
+          HpMat& M = *mats[mt];
+          HpUse& u = hp_use[mt][b];
+          u.s = -1;
+          u.load = -1;
+          u.wait_saved = false;
+          for (int sl = 0; sl < HpMat::S; ++sl)
+            if (M.part[sl] == need[mt]) u.s = sl;
+          if (u.s < 0) {
+            for (int sl = 0; sl < HpMat::S; ++sl)
+              if (sl != M.prev && (u.s < 0 || M.stamp[sl] < M.stamp[u.s])) u.s = sl;
+            if (M.part[u.s] >= 0 && M.dirty[u.s]) {
+              hp_wb[M.last_block[u.s] + 1].push_back({mt, u.s, M.part[u.s]});
+              u.wait_saved = true;
+            }
+            u.load = need[mt];
+            M.part[u.s] = need[mt];
+          }
+          M.dirty[u.s] = true;
+          M.stamp[u.s] = ++c->hp_clock;
+          M.last_block[u.s] = b;
+          M.prev = u.s;
+        }
+      }
+  }
+  std::vector<int> hp_pos;  // position of block (t, i) in hp_order
+  if (c->hp()) {
+    hp_pos.resize(hp_order.size());
+    for (size_t k = 0; k < hp_order.size(); ++k)
+      hp_pos[hp_order[k].first * n + hp_order[k].second] = static_cast<int>(k);
   }
   for (auto& r : c->ranks) {
     std::vector<gv::BlockDesc> desc(static_cast<size_t>(n) * m);
@@ -572,8 +630,8 @@ gv_status run_steps(gv_ctx* c) {
         d.crow0 = static_cast<uint32_t>(c->D == 1 ? c->part.off[j]
                                                   : static_cast<uint64_t>(slot_of[j]) * r.slot_rows);
         if (c->hp()) {
-          d.vrow0 = static_cast<uint32_t>(hp_acts[t * n + i].vs * r.slot_rows);
-          d.crow0 = static_cast<uint32_t>(hp_acts[t * n + i].cs * r.slot_rows);
+          d.vrow0 = static_cast<uint32_t>(hp_use[0][hp_pos[t * n + i]].s * r.slot_rows);
+          d.crow0 = static_cast<uint32_t>(hp_use[1][hp_pos[t * n + i]].s * r.slot_rows);
         }
         d.alias0 = static_cast<uint32_t>(c->part.off[j]);
         d.m = static_cast<uint32_t>(psize(c, j));
@@ -596,71 +654,89 @@ gv_status run_steps(gv_ctx* c) {
     while (r.ev_sgd.size() < need) r.ev_sgd.push_back(new_event(true));
   }
   // enqueue the steps
-  for (uint32_t t = 0; t < n; ++t) {
+  auto launch_blocks = [&](Rank& r, uint32_t t, uint32_t g0, uint32_t cnt_blk) -> gv_status {
+    gv::SgdArgs a{};
+    a.samples = r.blocks.p;
+    a.vertex = r.vertex;
+    a.context = r.context;
+    a.alias = c->d_alias;
+    a.stride = c->stride;
+    a.lr = lr[t];
+    a.neg_weight = c->opt.neg_weight;
+    a.pool_index = e;
+    a.key0 = key0;
+    a.key1 = key1;
+    a.loss_acc = c->opt.compute_loss ? r.loss.p : nullptr;
+    a.hot_rows = c->hot_rows;
+    gv_step_plan plan;
+    gv_plan_step(n, c->D, r.d, t, &plan);
+    a.desc = r.desc.p + t * m + g0;
+    a.nblk = static_cast<int>(cnt_blk);
+    uint64_t tot = 0;
+    for (uint32_t g = g0; g < g0 + cnt_blk; ++g)
+      tot += r.final_off[g * n + plan.cpart[g] + 1] - r.final_off[g * n + plan.cpart[g]];
+    a.total = tot;
+    cudaEvent_t eb = r.ev_sgd[2 * r.sgd_launches], ee = r.ev_sgd[2 * r.sgd_launches + 1];
+    CK(cudaEventRecord(eb, r.compute));
+    if (c->opt.ordered)
+      CK(gv::launch_sgd_ordered(a, c->dim, c->K, r.compute));
+    else
+      CK(gv::launch_sgd_hogwild(a, c->dim, c->K, c->sms, r.compute));
+    CK(cudaEventRecord(ee, r.compute));
+    r.sgd_launches++;
+    r.kernel_launches++;
+    return GV_OK;
+  };
+  if (c->hp()) {
+    // out-of-core (Alg. 3): before block (i, j), its vertex and
+    // context partitions are loaded into device slots; the load and
+    // write-back streams run ahead of the compute stream
+    Rank& r = c->ranks[0];
+    const size_t row_bytes = sizeof(float) * c->stride;
+    HpMat* mats[2] = {&c->hpv, &c->hpc};
+    float* devs[2] = {r.vertex, r.context};
+    float* hosts[2] = {c->h_vertex, c->h_context};
+    auto slot_ptr = [&](int mt, int sl) {
+      return devs[mt] + static_cast<uint64_t>(sl) * r.slot_rows * c->stride;
+    };
+    auto write_back = [&](const HpWb& w) -> gv_status {
+      HpMat& M = *mats[w.mat];
+      CK(cudaStreamWaitEvent(c->hp_d2h, M.free_[w.s], 0));
+      CK(cudaMemcpyAsync(hosts[w.mat] + c->part.off[w.p] * c->stride, slot_ptr(w.mat, w.s),
+                         row_bytes * psize(c, w.p), cudaMemcpyDeviceToHost, c->hp_d2h));
+      CK(cudaEventRecord(M.saved[w.s], c->hp_d2h));
+      CK(cudaEventRecord(M.part_saved[w.p], c->hp_d2h));
+      return GV_OK;
+    };
+    for (const HpWb& w : hp_wb[0])  // victims last used in an earlier episode
+      if (gv_status st = write_back(w)) return st;
+    for (size_t k = 0; k < hp_order.size(); ++k) {
+      for (int mt = 0; mt < 2; ++mt) {
+        const HpUse& u = hp_use[mt][k];
+        HpMat& M = *mats[mt];
+        if (u.load >= 0) {
+          CK(cudaStreamWaitEvent(c->hp_h2d, M.free_[u.s], 0));
+          if (u.wait_saved) CK(cudaStreamWaitEvent(c->hp_h2d, M.saved[u.s], 0));
+          // the host copy of the partition is current (a per-partition event:
+          // a slot's own event is re-recorded by later write-backs)
+          CK(cudaStreamWaitEvent(c->hp_h2d, M.part_saved[u.load], 0));
+          CK(cudaMemcpyAsync(slot_ptr(mt, u.s), hosts[mt] + c->part.off[u.load] * c->stride,
+                             row_bytes * psize(c, u.load), cudaMemcpyHostToDevice, c->hp_h2d));
+          CK(cudaEventRecord(M.loaded[u.s], c->hp_h2d));
+        }
+        CK(cudaStreamWaitEvent(r.compute, M.loaded[u.s], 0));
+      }
+      if (gv_status st = launch_blocks(r, hp_order[k].first, hp_order[k].second, 1)) return st;
+      for (int mt = 0; mt < 2; ++mt) CK(cudaEventRecord(mats[mt]->free_[hp_use[mt][k].s], r.compute));
+      for (const HpWb& w : hp_wb[k + 1])
+        if (gv_status st = write_back(w)) return st;
+    }
+  }
+  for (uint32_t t = 0; t < n && !c->hp(); ++t) {
     for (auto& r : c->ranks) {
-      gv::SgdArgs a{};
-      a.samples = r.blocks.p;
-      a.vertex = r.vertex;
-      a.context = r.context;
-      a.alias = c->d_alias;
-      a.stride = c->stride;
-      a.lr = lr[t];
-      a.neg_weight = c->opt.neg_weight;
-      a.pool_index = e;
-      a.key0 = key0;
-      a.key1 = key1;
-      a.loss_acc = c->opt.compute_loss ? r.loss.p : nullptr;
-      a.hot_rows = c->hot_rows;
       gv_step_plan plan;
       gv_plan_step(n, c->D, r.d, t, &plan);
-      auto launch = [&](uint32_t g0, uint32_t cnt_blk) -> gv_status {
-        a.desc = r.desc.p + t * m + g0;
-        a.nblk = static_cast<int>(cnt_blk);
-        uint64_t tot = 0;
-        for (uint32_t g = g0; g < g0 + cnt_blk; ++g)
-          tot += r.final_off[g * n + plan.cpart[g] + 1] - r.final_off[g * n + plan.cpart[g]];
-        a.total = tot;
-        cudaEvent_t eb = r.ev_sgd[2 * r.sgd_launches], ee = r.ev_sgd[2 * r.sgd_launches + 1];
-        CK(cudaEventRecord(eb, r.compute));
-        if (c->opt.ordered)
-          CK(gv::launch_sgd_ordered(a, c->dim, c->K, r.compute));
-        else
-          CK(gv::launch_sgd_hogwild(a, c->dim, c->K, c->sms, r.compute));
-        CK(cudaEventRecord(ee, r.compute));
-        r.sgd_launches++;
-        r.kernel_launches++;
-        return GV_OK;
-      };
-      if (c->hp()) {
-        // out-of-core (Alg. 3): before block (i, j), send its vertex
-        // and context partitions to the device (writing back what they evict);
-        // the copy stream runs ahead, so block k+1's transfers overlap block k
-        const size_t row_bytes = sizeof(float) * c->stride;
-        for (uint32_t g = 0; g < m; ++g) {
-          const HpAct& h = hp_acts[t * n + g];
-          struct X { int s, load, evict; float* dev; float* host; cudaEvent_t* fr; cudaEvent_t* ld; };
-          const X xs[2] = {{h.vs, h.vload, h.vevict, r.vertex, c->h_vertex, c->ev_vfree, c->ev_vload},
-                           {h.cs, h.cload, h.cevict, r.context, c->h_context, c->ev_cfree, c->ev_cload}};
-          for (const X& x : xs) {
-            if (x.load < 0) continue;
-            float* slot = x.dev + static_cast<uint64_t>(x.s) * r.slot_rows * c->stride;
-            CK(cudaStreamWaitEvent(c->copy_stream, x.fr[x.s], 0));
-            if (x.evict >= 0)
-              CK(cudaMemcpyAsync(x.host + c->part.off[x.evict] * c->stride, slot,
-                                 row_bytes * psize(c, x.evict), cudaMemcpyDeviceToHost, c->copy_stream));
-            CK(cudaMemcpyAsync(slot, x.host + c->part.off[x.load] * c->stride,
-                               row_bytes * psize(c, x.load), cudaMemcpyHostToDevice, c->copy_stream));
-            CK(cudaEventRecord(x.ld[x.s], c->copy_stream));
-          }
-          CK(cudaStreamWaitEvent(r.compute, c->ev_vload[h.vs], 0));
-          CK(cudaStreamWaitEvent(r.compute, c->ev_cload[h.cs], 0));
-          gv_status st = launch(g, 1);
-          if (st) return st;
-          CK(cudaEventRecord(c->ev_vfree[h.vs], r.compute));
-          CK(cudaEventRecord(c->ev_cfree[h.cs], r.compute));
-        }
-        continue;
-      }
+      auto launch = [&](uint32_t g0, uint32_t cnt_blk) { return launch_blocks(r, t, g0, cnt_blk); };
       if (c->D == 1) {
         gv_status st = launch(0, m);
         if (st) return st;
@@ -850,8 +926,8 @@ gv_status setup_device(gv_ctx* c) {
       CK(cudaHostAlloc(&c->h_context, hbytes, cudaHostAllocDefault));
       std::memset(c->h_context, 0, hbytes);
       r.slot_rows = max_part;
-      r.vrows = 2 * max_part;
-      r.crows = 2 * max_part;
+      r.vrows = HpMat::S * max_part;
+      r.crows = HpMat::S * max_part;
       CK(cudaMalloc(&r.vertex, sizeof(float) * r.vrows * c->stride));
       CK(cudaMalloc(&r.context, sizeof(float) * r.crows * c->stride));
       CK(cudaMemset(r.vertex, 0, sizeof(float) * r.vrows * c->stride));
@@ -863,13 +939,20 @@ gv_status setup_device(gv_ctx* c) {
                            r.compute));
         CK(cudaStreamSynchronize(r.compute));
       }
-      for (int k = 0; k < 2; ++k) {
-        c->ev_vfree[k] = new_event(false);
-        c->ev_cfree[k] = new_event(false);
-        c->ev_vload[k] = new_event(false);
-        c->ev_cload[k] = new_event(false);
-        CK(cudaEventRecord(c->ev_vfree[k], r.compute));
-        CK(cudaEventRecord(c->ev_cfree[k], r.compute));
+      CK(cudaStreamCreateWithFlags(&c->hp_h2d, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->hp_d2h, cudaStreamNonBlocking));
+      for (HpMat* M : {&c->hpv, &c->hpc}) {
+        M->part_saved.resize(n);
+        for (cudaEvent_t& e : M->part_saved) {
+          e = new_event(false);
+          CK(cudaEventRecord(e, r.compute));
+        }
+        for (int k = 0; k < HpMat::S; ++k) {
+          for (cudaEvent_t* e : {&M->free_[k], &M->saved[k], &M->loaded[k]}) {
+            *e = new_event(false);
+            CK(cudaEventRecord(*e, r.compute));
+          }
+        }
       }
       r.vrow_first = 0;
     } else {
@@ -1221,16 +1304,16 @@ static gv_status embeddings_io(gv_ctx* c, bool context, float* out, const float*
     Rank& r = c->ranks[0];
     float* host = context ? c->h_context : c->h_vertex;
     float* dev = context ? r.context : r.vertex;
-    int* part_of_slot = context ? c->cslot_part : c->vslot_part;
-    for (int sl = 0; sl < 2; ++sl) {
-      const int p = part_of_slot[sl];
+    HpMat& M = context ? c->hpc : c->hpv;
+    for (int sl = 0; sl < HpMat::S; ++sl) {
+      const int p = M.part[sl];
       if (p < 0) continue;
       float* slot = dev + static_cast<uint64_t>(sl) * r.slot_rows * stride;
-      if (out)
+      if (out && M.dirty[sl])
         CK(cudaMemcpy(host + c->part.off[p] * stride, slot, sizeof(float) * psize(c, p) * stride,
                       cudaMemcpyDeviceToHost));
-      else
-        part_of_slot[sl] = -1;  // overwritten below: drop the device copy
+      M.dirty[sl] = false;
+      if (!out) M.part[sl] = -1;  // overwritten below: drop the device copy
     }
     for (uint32_t id = 0; id < c->nv; ++id) {
       const uint64_t o = static_cast<uint64_t>(c->part.inv_perm[id]) * dim;
@@ -1559,9 +1642,14 @@ void gv_destroy(gv_ctx* c) {
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->h_vertex) cudaFreeHost(c->h_vertex);
   if (c->h_context) cudaFreeHost(c->h_context);
-  for (int k = 0; k < 2; ++k)
-    for (cudaEvent_t e : {c->ev_vfree[k], c->ev_cfree[k], c->ev_vload[k], c->ev_cload[k]})
-      if (e) cudaEventDestroy(e);
+  if (c->hp_h2d) cudaStreamDestroy(c->hp_h2d);
+  if (c->hp_d2h) cudaStreamDestroy(c->hp_d2h);
+  for (HpMat* M : {&c->hpv, &c->hpc})
+    for (int k = 0; k < HpMat::S; ++k)
+      for (cudaEvent_t e : {M->free_[k], M->saved[k], M->loaded[k]})
+        if (e) cudaEventDestroy(e);
+  for (HpMat* M : {&c->hpv, &c->hpc})
+    for (cudaEvent_t e : M->part_saved) cudaEventDestroy(e);
   cudaFree(c->d_packed);
   cudaFree(c->d_alias);
   cudaFree(c->d_woff);
