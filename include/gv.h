@@ -272,6 +272,21 @@ gv_status gv_augment(gv_ctx* ctx, uint32_t walk_len, uint32_t s,
 gv_status gv_augment_device(gv_ctx* ctx, uint32_t walk_len, uint32_t s, uint32_t segments,
                             uint64_t count, uint64_t seed);
 
+/* NEXT-2 ablation of the pool shuffle (tab:shuffle): as
+ * gv_augment_device, with shuffle = GV_SHUFFLE_PSEUDO (the paper's pseudo
+ * shuffle; identical to gv_augment_device), GV_SHUFFLE_NONE (each segment's
+ * pairs in walk order; pseudo-shuffling each segment of it gives the
+ * GV_SHUFFLE_PSEUDO pool), or GV_SHUFFLE_RANDOM (the GV_SHUFFLE_NONE pool
+ * under a keyed pseudo-random bijection of its positions — a 4-round
+ * Feistel network keyed by Philox(seed, 'SHUF') — the GPU analogue of a
+ * full random shuffle; needs 8*count bytes of device scratch).
+ * Errors: as gv_augment_device, plus GV_ERR_INVALID_ARG for another shuffle. */
+#define GV_SHUFFLE_PSEUDO 0
+#define GV_SHUFFLE_NONE 1
+#define GV_SHUFFLE_RANDOM 2
+gv_status gv_augment_device_ex(gv_ctx* ctx, uint32_t walk_len, uint32_t s, uint32_t segments,
+                               uint64_t count, uint64_t seed, int shuffle);
+
 /* Copy the pending (not yet trained) pool to the host: out_pairs[2*cap],
  * *count = its size. Tests. */
 gv_status gv_debug_get_pending(gv_ctx* ctx, uint32_t* out_pairs, uint64_t cap, uint64_t* count);

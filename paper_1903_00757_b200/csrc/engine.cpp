@@ -178,6 +178,7 @@ struct gv_ctx {
   uint32_t* d_wnbr = nullptr;
   uint2* d_walias = nullptr;
   uint2* d_dalias = nullptr;
+  DevBuf<uint2> shuf_tmp;  // random-shuffle ablation scratch
   // shared device tables
   uint32_t* d_packed = nullptr;
   uint2* d_alias = nullptr;
@@ -1413,7 +1414,14 @@ gv_status gv_augment(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_t threads,
 
 gv_status gv_augment_device(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_t segments,
                             uint64_t count, uint64_t seed) {
+  return gv_augment_device_ex(c, walk_len, s, segments, count, seed, GV_SHUFFLE_PSEUDO);
+}
+
+gv_status gv_augment_device_ex(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_t segments,
+                               uint64_t count, uint64_t seed, int shuffle) {
   if (gv_status st = check_ctx(c, true)) return st;
+  if (shuffle != GV_SHUFFLE_PSEUDO && shuffle != GV_SHUFFLE_NONE && shuffle != GV_SHUFFLE_RANDOM)
+    return fail(c, GV_ERR_INVALID_ARG, "shuffle must be GV_SHUFFLE_PSEUDO, _NONE or _RANDOM");
   if (walk_len == 0 || walk_len > 1000 || s == 0 || s > walk_len || segments == 0)
     return fail(c, GV_ERR_INVALID_ARG, "need 0 < walk_len <= 1000, 0 < s <= walk_len, segments > 0");
   if (c->D != 1) return fail(c, GV_ERR_STATE, "gv_augment_device needs a single rank");
@@ -1453,7 +1461,15 @@ gv_status gv_augment_device(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_t s
     c->raw[k] = bigger;
   }
   gv::WalkDev wd{c->d_woff, c->d_wnbr, c->d_walias, c->d_dalias, c->nv};
-  CK(gv::launch_augment(wd, walk_len, s, segments, count, seed, c->raw[k].p + have, c->copy_stream));
+  if (shuffle == GV_SHUFFLE_RANDOM) {  // walk order into scratch, then a keyed permutation
+    CK(c->shuf_tmp.ensure(count));
+    CK(gv::launch_augment(wd, walk_len, s, segments, count, seed, 1, c->shuf_tmp.p,
+                          c->copy_stream));
+    CK(gv::launch_random_permute(c->shuf_tmp.p, count, seed, c->raw[k].p + have, c->copy_stream));
+  } else {
+    CK(gv::launch_augment(wd, walk_len, s, segments, count, seed,
+                          shuffle == GV_SHUFFLE_NONE ? 1 : 0, c->raw[k].p + have, c->copy_stream));
+  }
   CK(cudaEventRecord(c->raw_ready[k], c->copy_stream));
   c->raw_count[k] = have + count;
   return GV_OK;

@@ -786,6 +786,7 @@ constexpr int kAugBlock = 128;
 __global__ void __launch_bounds__(kAugBlock) augment_kernel(WalkDev g, uint32_t L, uint32_t s,
                                                             uint32_t T, uint64_t count,
                                                             uint32_t key0, uint32_t key1,
+                                                            uint32_t no_shuffle,
                                                             uint2* __restrict__ out) {
   extern __shared__ uint32_t sh[];
   uint32_t* walks = sh;                                  // [kAugBlock][L+1]
@@ -853,7 +854,7 @@ __global__ void __launch_bounds__(kAugBlock) augment_kernel(WalkDev g, uint32_t 
           const uint32_t xb = my[bb];
           if (xb == xa) continue;
           const uint32_t j = static_cast<uint32_t>(k % s);
-          out[b + sub_start[j] + k / s] = make_uint2(xa, xb);
+          out[b + (no_shuffle ? k : sub_start[j] + k / s)] = make_uint2(xa, xb);
           ++k;
         }
       }
@@ -1248,7 +1249,8 @@ cudaError_t launch_segmented_copy(const uint2* src, uint2* dst, const CopySeg* s
 }
 
 cudaError_t launch_augment(const WalkDev& g, uint32_t walk_len, uint32_t s, uint32_t segments,
-                           uint64_t count, uint64_t seed, uint2* out, cudaStream_t st) {
+                           uint64_t count, uint64_t seed, uint32_t shuffle, uint2* out,
+                           cudaStream_t st) {
   if (count == 0 || segments == 0) return cudaSuccess;
   const size_t smem = static_cast<size_t>(kAugBlock) * (walk_len + 1) * 4 + 8 + 8 * s;
   static size_t set = 0;
@@ -1260,7 +1262,71 @@ cudaError_t launch_augment(const WalkDev& g, uint32_t walk_len, uint32_t s, uint
   const unsigned grid = std::min<uint32_t>(segments, static_cast<uint32_t>(num_sms()) * 16);
   augment_kernel<<<grid, kAugBlock, smem, st>>>(g, walk_len, s, segments, count,
                                                 static_cast<uint32_t>(seed),
-                                                static_cast<uint32_t>(seed >> 32), out);
+                                                static_cast<uint32_t>(seed >> 32),
+                                                shuffle == 1 ? 1u : 0u, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------ random shuffle (ablation)
+// A keyed bijection of [0, 2^(2h)) by a 4-round Feistel network on h-bit
+// halves, restricted to [0, count) by cycle-walking (the domain is < 4 count,
+// so a walk takes < 4 rounds of the network on average). Each thread moves
+// one pair: a scatter of 8-byte records, the GPU analogue of the random
+// shuffle the paper times (tab:shuffle).
+struct FeistelKey {
+  uint32_t k[4];
+  uint32_t h;  // bits per half
+};
+
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+__device__ __forceinline__ uint64_t feistel(uint64_t x, const FeistelKey& f) {
+  const uint64_t mask = (1ull << f.h) - 1;
+  uint64_t L = x >> f.h, R = x & mask;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint64_t F = mix32(static_cast<uint32_t>(R) ^ f.k[r]) & mask;
+    const uint64_t nl = R;
+    R = L ^ F;
+    L = nl;
+  }
+  return (L << f.h) | R;
+}
+
+__global__ void random_permute_kernel(const uint2* __restrict__ in, uint64_t count, FeistelKey f,
+                                      uint2* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += stride) {
+    uint64_t y = feistel(i, f);
+    while (y >= count) y = feistel(y, f);
+    out[y] = __ldcs(in + i);
+  }
+}
+
+cudaError_t launch_random_permute(const uint2* in, uint64_t count, uint64_t seed, uint2* out,
+                                  cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  uint32_t bits = 2;
+  while (bits < 64 && (1ull << bits) < count) ++bits;
+  FeistelKey f;
+  f.h = (bits + 1) / 2;
+  // round keys: one Philox block of the shuffle seed (host evaluation)
+  const u32x4 r = philox4x32_10(u32x4{0u, 0u, 0u, kTagShuf}, static_cast<uint32_t>(seed),
+                                static_cast<uint32_t>(seed >> 32));
+  f.k[0] = r.x;
+  f.k[1] = r.y;
+  f.k[2] = r.z;
+  f.k[3] = r.w;
+  const unsigned grid = static_cast<unsigned>(num_sms()) * 8;
+  random_permute_kernel<<<grid, 256, 0, st>>>(in, count, f, out);
   return cudaGetLastError();
 }
 

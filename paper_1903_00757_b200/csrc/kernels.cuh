@@ -73,8 +73,15 @@ struct WalkDev {
 };
 // Appends `count` pairs (ORIGINAL ids) to out: `segments` pool segments as in
 // gv_augment with threads = segments (reading R-AUG), one CTA per segment.
+// shuffle: 0 = pseudo shuffle, 1 = none (each segment in walk
+// order) — the ablation of tab:shuffle.
 cudaError_t launch_augment(const WalkDev& g, uint32_t walk_len, uint32_t s, uint32_t segments,
-                           uint64_t count, uint64_t seed, uint2* out, cudaStream_t st);
+                           uint64_t count, uint64_t seed, uint32_t shuffle, uint2* out,
+                           cudaStream_t st);
+// Random shuffle of a pool (tab:shuffle ablation): out[pi(k)] = in[k] for a
+// keyed bijection pi of [0, count) (4-round Feistel network, cycle-walking).
+cudaError_t launch_random_permute(const uint2* in, uint64_t count, uint64_t seed, uint2* out,
+                                  cudaStream_t st);
 
 // ---- bucketing ----
 struct BucketPlan {

@@ -64,5 +64,6 @@ GV_HD uint32_t alias_pick(uint32_t prob, uint32_t alias, uint32_t slot, uint32_t
 
 constexpr uint32_t kTagInit = 0x494E4954u;  // 'INIT'
 constexpr uint32_t kTagWalk = 0x57414C4Bu;  // 'WALK'
+constexpr uint32_t kTagShuf = 0x53485546u;  // 'SHUF'
 
 }  // namespace gv

@@ -21,6 +21,7 @@ STATUS = ["GV_OK", "GV_ERR_INVALID_ARG", "GV_ERR_STATE", "GV_ERR_OUT_OF_RANGE", 
 GV_OK, GV_ERR_INVALID_ARG, GV_ERR_STATE, GV_ERR_OUT_OF_RANGE, GV_ERR_EMPTY, GV_ERR_CAPACITY, \
     GV_ERR_NOMEM, GV_ERR_CUDA, GV_ERR_COMM = range(9)
 GV_LR_CONSTANT, GV_LR_LINEAR = 0, 1
+GV_SHUFFLE_PSEUDO, GV_SHUFFLE_NONE, GV_SHUFFLE_RANDOM = 0, 1, 2
 
 
 class GVError(RuntimeError):
@@ -105,6 +106,8 @@ SIGNATURES = {
     "gv_augment": (st, [ctx_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, u32p]),
     "gv_run": (st, [ctx_p, C.POINTER(gv_augment_cfg), C.c_uint64, C.POINTER(gv_run_report)]),
     "gv_augment_device": (st, [ctx_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64]),
+    "gv_augment_device_ex": (st, [ctx_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
+                                  C.c_int]),
     "gv_debug_get_pending": (st, [ctx_p, u32p, C.c_uint64, u64p]),
     "gv_get_partition": (st, [ctx_p, u32p, u64p]),
     "gv_get_alias": (st, [ctx_p, C.c_uint32, u32p, u32p, C.c_uint64]),
@@ -276,6 +279,11 @@ def gv_augment_device(ctx, walk_len, s, segments, count, seed):
     _ck(lib.gv_augment_device(ctx, walk_len, s, segments, count, seed), ctx)
 
 
+def gv_augment_device_ex(ctx, walk_len, s, segments, count, seed, shuffle):
+    """gv_augment_device with a shuffle mode (tab:shuffle ablation)."""
+    _ck(lib.gv_augment_device_ex(ctx, walk_len, s, segments, count, seed, shuffle), ctx)
+
+
 def gv_debug_get_pending(ctx):
     n = C.c_uint64(0)
     _ck(lib.gv_debug_get_pending(ctx, None, 0, C.byref(n)), ctx)
@@ -419,8 +427,8 @@ class GraphVite:
     def augment(self, walk_len, s, threads, count, seed, out=None):
         return gv_augment(self.ctx, walk_len, s, threads, count, seed, out)
 
-    def augment_device(self, walk_len, s, segments, count, seed):
-        gv_augment_device(self.ctx, walk_len, s, segments, count, seed)
+    def augment_device(self, walk_len, s, segments, count, seed, shuffle=GV_SHUFFLE_PSEUDO):
+        gv_augment_device_ex(self.ctx, walk_len, s, segments, count, seed, shuffle)
 
     def partition(self):
         return gv_get_partition(self.ctx, self.nv, self.n)

@@ -285,6 +285,39 @@ def test_device_augmentation_bitexact(c1_graph, segments, s, count, L):
     p.close()
 
 
+@pytest.mark.parametrize("segments,s,count", [(7, 5, 123_457), (96, 2, 300_000)])
+def test_device_augmentation_shuffle_modes(c1_graph, segments, s, count):
+    """tab:shuffle ablation modes. NONE: each segment in walk order —
+    pseudo-shuffling every segment of it (the oracle's or_pseudo_shuffle,
+    segment t = [count*t/T, count*(t+1)/T)) gives the oracle's pool byte for
+    byte. RANDOM: a permutation of the NONE pool (same multiset of pairs),
+    deterministic in the seed, and far from the identity."""
+    src, dst = c1_graph
+    p = G.GraphVite(C1["nv"], 8, 1)
+    p.load_edges(src, dst)
+    ref = O.Sampler(O.Graph(C1["nv"], src, dst)).augment(40, s, segments, count, 4242)
+    p.augment_device(40, s, segments, count, 4242, shuffle=G.GV_SHUFFLE_NONE)
+    none = G.gv_debug_get_pending(p.ctx)
+    for t in range(segments):
+        b, e = count * t // segments, count * (t + 1) // segments
+        assert np.array_equal(O.pseudo_shuffle(none[b:e], s), ref[b:e]), t
+    assert not np.array_equal(none, ref)
+    p.train_episode()
+    outs = []
+    for _ in range(2):
+        p.augment_device(40, s, segments, count, 4242, shuffle=G.GV_SHUFFLE_RANDOM)
+        outs.append(G.gv_debug_get_pending(p.ctx))
+        p.train_episode()
+    rnd = outs[0]
+    assert np.array_equal(outs[0], outs[1])
+    key = lambda a: np.sort(a[:, 0].astype(np.uint64) << np.uint64(32) | a[:, 1])
+    assert np.array_equal(key(rnd), key(none))
+    assert np.mean(np.all(rnd == none, axis=1)) < 0.01
+    with pytest.raises(G.GVError):
+        p.augment_device(40, s, segments, 10, 1, shuffle=3)
+    p.close()
+
+
 def test_device_pipeline_matches_oracle(c1_graph):
     """gv_run with device augmentation (pool k+1 generated while pool k
     trains), ordered kernel: equals the oracle fed with its own augmentation."""
