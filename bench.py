@@ -172,6 +172,21 @@ def cpu_baseline(src, dst, sample, threads, seed):
             "sample": arm.describe(dt)}
 
 
+def cpu_hogwild(src, dst, sample, threads, seed):
+    """The paper's CPU-baseline class (LINE-style asynchronous SGD on
+    all cores): the oracle trainer with each block's samples over OpenMP
+    threads, lock-free. Context only, like cpu_baseline."""
+    arm = OracleArm(src, dst, sample, threads)
+    cores = os.cpu_count() or 1
+    pool = arm.sampler.augment(CFG["walk"], CFG["s"], threads, sample, seed)
+    t0 = time.perf_counter()
+    arm.t.train_pool_hogwild(pool, cores)
+    dt = time.perf_counter() - t0
+    return {"value": sample / dt, "unit": "samples/s", "cores": cores, "kind": "oracle-hogwild-openmp",
+            "sample": f"{sample} samples (one pool, same augmentation as cpu_baseline), d={CFG['d']}, "
+                      f"n=1, {cores} OpenMP threads, {dt:.2f} s"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -346,9 +361,10 @@ def run_ours(args):
             if not name.startswith("gpu"):
                 pipeline[name + "_produce_ms"] = rep["produce_ms"]
                 pipeline[name + "_train_wait_ms"] = rep["train_wait_ms"]
-    cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    cpu = cpu_hog = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(src, dst, args.cpu_sample, threads, 1000)
+        cpu_hog = cpu_hogwild(src, dst, args.cpu_sample * 4, threads, 1001)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
@@ -364,7 +380,8 @@ def run_ours(args):
                        "virtual_ranks": args.vranks,
                        "host_partitions": bool(args.host_partitions),
                        "mode": "ordered" if args.ordered else "hogwild"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu, "cpu_hogwild": cpu_hog, "e2e": e2e,
+            "gpu_launches": launches,
             "clocks": clk, "pipeline": pipeline,
             "detail": {"ms_total_per_pool": tot_ms, "sgd_ms_per_pool": sgd_ms / args.steps,
                        "bucket_ms": stats["ms_bucket"], "exchange_ms": stats["ms_exchange"],

@@ -488,6 +488,54 @@ int or_trainer_train_pool(or_trainer* t, const uint32_t* pairs, uint64_t count,
   return OR_OK;
 }
 
+/* ---- CPU baseline class (bench.py's cpu_hogwild line only; NOT a parity
+ * reference). The paper's CPU systems train with LINE-style asynchronous SGD
+ * over all cores. This is or_trainer_train_pool with each block's
+ * samples split over `threads` OpenMP threads that update the shared
+ * matrices without locks (Hogwild): same bucketing, Philox negatives and lr
+ * schedule; the result depends on the thread interleaving.                 */
+int or_trainer_train_pool_hogwild(or_trainer* t, const uint32_t* pairs, uint64_t count,
+                                  int threads, double* loss_out) {
+  uint32_t n = t->n;
+  uint64_t* block_off = (uint64_t*)malloc(((size_t)n * n + 1) * 8);
+  uint32_t* lp = (uint32_t*)malloc((count ? count : 1) * 8);
+  if (!block_off || !lp) { free(block_off); free(lp); return OR_ERR_NOMEM; }
+  int rc = or_bucket(pairs, count, t->nv, t->perm, t->part_off, n, lp, block_off);
+  if (rc) { free(block_off); free(lp); return rc; }
+  uint32_t e = t->pool_index, d = t->d;
+  double loss = 0.0;
+  for (uint32_t step = 0; step < n; step++) {
+    float lr = or_lr(t->lr_kind, t->lr0, t->floor_ratio, t->samples_done, t->total);
+    uint64_t step_samples = 0;
+    for (uint32_t i = 0; i < n; i++) {
+      uint32_t j = or_schedule_cid(n, step, i);
+      uint64_t b = (uint64_t)i * n + j;
+      uint64_t cnt = block_off[b + 1] - block_off[b];
+      const uint32_t* blk = lp + 2 * block_off[b];
+      double bl = 0.0;
+#pragma omp parallel for num_threads(threads) schedule(static) reduction(+ : bl)
+      for (int64_t q = 0; q < (int64_t)cnt; q++) {
+        float* C[9];
+        uint32_t u = t->inv_perm[t->part_off[i] + blk[2 * q]];
+        uint32_t v = t->inv_perm[t->part_off[j] + blk[2 * q + 1]];
+        C[0] = t->context + (uint64_t)v * d;
+        for (uint32_t k = 0; k < t->K; k++) {
+          uint32_t nl = negative_local(t, (uint32_t)q, i, j, e, k);
+          C[1 + k] = t->context + (uint64_t)t->inv_perm[t->part_off[j] + nl] * d;
+        }
+        bl += or_sgd_sample(t->vertex + (uint64_t)u * d, C, 1 + t->K, d, lr, t->neg_weight);
+      }
+      loss += bl;
+      step_samples += cnt;
+    }
+    t->samples_done += step_samples;
+  }
+  t->pool_index++;
+  if (loss_out) *loss_out = loss;
+  free(block_off); free(lp);
+  return OR_OK;
+}
+
 int or_trainer_explicit(or_trainer* t, const uint32_t* u, const uint32_t* v,
                         const uint32_t* negs, uint64_t count, float lr) {
   float* C[9];

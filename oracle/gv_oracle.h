@@ -73,6 +73,10 @@ int or_trainer_load_edges(or_trainer* t, const uint32_t* src, const uint32_t* ds
                           const float* w, uint64_t ne);
 int or_trainer_train_pool(or_trainer* t, const uint32_t* pairs, uint64_t count,
                           double* loss_out);
+/* CPU baseline class (bench only, not a parity reference): train_pool with
+ * each block's samples over `threads` OpenMP threads, lock-free. */
+int or_trainer_train_pool_hogwild(or_trainer* t, const uint32_t* pairs, uint64_t count,
+                                  int threads, double* loss_out);
 /* Train one block (i,j) given its local pairs, pool index e and lr. */
 int or_trainer_train_block(or_trainer* t, const uint32_t* local_pairs, uint64_t count,
                            uint32_t i, uint32_t j, uint32_t e, float lr, double* loss_out);

@@ -26,7 +26,9 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (IEEE float, no contraction)."""
     newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
-        cmd = ["gcc", "-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math",
+        # -fopenmp only affects or_trainer_train_pool_hogwild (the CPU
+        # baseline class); every other function is serial
+        cmd = ["gcc", "-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
                "-fPIC", "-shared", "-o", _LIB + ".tmp", _SRC, "-lm"]
         subprocess.check_call(cmd)
         os.replace(_LIB + ".tmp", _LIB)
@@ -71,6 +73,7 @@ def _declare(L):
                                         C.c_float, C.POINTER(vp)]),
         "or_trainer_load_edges": (C.c_int, [vp, u32p, u32p, f32p, C.c_uint64]),
         "or_trainer_train_pool": (C.c_int, [vp, u32p, C.c_uint64, f64p]),
+        "or_trainer_train_pool_hogwild": (C.c_int, [vp, u32p, C.c_uint64, C.c_int, f64p]),
         "or_trainer_train_block": (C.c_int, [vp, u32p, C.c_uint64, C.c_uint32, C.c_uint32,
                                              C.c_uint32, C.c_float, f64p]),
         "or_trainer_negatives": (C.c_int, [vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, u32p]),
@@ -297,6 +300,14 @@ class Trainer:
         loss = C.c_double(0)
         _check(lib().or_trainer_train_pool(self.h, _p(pairs, u32p), len(pairs) // 2,
                                            C.byref(loss)), "train_pool")
+        return loss.value
+
+    def train_pool_hogwild(self, pairs, threads):
+        """CPU baseline class (bench only): OpenMP Hogwild over each block."""
+        pairs = _u32(pairs).reshape(-1)
+        loss = C.c_double(0)
+        _check(lib().or_trainer_train_pool_hogwild(self.h, _p(pairs, u32p), len(pairs) // 2,
+                                                   threads, C.byref(loss)), "train_pool_hogwild")
         return loss.value
 
     def train_block(self, local_pairs, i, j, e, lr_):

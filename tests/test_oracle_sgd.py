@@ -235,3 +235,23 @@ def test_training_learns_link_prediction():
         t.train_pool(synth.edge_pool(tr_s, tr_d, 500_000, seed=10 + k))
     auc = O.linkpred_auc(t.get("vertex"), pos, neg)
     assert auc >= 0.8 and auc > auc0 + 0.2, (auc0, auc)
+
+
+def test_cpu_hogwild_baseline_matches_serial_with_one_thread():
+    """The CPU-baseline class (OpenMP Hogwild, bench only): with one thread it
+    is train_pool exactly; with four it tracks the serial loss."""
+    src, dst = synth.chung_lu(3000, 15_000, seed=1)
+    pool = synth.edge_pool(src, dst, 200_000, seed=9)
+    res = {}
+    for name, fn in [("serial", lambda t: t.train_pool(pool)),
+                     ("hog1", lambda t: t.train_pool_hogwild(pool, 1)),
+                     ("hog4", lambda t: t.train_pool_hogwild(pool, 4))]:
+        t = O.Trainer(3000, 32, 2, K=1, lr0=0.025, lr_kind=1, total_samples=400_000)
+        t.load_edges(src, dst)
+        loss = fn(t) + fn(t)
+        res[name] = (loss, t.get("vertex"), t.get("context"))
+    assert res["hog1"][0] == res["serial"][0]
+    assert np.array_equal(res["hog1"][1], res["serial"][1])
+    assert np.array_equal(res["hog1"][2], res["serial"][2])
+    assert np.isfinite(res["hog4"][1]).all()
+    assert abs(res["hog4"][0] - res["serial"][0]) <= 0.02 * res["serial"][0]
