@@ -335,6 +335,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+__device__ __forceinline__ void bulk_red_row(void* gmem, const void* smem, uint32_t bytes,
+                                             uint64_t pol) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile(
+      "cp.reduce.async.bulk.global.shared::cta.bulk_group.L2::cache_hint.add.f32 [%0], [%1], %2, %3;\n"
+      ::"l"(gmem), "r"(sa), "r"(bytes), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void bulk_row(void* smem, const void* gmem, uint32_t bytes,
                                          uint64_t* bar, uint64_t pol) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
@@ -416,6 +435,12 @@ constexpr int kRingLPS = GV_RING_LPS;  // lanes per sample: 16 (2 samples / warp
 // compute-sanitizer racecheck cannot verify the async-proxy ordering, so the
 // default is LDGSTS; GV_RING_TMA=1 builds the TMA variant.
 constexpr bool kRingTma = GV_RING_TMA != 0;
+// GV_RING_TMA=2: the deltas also leave through the TMA unit — each lane
+// writes its columns of err and g_t U over the stage it has consumed, and one
+// lane per group issues a bulk reduce-add (cp.reduce.async.bulk .add.f32, an
+// element-wise atomic add in L2) per row instead of red.global.add.v4 from
+// registers.
+constexpr bool kRingTmaRed = GV_RING_TMA == 2;
 
 template <int K, int LPS>
 struct RingCfg {
@@ -578,7 +603,7 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
     }
     uint32_t u, c[K + 1], hot;
     ids_of(i, chunk, u, c, hot);
-    const float4* stage = my + st * RC::STAGE;
+    float4* stage = my + st * RC::STAGE;
     Row<CPL> U, C[K + 1], err;
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
@@ -590,6 +615,20 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
         C[t].v[q] = ok ? stage[(1 + t) * 32 + col] : make_float4(0.f, 0.f, 0.f, 0.f);
       err.v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    // delta of row r (0 = vertex, 1 + t = target t): red from registers, or
+    // (kRingTmaRed) written over the consumed stage row for the bulk reduce
+    auto put_delta = [&](int r, uint32_t row, float g, const Row<CPL>& x, uint64_t pol) {
+      if (kRingTmaRed) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          const int col = gl + LPS * q;
+          if (act && col < dim4)
+            stage[r * 32 + col] = make_float4(g * x.v[q].x, g * x.v[q].y, g * x.v[q].z, g * x.v[q].w);
+        }
+      } else {
+        red_rowg<CPL>(r == 0 ? vertex : context, row, stride, gl, LPS, dim4, g, x, act, pol);
+      }
+    };
     bool dup = false;
 #pragma unroll
     for (int t = 1; t <= K; ++t)
@@ -608,8 +647,7 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
         const float pr = ring_rcp(1.0f + e);
         const float g = ((t == 0 ? 1.0f : 0.0f) - pr) * a.lr * (t == 0 ? 1.0f : a.neg_weight);
         axpy<CPL>(err, g, C[t]);
-        red_rowg<CPL>(context, c[t], stride, gl, LPS, dim4, g, U, act,
-                      ((hot >> (1 + t)) & 1u) ? pol_hot : pol_cold);
+        put_delta(1 + t, c[t], g, U, ((hot >> (1 + t)) & 1u) ? pol_hot : pol_cold);
         if (want_loss && act) loss += softplus_e(e, x[t]) + (t == 0 ? 0.0f : x[t]);
       }
     } else {
@@ -624,14 +662,32 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
         const float pr = ring_rcp(1.0f + e);
         const float g = ((t == 0 ? 1.0f : 0.0f) - pr) * a.lr * (t == 0 ? 1.0f : a.neg_weight);
         axpy<CPL>(err, g, C[t]);
-        red_rowg<CPL>(context, c[t], stride, gl, LPS, dim4, g, U, act,
-                      ((hot >> (1 + t)) & 1u) ? pol_hot : pol_cold);
+        put_delta(1 + t, c[t], g, U, ((hot >> (1 + t)) & 1u) ? pol_hot : pol_cold);
         axpy<CPL>(C[t], g, U);
         if (want_loss && act) loss += softplus_e(e, x) + (t == 0 ? 0.0f : x);
       }
     }
-    red_rowg<CPL>(vertex, u, stride, gl, LPS, dim4, 1.0f, err, act,
-                  (hot & 1u) ? pol_hot : pol_cold);
+    put_delta(0, u, 1.0f, err, (hot & 1u) ? pol_hot : pol_cold);
+    if (kRingTmaRed) {
+      // the group's generic writes of the deltas, then one lane hands the
+      // rows to the TMA unit (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (gl == 0) {
+        if (act) {
+#pragma unroll
+          for (int t = 0; t < T; ++t)
+            bulk_red_row((t == 0 ? vertex : context) +
+                             static_cast<uint64_t>(t == 0 ? u : c[t - 1]) * stride,
+                         stage + t * 32, static_cast<uint32_t>(dim4 * 16),
+                         ((hot >> t) & 1u) ? pol_hot : pol_cold);
+        }
+        bulk_commit();
+        // the stage refilled next (iteration i - 1's) must have been read
+        bulk_wait_read<1>();
+      }
+      __syncwarp();
+    }
     if (i + P < iters) issue(i + P, st_in, chunk);
     if (!kRingTma) cp_commit();
     st = (st + 1 == R) ? 0 : st + 1;
@@ -645,6 +701,7 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
     }
   }
   if (!kRingTma) cp_wait<0>();
+  if (kRingTmaRed && gl == 0) bulk_wait_all();
   return loss;
 }
 
