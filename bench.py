@@ -68,6 +68,10 @@ def parse():
     ap.add_argument("--ordered", action="store_true", help="ordered verification kernel (slow)")
     ap.add_argument("--host-partitions", type=int, default=0,
                     help="out-of-core (NEXT-3): n host-resident partitions on one GPU")
+    ap.add_argument("--parts-per-rank", type=int, default=1,
+                    help="m = n / ranks partitions per rank: m >= 2 overlaps each context "
+                         "rotation with the rank's remaining m - 1 blocks of the step (large "
+                         "partitions, e.g. C5 over 8 GPUs)")
     ap.add_argument("--vranks", type=int, default=1,
                     help="run the N-rank schedule (n = vranks) as virtual ranks on one GPU: "
                          "measures bucketing / exchange / rotation overheads, not scaling")
@@ -232,7 +236,8 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     if world > 1:
         dist.init_process_group("gloo" if "GV_BENCH_DEVICE" in os.environ else "nccl")
-    n = world * args.vranks  # one partition per rank (configs[2]); n = 1 on one GPU (configs[1])
+    # one partition per rank by default (configs[2]); n = 1 on one GPU (configs[1])
+    n = world * args.vranks * args.parts_per_rank
     if args.host_partitions:
         n = args.host_partitions
     threads = args.threads or max(1, (os.cpu_count() or 16) // max(1, world))
@@ -308,7 +313,7 @@ def run_ours(args):
     try:  # DRAM bytes of the same kernel from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "sgd_traffic.json")) as f:
             tr = json.load(f)[args.config]  # captured for this config (n = 1)
-        if args.vranks == 1 and world == 1 and not args.host_partitions:
+        if n == 1 and world == 1:
             traffic = tr["dram_bytes_per_sample"] * per_launch_samples
     except Exception:
         pass
@@ -377,7 +382,7 @@ def run_ours(args):
                        f"(chung-lu gamma {CFG['gamma']}), d={CFG['d']}, K={CFG['K']}, walk 40, "
                        f"s={CFG['s']}, pool {P:,} samples per rank, n={n}",
                        "partitions": n, "pool_per_rank": P, "l2": "inputs > L2 (no flush)",
-                       "virtual_ranks": args.vranks,
+                       "virtual_ranks": args.vranks, "parts_per_rank": args.parts_per_rank,
                        "host_partitions": bool(args.host_partitions),
                        "mode": "ordered" if args.ordered else "hogwild"},
             "roofline": roof, "cpu_baseline": cpu, "cpu_hogwild": cpu_hog, "e2e": e2e,
