@@ -309,7 +309,9 @@ typedef struct {
 } gv_augment_cfg;
 typedef struct {
   uint64_t pools, samples;
-  double wall_ms, produce_ms, train_wait_ms, producer_wait_ms;
+  double wall_ms;          /* from the first pool to the last result; excludes the
+                              one-time allocation of the two pinned host pools */
+  double produce_ms, train_wait_ms, producer_wait_ms;
   double loss_sum;
 } gv_run_report;
 gv_status gv_run(gv_ctx* ctx, const gv_augment_cfg* cfg, uint64_t total_samples,

@@ -44,41 +44,78 @@ inline uint32_t draw(const uint32_t* prob, const uint32_t* alias, uint32_t m, co
   return alias_pick(prob[slot], alias[slot], slot, r.z);
 }
 
+// Walks are generated kBatch at a time, one step of every walk of the batch
+// per round, in two phases: (1) read the current node's CSR range, draw the
+// Philox numbers and the alias slot, prefetch the slot's table entries and
+// neighbour; (2) resolve the draw and prefetch the next node's CSR offsets.
+// The batch's independent random accesses are thus in flight together (the
+// walk is a chain of dependent cache misses otherwise). Pairs are emitted in
+// walk order and written straight to their pseudo-shuffled positions, so the
+// segment is exactly the serial definition (R-AUG): walk w, step k draws
+// Philox {w, k, thread, 'WALK'} whatever the batching.
+constexpr uint32_t kBatch = 16;
+
 void fill_segment(const WalkTables& t, uint32_t walk_len, uint32_t s, uint32_t thread,
                   uint64_t cap, uint64_t seed, uint32_t* out) {
   const HostGraph& g = *t.g;
   const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
-  std::vector<uint32_t> seg(2 * cap);
-  std::vector<uint32_t> walk(walk_len + 1);
+  const uint32_t W = walk_len + 1;
+  std::vector<uint32_t> walks(static_cast<size_t>(kBatch) * W);
+  std::vector<uint64_t> sub_start(s);  // pseudo shuffle: pair k -> sub_start[k % s] + k / s
+  uint64_t acc = 0;
+  for (uint32_t j = 0; j < s; ++j) {
+    sub_start[j] = acc;
+    acc += cap > j ? (cap - j + s - 1) / s : 0;
+  }
+  const uint64_t* off = g.off.data();
+  const uint32_t* nbr = g.nbr.data();
+  const uint32_t* ep = t.eprob.data();
+  const uint32_t* ea = t.ealias.data();
+  uint64_t o[kBatch], slot[kBatch];
+  uint32_t rz[kBatch];
   uint64_t filled = 0;
-  for (uint32_t w = 0; filled < cap; ++w) {
-    u32x4 r = philox4x32_10(u32x4{w, 0u, thread, kTagWalk}, k0, k1);
-    walk[0] = draw(t.departure.prob.data(), t.departure.alias.data(), g.nv, r);
-    for (uint32_t k = 1; k <= walk_len; ++k) {
-      const uint32_t x = walk[k - 1];
-      const uint64_t o = g.off[x];
-      const uint32_t m = static_cast<uint32_t>(g.off[x + 1] - o);
-      r = philox4x32_10(u32x4{w, k, thread, kTagWalk}, k0, k1);
-      walk[k] = g.nbr[o + draw(t.eprob.data() + o, t.ealias.data() + o, m, r)];
+  for (uint32_t w0 = 0; filled < cap; w0 += kBatch) {
+    for (uint32_t i = 0; i < kBatch; ++i) {
+      const u32x4 r = philox4x32_10(u32x4{w0 + i, 0u, thread, kTagWalk}, k0, k1);
+      const uint32_t x = draw(t.departure.prob.data(), t.departure.alias.data(), g.nv, r);
+      walks[i * W] = x;
+      __builtin_prefetch(off + x);
     }
-    // pairs within distance s, by increasing start then end position
-    for (uint32_t a = 0; a <= walk_len && filled < cap; ++a) {
-      const uint32_t last = a + s < walk_len ? a + s : walk_len;
-      for (uint32_t b = a + 1; b <= last && filled < cap; ++b) {
-        if (walk[a] == walk[b]) continue;
-        seg[2 * filled] = walk[a];
-        seg[2 * filled + 1] = walk[b];
-        ++filled;
+    for (uint32_t k = 1; k <= walk_len; ++k) {
+      for (uint32_t i = 0; i < kBatch; ++i) {
+        const uint32_t x = walks[i * W + k - 1];
+        o[i] = off[x];
+        const uint32_t m = static_cast<uint32_t>(off[x + 1] - o[i]);
+        const u32x4 r = philox4x32_10(u32x4{w0 + i, k, thread, kTagWalk}, k0, k1);
+        slot[i] = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, m);
+        rz[i] = r.z;
+        __builtin_prefetch(ep + o[i] + slot[i]);
+        __builtin_prefetch(ea + o[i] + slot[i]);
+        __builtin_prefetch(nbr + o[i] + slot[i]);
+      }
+      for (uint32_t i = 0; i < kBatch; ++i) {
+        const uint64_t q = o[i] + slot[i];
+        const uint32_t pick = alias_pick(ep[q], ea[q], static_cast<uint32_t>(slot[i]), rz[i]);
+        const uint32_t x = nbr[o[i] + pick];
+        walks[i * W + k] = x;
+        __builtin_prefetch(off + x);
+      }
+    }
+    // pairs within distance s, walk by walk, by increasing start then end position
+    for (uint32_t i = 0; i < kBatch && filled < cap; ++i) {
+      const uint32_t* walk = walks.data() + static_cast<size_t>(i) * W;
+      for (uint32_t a = 0; a <= walk_len && filled < cap; ++a) {
+        const uint32_t last = a + s < walk_len ? a + s : walk_len;
+        for (uint32_t b = a + 1; b <= last && filled < cap; ++b) {
+          if (walk[a] == walk[b]) continue;
+          const uint64_t pos = sub_start[filled % s] + filled / s;
+          out[2 * pos] = walk[a];
+          out[2 * pos + 1] = walk[b];
+          ++filled;
+        }
       }
     }
   }
-  // pseudo shuffle: sub-block j holds pairs j, j+s, j+2s, ...
-  uint64_t pos = 0;
-  for (uint32_t j = 0; j < s; ++j)
-    for (uint64_t k = j; k < cap; k += s, ++pos) {
-      out[2 * pos] = seg[2 * k];
-      out[2 * pos + 1] = seg[2 * k + 1];
-    }
 }
 
 }  // namespace

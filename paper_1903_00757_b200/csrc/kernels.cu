@@ -1183,8 +1183,9 @@ cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaSt
     const int G = 32 / kRingLPS, R = kRingP + 1;
     const size_t wb = (static_cast<size_t>(G) * R * (K + 2) * 32 + (G * R + 1) / 2) * 16;
     // 4-warp CTAs: one warp per SM sub-partition (3-warp CTAs that fit 9
-    // warps/SM measured slower than 4-warp CTAs at 8 warps/SM: uneven SMSPs)
-    const int warps = wb * 4 <= 200 * 1024 ? 4 : 1;
+    // warps/SM measured slower than 4-warp CTAs at 8 warps/SM: uneven SMSPs);
+    // large K (rows per stage) fits fewer warps per CTA
+    const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / wb)));
     const size_t smem = wb * warps;
     static int occr[8] = {};
     int& o = occr[ki];

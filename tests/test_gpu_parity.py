@@ -434,10 +434,11 @@ def test_ordered_shapes_match_oracle(c1_graph, d, K, n):
     assert _rel(p.context(), o.get("context")) <= 1e-5
 
 
-@pytest.mark.parametrize("d,K", [(96, 1), (64, 3), (132, 1), (256, 2)])
+@pytest.mark.parametrize("d,K", [(96, 1), (64, 3), (132, 1), (256, 2), (128, 8), (512, 1)])
 def test_hogwild_shapes_track_oracle(d, K):
     """Hogwild kernels for other shapes (the ring kernel with masked lanes at
-    d = 96/64, K = 3; the full-warp kernel at d = 132/256): loss per pool within
+    d = 96/64, K = 3, and with 2-warp CTAs at K = 8; the full-warp kernel at
+    d = 132/256/512): loss per pool within
     3% of the oracle's on a 10^5-node graph, finite embeddings."""
     nv, ne = 100_000, 500_000
     src, dst = synth.chung_lu(nv, ne, gamma=2.1, wmax=1000.0, seed=8)

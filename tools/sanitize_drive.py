@@ -24,16 +24,21 @@ for n, vr, ordered in [(1, 1, 0), (4, 1, 0), (4, 2, 0), (4, 2, 1), (2, 1, 1)]:
     g.train_episode()
     assert np.isfinite(g.vertex()).all()
     g.close()
-g = G.GraphVite(3000, 128, 3, 1, 0.025, host_partitions=1)
-g.load_edges(src, dst)
-g.push(pool)
-g.train_episode()
-assert np.isfinite(g.vertex()).all()
-g.close()
+for n in (3, 5):  # out-of-core: three slots, load / write-back streams, paired-step order
+    g = G.GraphVite(3000, 128, n, 1, 0.025, host_partitions=1)
+    g.load_edges(src, dst)
+    for _ in range(2):
+        g.push(pool)
+        g.train_episode()
+    assert np.isfinite(g.vertex()).all()
+    g.close()
 g = G.GraphVite(3000, 64, 1, 3, 0.025)
 g.load_edges(src, dst)
 g.augment_device(10, 3, 37, 20_011, 5)
 g.train_episode()
+for mode in (G.GV_SHUFFLE_NONE, G.GV_SHUFFLE_RANDOM):
+    g.augment_device(10, 3, 37, 20_011, 6, shuffle=mode)
+    g.train_episode()
 G.gv_train_explicit(g.ctx, [0, 1], [2, 3], [[4, 5, 6], [7, 7, 2]], 0.1)
 g.close()
 print("sanitize drive ok")
