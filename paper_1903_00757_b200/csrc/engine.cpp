@@ -120,6 +120,8 @@ struct Rank {
   DevBuf<uint64_t> all_counts;  // NCCL: gathered counts of every rank
   DevBuf<gv::BlockDesc> desc;
   DevBuf<gv::CopySeg> segs;
+  DevBuf<uint64_t> place_args;  // fused exchange: dst_off[bins] | outs[D] (device pointers)
+  gv::BucketPlan plan{};
   DevBuf<double> loss;
   uint64_t* counts_host = nullptr;  // pinned
   std::vector<uint64_t> local_off;  // this rank's local block_off (bins + 1)
@@ -226,6 +228,9 @@ struct gv_ctx {
   cudaEvent_t my_ev_first[gv::kIpcEvRing] = {};
   cudaEvent_t my_ev_rot[gv::kIpcEvRing] = {};
   uint64_t exported_blocks_gen = 0;
+  // receive buffers replaced while peers had them mapped: freed once every
+  // peer has moved past the pool that announced the new handle
+  std::vector<std::pair<uint2*, uint64_t>> blocks_graveyard;  // (ptr, retired at pool e)
   double ipc_timeout = 300.0;
   bool ipc() const { return opt.world_size > 1 && opt.transport == 0; }
   bool use_nccl() const { return opt.world_size > 1 && opt.transport == 1; }
@@ -294,6 +299,111 @@ gv_status sync_all(gv_ctx* c) {
 }
 
 // --------------------------------------------------------------- prepare
+// a5 + a6 fused (D > 1, virtual ranks or CUDA-IPC processes): every local
+// rank s scatters its pool segment straight into the receive buffers of the
+// owners of the block rows. Block (i, j) of owner d = concatenation over
+// source ranks 0..D-1 of their sub-blocks (i, j) in pool order — the global
+// stable counting sort (R-BUCKET) — so source s writes its sub-block (i, j)
+// at final_off_d[(i, j)] + (samples of (i, j) in ranks < s).
+gv_status place_fused(gv_ctx* c, const std::vector<std::vector<uint64_t>>& bc) {
+  const uint32_t n = c->n, m = c->m, bins = n * n, bpr = m * n;
+  const int D = c->D;
+  const uint64_t e = c->pool_index;
+  // final layout of every rank's rows (all ranks: sources need the owners')
+  std::vector<std::vector<uint64_t>> final_off(D, std::vector<uint64_t>(bpr + 1, 0));
+  for (int d = 0; d < D; ++d)
+    for (uint32_t q = 0; q < bpr; ++q)
+      final_off[d][q + 1] = final_off[d][q] + c->global_counts[d * bpr + q];
+  // receive buffers (headroom: pool sizes fluctuate)
+  for (auto& r : c->ranks) {
+    const uint64_t total = final_off[r.d][bpr];
+    if (total > r.blocks.cap) {
+      if (c->ipc() && r.blocks.p) {  // peers may still map it: retire, free later
+        c->blocks_graveyard.push_back({r.blocks.p, e});
+        r.blocks.p = nullptr;
+        r.blocks.cap = 0;
+      }
+      CK(r.blocks.ensure(total + total / 8));
+    }
+  }
+  std::vector<uint2*> outs(D, nullptr);
+  if (c->ipc()) {
+    Rank& r = c->ranks[0];
+    gv::IpcRankShm& me = c->shm->rank[r.d];
+    if (c->exported_blocks_gen != r.blocks.gen) {  // (re)allocated: export again
+      CK(cudaIpcGetMemHandle(&me.blocks_handle, r.blocks.p));
+      me.blocks_gen = me.blocks_gen + 1;
+      c->exported_blocks_gen = r.blocks.gen;
+    }
+    me.recv_epoch.store(e + 1, std::memory_order_release);
+    for (int q = 0; q < D; ++q) {
+      if (q == r.d) {
+        outs[q] = r.blocks.p;
+        continue;
+      }
+      gv::IpcRankShm& pr = c->shm->rank[q];
+      if (!gv::ipc_wait(pr.recv_epoch, e + 1, c->ipc_timeout))
+        return fail(c, GV_ERR_COMM, "IPC timeout waiting for a peer's receive buffer");
+      if (c->peer_blocks_gen[q] != pr.blocks_gen) {
+        if (c->peer_blocks[q]) CK(cudaIpcCloseMemHandle(c->peer_blocks[q]));
+        void* ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, pr.blocks_handle, cudaIpcMemLazyEnablePeerAccess));
+        c->peer_blocks[q] = static_cast<uint2*>(ptr);
+        c->peer_blocks_gen[q] = pr.blocks_gen;
+      }
+      outs[q] = c->peer_blocks[q];
+    }
+    // every peer has moved past the pools that announced newer handles
+    for (auto it = c->blocks_graveyard.begin(); it != c->blocks_graveyard.end();) {
+      if (it->second + 1 < e + 1) {
+        CK(cudaFree(it->first));
+        it = c->blocks_graveyard.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  } else {
+    for (auto& r : c->ranks) outs[r.d] = r.blocks.p;
+  }
+  for (auto& r : c->ranks) {
+    std::vector<uint64_t> args(bins + D);
+    for (uint32_t q = 0; q < bins; ++q) {
+      const uint32_t d = q / bpr;
+      uint64_t off = final_off[d][q - d * bpr];
+      for (int s2 = 0; s2 < r.d; ++s2) off += bc[s2][q];
+      args[q] = off;
+    }
+    for (int d = 0; d < D; ++d) args[bins + d] = reinterpret_cast<uint64_t>(outs[d]);
+    CK(r.place_args.ensure(args.size()));
+    CK(cudaMemcpyAsync(r.place_args.p, args.data(), args.size() * sizeof(uint64_t),
+                       cudaMemcpyHostToDevice, r.compute));  // pageable: staged before return
+    CK(gv::launch_bucket_place(c->raw[c->active].p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
+                               c->part.pbits, r.plan, r.scratch.p, r.place_args.p,
+                               reinterpret_cast<uint2* const*>(r.place_args.p + bins), bpr,
+                               reinterpret_cast<uint32_t*>(r.counts.p + bins + 1), r.compute,
+                               &r.kernel_launches));
+    CK(cudaEventRecord(r.ev_bucket, r.compute));
+    CK(cudaEventRecord(r.ev_exch_sent, r.compute));
+  }
+  // an owner trains its rows only after every source has placed its samples
+  if (c->ipc()) {
+    Rank& r = c->ranks[0];
+    CK(cudaEventRecord(c->my_ev_pull[e & 1], r.compute));
+    c->shm->rank[r.d].pull_epoch.store(e + 1, std::memory_order_release);
+    for (int q = 0; q < D; ++q) {
+      if (q == r.d) continue;
+      if (!gv::ipc_wait(c->shm->rank[q].pull_epoch, e + 1, c->ipc_timeout))
+        return fail(c, GV_ERR_COMM, "IPC timeout waiting for a peer's scatter");
+      CK(cudaStreamWaitEvent(r.compute, c->peer_ev_pull[q][e & 1], 0));
+    }
+  } else {
+    for (auto& d : c->ranks)
+      for (auto& s2 : c->ranks)
+        if (s2.d != d.d) CK(cudaStreamWaitEvent(d.compute, s2.ev_exch_sent, 0));
+  }
+  return GV_OK;
+}
+
 // a3-a6: bucket every local rank's pool segment, exchange block rows.
 gv_status prepare(gv_ctx* c) {
   if (c->state == PoolState::Prepared) return GV_OK;
@@ -309,6 +419,10 @@ gv_status prepare(gv_ctx* c) {
   const int a = c->active;
   const uint32_t n = c->n, bins = n * n;
   const uint64_t P = c->pool_P;
+  // D > 1 without NCCL (virtual ranks, CUDA-IPC processes): the scatter of a5
+  // writes every sample straight into the receive buffer of the rank that
+  // owns its block row (a6 fused into a5); it runs after the counts are known
+  const bool fused = c->D > 1 && !c->use_nccl();
   // 1) bucketing per rank (a3-a5)
   for (auto& r : c->ranks) {
     r.kernel_launches = 0;
@@ -322,38 +436,35 @@ gv_status prepare(gv_ctx* c) {
     }
     CK(cudaStreamWaitEvent(r.compute, c->raw_ready[a], 0));
     CK(cudaEventRecord(r.ev_start, r.compute));
-    const gv::BucketPlan plan = gv::make_bucket_plan(n, r.seg_count);
-    CK(r.scratch.ensure(gv::bucket_scratch_bytes(plan)));
-    DevBuf<uint2>& out = (c->D == 1) ? r.blocks : r.local_blocks;
-    if (c->ipc() && c->pool_index > 0) {
-      // peers pulled their chunks of the previous pool out of local_blocks
-      const uint64_t e = c->pool_index;
-      const bool realloc = out.cap < r.seg_count;
-      for (int q = 0; q < c->D; ++q) {
-        if (q == r.d) continue;
-        if (!gv::ipc_wait(c->shm->rank[q].pull_epoch, e, c->ipc_timeout))
-          return fail(c, GV_ERR_COMM, "IPC timeout waiting for a peer's block pulls");
-        cudaEvent_t ev = c->peer_ev_pull[q][(e - 1) & 1];
-        if (realloc) CK(cudaEventSynchronize(ev));  // the old buffer is freed below
-        else CK(cudaStreamWaitEvent(r.compute, ev, 0));
-      }
-    }
-    CK(out.ensure(r.seg_count));
+    r.plan = gv::make_bucket_plan(n, r.seg_count);
+    CK(r.scratch.ensure(gv::bucket_scratch_bytes(r.plan)));
     CK(cudaMemsetAsync(r.counts.p + bins + 1, 0, sizeof(uint64_t), r.compute));
-    CK(gv::launch_bucket(c->raw[a].p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
-                         c->part.pbits, plan, r.scratch.p, out.p, r.counts.p,
-                         reinterpret_cast<uint32_t*>(r.counts.p + bins + 1), r.compute,
-                         &r.kernel_launches));
-    CK(cudaEventRecord(r.ev_bucket, r.compute));
+    uint32_t* err = reinterpret_cast<uint32_t*>(r.counts.p + bins + 1);
+    if (fused) {
+      CK(gv::launch_bucket_count(c->raw[a].p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
+                                 c->part.pbits, r.plan, r.scratch.p, r.counts.p, err, r.compute,
+                                 &r.kernel_launches));
+    } else {
+      DevBuf<uint2>& out = (c->D == 1) ? r.blocks : r.local_blocks;
+      CK(out.ensure(r.seg_count));
+      CK(gv::launch_bucket(c->raw[a].p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
+                           c->part.pbits, r.plan, r.scratch.p, out.p, r.counts.p, err, r.compute,
+                           &r.kernel_launches));
+      CK(cudaEventRecord(r.ev_bucket, r.compute));
+    }
   }
-  // the raw buffer may be refilled once every rank has bucketed it
-  for (auto& r : c->ranks) CK(cudaStreamWaitEvent(c->copy_stream, r.ev_bucket, 0));
-  CK(cudaEventRecord(c->raw_free[a], c->copy_stream));
-  {
+  // the raw buffer may be refilled once every rank has bucketed (and, fused,
+  // placed) it
+  auto release_raw = [&]() -> gv_status {
+    for (auto& r : c->ranks) CK(cudaStreamWaitEvent(c->copy_stream, r.ev_bucket, 0));
+    CK(cudaEventRecord(c->raw_free[a], c->copy_stream));
     std::lock_guard<std::mutex> lk(c->mu);
     c->last_active = a;
     c->last_count = P;
-  }
+    return GV_OK;
+  };
+  if (!fused)
+    if (gv_status st = release_raw()) return st;
   // 2) counts to the host (NCCL: all-gather first)
   std::vector<std::vector<uint64_t>> cnt(c->D, std::vector<uint64_t>(bins + 2, 0));
   if (c->ipc()) {
@@ -364,11 +475,6 @@ gv_status prepare(gv_ctx* c) {
     CK(cudaStreamSynchronize(r.compute));
     gv::IpcRankShm& me = c->shm->rank[r.d];
     std::memcpy(me.counts[e & 1], r.counts_host, sizeof(uint64_t) * (bins + 2));
-    if (c->exported_blocks_gen != r.local_blocks.gen) {  // (re)allocated: export again
-      CK(cudaIpcGetMemHandle(&me.blocks_handle, r.local_blocks.p));
-      me.blocks_gen = me.blocks_gen + 1;
-      c->exported_blocks_gen = r.local_blocks.gen;
-    }
     me.counts_epoch.store(e + 1, std::memory_order_release);
     for (int q = 0; q < c->D; ++q) {
       if (!gv::ipc_wait(c->shm->rank[q].counts_epoch, e + 1, c->ipc_timeout))
@@ -397,6 +503,8 @@ gv_status prepare(gv_ctx* c) {
   for (int q = 0; q < c->D; ++q) bad |= cnt[q][bins + 1] != 0;
   if (bad) {
     c->state = PoolState::Idle;
+    if (fused)
+      if (gv_status st = release_raw()) return st;
     return fail(c, GV_ERR_OUT_OF_RANGE, "sample pool contains a node id >= num_nodes");
   }
   // per-rank bin counts from block offsets
@@ -412,6 +520,8 @@ gv_status prepare(gv_ctx* c) {
     c->pool_P_global += c->global_counts[b];
     if (c->global_counts[b] > 0xFFFFFFFFull) {
       c->state = PoolState::Idle;
+      if (fused)
+        if (gv_status st = release_raw()) return st;
       return fail(c, GV_ERR_CAPACITY, "a block holds more than 2^32-1 samples");
     }
   }
@@ -423,7 +533,10 @@ gv_status prepare(gv_ctx* c) {
     const uint32_t b0 = r.d * m * n;
     for (uint32_t q = 0; q < m * n; ++q) r.final_off[q + 1] = r.final_off[q] + c->global_counts[b0 + q];
   }
-  if (c->D > 1) {
+  if (fused) {
+    if (gv_status st = place_fused(c, bc)) return st;
+    if (gv_status st = release_raw()) return st;
+  } else if (c->D > 1) {
     // chunk from rank s to rank d = local bins of rows [d m, (d+1) m) of rank s
     auto chunk_begin = [&](int s, int d) { return cnt[s][d * m * n]; };
     auto chunk_len = [&](int s, int d) { return cnt[s][(d + 1) * m * n] - cnt[s][d * m * n]; };
@@ -433,35 +546,7 @@ gv_status prepare(gv_ctx* c) {
       CK(r.recv.ensure(total));
       CK(r.blocks.ensure(total));
     }
-    if (c->ipc()) {
-      // pull: rank d copies each source's chunk out of the source's local blocks
-      Rank& r = c->ranks[0];
-      const uint64_t e = c->pool_index;
-      uint64_t roff = 0;
-      for (int q = 0; q < c->D; ++q) {
-        const uint64_t len = chunk_len(q, r.d);
-        const uint2* src = nullptr;
-        if (q == r.d) {
-          src = r.local_blocks.p;
-        } else if (len) {
-          gv::IpcRankShm& pr = c->shm->rank[q];
-          if (c->peer_blocks_gen[q] != pr.blocks_gen) {
-            if (c->peer_blocks[q]) CK(cudaIpcCloseMemHandle(c->peer_blocks[q]));
-            void* ptr = nullptr;
-            CK(cudaIpcOpenMemHandle(&ptr, pr.blocks_handle, cudaIpcMemLazyEnablePeerAccess));
-            c->peer_blocks[q] = static_cast<uint2*>(ptr);
-            c->peer_blocks_gen[q] = pr.blocks_gen;
-          }
-          src = c->peer_blocks[q];
-        }
-        if (len)
-          CK(cudaMemcpyAsync(r.recv.p + roff, src + chunk_begin(q, r.d), len * sizeof(uint2),
-                             cudaMemcpyDeviceToDevice, r.compute));
-        roff += len;
-      }
-      CK(cudaEventRecord(c->my_ev_pull[e & 1], r.compute));
-      c->shm->rank[r.d].pull_epoch.store(e + 1, std::memory_order_release);
-    } else if (c->use_nccl()) {
+    if (c->use_nccl()) {
       Rank& r = c->ranks[0];
       NK(nccl().GroupStart());
       uint64_t roff = 0;
@@ -475,22 +560,6 @@ gv_status prepare(gv_ctx* c) {
         roff += chunk_len(p, r.d);
       }
       NK(nccl().GroupEnd());
-    } else {
-      // virtual ranks: rank s copies its chunk into rank d's receive buffer
-      for (auto& s : c->ranks) {
-        for (auto& d : c->ranks) CK(cudaStreamWaitEvent(s.compute, d.ev_recv_consumed, 0));
-        for (auto& d : c->ranks) {
-          uint64_t roff = 0;
-          for (int q = 0; q < s.d; ++q) roff += chunk_len(q, d.d);
-          const uint64_t len = chunk_len(s.d, d.d);
-          if (len)
-            CK(cudaMemcpyAsync(d.recv.p + roff, s.local_blocks.p + chunk_begin(s.d, d.d),
-                               len * sizeof(uint2), cudaMemcpyDeviceToDevice, s.compute));
-        }
-        CK(cudaEventRecord(s.ev_exch_sent, s.compute));
-      }
-      for (auto& d : c->ranks)
-        for (auto& s : c->ranks) CK(cudaStreamWaitEvent(d.compute, s.ev_exch_sent, 0));
     }
     // placement: block (i, j) = concatenation of the sub-blocks of ranks 0..D-1
     for (auto& r : c->ranks) {

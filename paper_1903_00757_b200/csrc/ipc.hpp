@@ -23,15 +23,16 @@ constexpr int kIpcSlotRing = 64;
 
 struct IpcRankShm {
   cudaIpcMemHandle_t ctx_handle;          // context slots buffer
-  cudaIpcMemHandle_t blocks_handle;       // local (pre-exchange) blocks of the pool
+  cudaIpcMemHandle_t blocks_handle;       // receive buffer: my block rows of the pool
   uint64_t blocks_gen;                    // bumped when blocks_handle changes
-  cudaIpcEventHandle_t ev_pull[2];        // "pulled my chunks of pool e" (slot e % 2)
+  cudaIpcEventHandle_t ev_pull[2];        // "placed my samples of pool e" (slot e % 2)
   cudaIpcEventHandle_t ev_first[kIpcEvRing];  // "block 0 of global step g done" (slot g % 4)
   cudaIpcEventHandle_t ev_rot[kIpcEvRing];    // "pulled my rotation of step g" (slot g % 4)
   uint32_t first_slot[kIpcSlotRing];      // context slot of send_part at step g (g % 64)
   uint64_t counts[2][kIpcMaxBins];        // block offsets + error flag of pool e (e % 2)
   std::atomic<uint64_t> counts_epoch;     // e + 1: counts/blocks of pool e published
   std::atomic<uint64_t> pull_epoch;       // e + 1: ev_pull of pool e recorded
+  std::atomic<uint64_t> recv_epoch;       // e + 1: receive buffer of pool e ready (handle current)
   std::atomic<uint64_t> first_epoch;      // g + 1: ev_first of step g recorded
   std::atomic<uint64_t> rot_epoch;        // g + 1: ev_rot of step g recorded
   std::atomic<uint64_t> joined;           // init handshake

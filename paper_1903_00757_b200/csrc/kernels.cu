@@ -1051,14 +1051,16 @@ __global__ void __launch_bounds__(1024) bucket_scan_totals_kernel(const uint64_t
 }
 
 // Stable scatter: the tile is split into 8 consecutive warp ranges; a sample's
-// slot = block_off[bin] + (tile's offset in the bin) + (count of the same bin in
+// slot = dst_off[bin] + (tile's offset in the bin) + (count of the same bin in
 // earlier warps of the tile) + (count in earlier chunks of this warp) + (rank
 // among lower lanes of its chunk, __match_any_sync). Tile order, then warp
 // order, then lane order = pool order, so the scatter is a stable counting sort.
+// The slot is in the buffer outs[bin / bins_per_out] — the owner of the
+// block row, possibly a peer GPU's memory mapped over NVLink.
 __global__ void __launch_bounds__(256) bucket_scatter_kernel(
     const uint2* __restrict__ in, uint64_t count, BinCtx b, uint32_t bins, uint32_t tile,
-    uint64_t tiles, const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ block_off,
-    uint2* __restrict__ out, uint32_t* err) {
+    uint64_t tiles, const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ dst_off,
+    uint2* const* __restrict__ outs, uint32_t bins_per_out, uint32_t* err) {
   extern __shared__ uint64_t smem64[];
   uint64_t* base = smem64;                                  // bins
   uint32_t* wcnt = reinterpret_cast<uint32_t*>(base + bins);  // 8 x bins
@@ -1089,7 +1091,7 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(
         wcnt[v * bins + q] = run;
         run += x;
       }
-      base[q] = block_off[q] + cnt[q * tiles + t];
+      base[q] = dst_off[q] + cnt[q * tiles + t];
     }
     __syncthreads();
     for (uint64_t i0 = wbeg; i0 < wend; i0 += 32) {  // pass 2: place
@@ -1101,7 +1103,7 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(
       const bool leader = (__ffs(mask) - 1) == lane;
       if (bin != 0xFFFFFFFFu) {
         const uint64_t pos = base[bin] + wcnt[w * bins + bin] + __popc(mask & lt_mask);
-        out[pos] = loc;
+        outs[bin / bins_per_out][pos] = loc;
       }
       __syncwarp();
       if (bin != 0xFFFFFFFFu && leader) wcnt[w * bins + bin] += __popc(mask);
@@ -1256,7 +1258,67 @@ BucketPlan make_bucket_plan(uint32_t n, uint64_t count) {
 
 size_t bucket_scratch_bytes(const BucketPlan& p) {
   const size_t cnt = static_cast<size_t>(p.bins) * std::max<uint64_t>(p.tiles, 1) * 4;
-  return (cnt + 255) / 256 * 256 + static_cast<size_t>(p.bins) * 8;
+  // per-tile counts | bin totals | one output pointer (launch_bucket)
+  return (cnt + 255) / 256 * 256 + (static_cast<size_t>(p.bins) * 8 + 255) / 256 * 256 + 8;
+}
+
+namespace {
+struct BucketScratch {
+  uint32_t* cnt;
+  uint64_t* bin_total;
+  uint2** outs;  // one pointer, for the single-buffer wrapper
+};
+BucketScratch scratch_parts(void* scratch, const BucketPlan& plan) {
+  const size_t cnt_bytes = static_cast<size_t>(plan.bins) * std::max<uint64_t>(plan.tiles, 1) * 4;
+  char* base = static_cast<char*>(scratch);
+  const size_t tot_off = (cnt_bytes + 255) / 256 * 256;
+  const size_t outs_off = tot_off + (static_cast<size_t>(plan.bins) * 8 + 255) / 256 * 256;
+  return {reinterpret_cast<uint32_t*>(base), reinterpret_cast<uint64_t*>(base + tot_off),
+          reinterpret_cast<uint2**>(base + outs_off)};
+}
+}  // namespace
+
+cudaError_t launch_bucket_count(const uint2* in, uint64_t count, const uint32_t* packed,
+                                uint32_t nv, uint32_t pbits, const BucketPlan& plan,
+                                void* scratch, uint64_t* block_off, uint32_t* err, cudaStream_t s,
+                                int* launches) {
+  BinCtx b{packed, nv, pbits, plan.n};
+  const BucketScratch sc = scratch_parts(scratch, plan);
+  if (plan.tiles == 0) {
+    cudaMemsetAsync(block_off, 0, (plan.bins + 1) * sizeof(uint64_t), s);
+    return cudaGetLastError();
+  }
+  const unsigned grid =
+      static_cast<unsigned>(umin64(plan.tiles, static_cast<uint64_t>(num_sms()) * 4));
+  bucket_hist_kernel<<<grid, 256, plan.bins * 4, s>>>(in, count, b, plan.bins, plan.tile,
+                                                      plan.tiles, sc.cnt, err);
+  bucket_scan_bins_kernel<<<plan.bins, 1024, 0, s>>>(sc.cnt, plan.tiles, sc.bin_total);
+  bucket_scan_totals_kernel<<<1, 1024, 0, s>>>(sc.bin_total, plan.bins, block_off);
+  if (launches) *launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const uint32_t* packed,
+                                uint32_t nv, uint32_t pbits, const BucketPlan& plan,
+                                const void* scratch, const uint64_t* dst_off, uint2* const* outs,
+                                uint32_t bins_per_out, uint32_t* err, cudaStream_t s,
+                                int* launches) {
+  if (plan.tiles == 0) return cudaSuccess;
+  BinCtx b{packed, nv, pbits, plan.n};
+  const BucketScratch sc = scratch_parts(const_cast<void*>(scratch), plan);
+  const unsigned grid =
+      static_cast<unsigned>(umin64(plan.tiles, static_cast<uint64_t>(num_sms()) * 4));
+  const size_t smem = static_cast<size_t>(plan.bins) * (8 + 8 * 4);
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    smem_set = smem;
+  }
+  bucket_scatter_kernel<<<grid, 256, smem, s>>>(in, count, b, plan.bins, plan.tile, plan.tiles,
+                                                sc.cnt, dst_off, outs, bins_per_out, err);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_bucket(const uint2* in, uint64_t count, const uint32_t* packed, uint32_t nv,
@@ -1271,31 +1333,14 @@ cudaError_t launch_bucket(const uint2* in, uint64_t count, const uint32_t* packe
     if (launches) *launches += 1;
     return cudaGetLastError();
   }
-  uint32_t* cnt = static_cast<uint32_t*>(scratch);
-  const size_t cnt_bytes = static_cast<size_t>(plan.bins) * std::max<uint64_t>(plan.tiles, 1) * 4;
-  uint64_t* bin_total =
-      reinterpret_cast<uint64_t*>(static_cast<char*>(scratch) + (cnt_bytes + 255) / 256 * 256);
-  if (plan.tiles == 0) {
-    cudaMemsetAsync(block_off, 0, (plan.bins + 1) * sizeof(uint64_t), s);
-    return cudaGetLastError();
-  }
-  const unsigned grid =
-      static_cast<unsigned>(umin64(plan.tiles, static_cast<uint64_t>(sms) * 4));
-  bucket_hist_kernel<<<grid, 256, plan.bins * 4, s>>>(in, count, b, plan.bins, plan.tile,
-                                                      plan.tiles, cnt, err);
-  bucket_scan_bins_kernel<<<plan.bins, 1024, 0, s>>>(cnt, plan.tiles, bin_total);
-  bucket_scan_totals_kernel<<<1, 1024, 0, s>>>(bin_total, plan.bins, block_off);
-  const size_t smem = static_cast<size_t>(plan.bins) * (8 + 8 * 4);
-  static size_t smem_set = 0;
-  if (smem > 48 * 1024 && smem > smem_set) {
-    cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    smem_set = smem;
-  }
-  bucket_scatter_kernel<<<grid, 256, smem, s>>>(in, count, b, plan.bins, plan.tile, plan.tiles,
-                                                cnt, block_off, out, err);
-  if (launches) *launches += 4;
-  return cudaGetLastError();
+  cudaError_t e = launch_bucket_count(in, count, packed, nv, pbits, plan, scratch, block_off, err,
+                                      s, launches);
+  if (e != cudaSuccess || plan.tiles == 0) return e;
+  uint2** outs = scratch_parts(scratch, plan).outs;  // the single output, one pointer
+  e = cudaMemcpyAsync(outs, &out, sizeof(uint2*), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  return launch_bucket_place(in, count, packed, nv, pbits, plan, scratch, block_off, outs,
+                             plan.bins, err, s, launches);
 }
 
 cudaError_t launch_segmented_copy(const uint2* src, uint2* dst, const CopySeg* segs, int nseg,

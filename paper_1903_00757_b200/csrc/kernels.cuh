@@ -102,6 +102,25 @@ cudaError_t launch_bucket(const uint2* in, uint64_t count, const uint32_t* packe
                           uint2* out, uint64_t* block_off_dev, uint32_t* err_dev,
                           cudaStream_t s, int* launches);
 
+// The same pipeline in two launches around the all-gather of the counts, so
+// that the scatter can write each sample straight into the buffer of the rank
+// that owns its block row (a5 fused with the a6 exchange: peer stores over
+// NVLink, or plain stores for virtual ranks / the local row).
+// Count phase (n > 1): range check + histogram + scans; block_off_dev as
+// above; the per-tile offsets stay in scratch for the place phase.
+cudaError_t launch_bucket_count(const uint2* in, uint64_t count, const uint32_t* packed,
+                                uint32_t nv, uint32_t pbits, const BucketPlan& plan,
+                                void* scratch, uint64_t* block_off_dev, uint32_t* err_dev,
+                                cudaStream_t s, int* launches);
+// Place phase: sample of bin q (stable rank r within this pool's bin q) goes
+// to outs[q / bins_per_out][dst_off[q] + r]. outs (device array of device
+// pointers, peer-mapped allowed) and dst_off[bins] are in device memory.
+cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const uint32_t* packed,
+                                uint32_t nv, uint32_t pbits, const BucketPlan& plan,
+                                const void* scratch, const uint64_t* dst_off,
+                                uint2* const* outs, uint32_t bins_per_out, uint32_t* err_dev,
+                                cudaStream_t s, int* launches);
+
 // Segmented copy (block-row exchange, a6): copy[k] moves len samples.
 struct CopySeg {
   uint64_t src, dst, len;
