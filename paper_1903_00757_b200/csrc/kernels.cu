@@ -931,29 +931,38 @@ struct BinCtx {
 // bin of a sample and its local ids; out-of-range ids raise *err and map to bin 0.
 __device__ __forceinline__ uint32_t bin_of(const BinCtx& b, uint2 p, uint2& local,
                                            uint32_t* err) {
-  if (p.x >= b.nv || p.y >= b.nv) {
-    *err = 1u;
-    local = make_uint2(0, 0);
-    return 0;
-  }
-  const uint32_t a = __ldg(b.packed + p.x), c = __ldg(b.packed + p.y);
+  // branch-free, so that a thread's several samples keep their gathers in flight
+  const bool bad = p.x >= b.nv || p.y >= b.nv;
+  const uint32_t a = __ldg(b.packed + (bad ? 0u : p.x)), c = __ldg(b.packed + (bad ? 0u : p.y));
+  if (bad) *err = 1u;
   if (b.pbits == 0) {
-    local = make_uint2(a, c);
+    local = bad ? make_uint2(0, 0) : make_uint2(a, c);
     return 0;
   }
   const uint32_t sh = 32 - b.pbits, mask = (1u << sh) - 1u;
-  local = make_uint2(a & mask, c & mask);
-  return (a >> sh) * b.n + (c >> sh);
+  local = bad ? make_uint2(0, 0) : make_uint2(a & mask, c & mask);
+  return bad ? 0u : (a >> sh) * b.n + (c >> sh);
 }
 
 __global__ void relabel_kernel(const uint2* __restrict__ in, uint64_t count, BinCtx b,
                                uint2* __restrict__ out, uint64_t* block_off, uint32_t* err) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
-       i += stride) {
-    uint2 loc;
-    bin_of(b, __ldcs(in + i), loc, err);
-    __stcs(out + i, loc);
+  constexpr int U = 4;  // samples per thread in flight
+  for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < count;
+       i0 += U * stride) {
+    uint2 p[U], loc[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const uint64_t i = i0 + j * stride;
+      p[j] = i < count ? __ldcs(in + i) : make_uint2(0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) bin_of(b, p[j], loc[j], err);
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const uint64_t i = i0 + j * stride;
+      if (i < count) __stcs(out + i, loc[j]);
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     block_off[0] = 0;
@@ -969,9 +978,30 @@ __global__ void bucket_hist_kernel(const uint2* __restrict__ in, uint64_t count,
     for (uint32_t q = threadIdx.x; q < bins; q += blockDim.x) hist[q] = 0;
     __syncthreads();
     const uint64_t beg = t * tile, end = umin64(count, beg + tile);
-    for (uint64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
-      uint2 loc;
-      atomicAdd(&hist[bin_of(b, __ldg(in + i), loc, err)], 1u);
+    // 8 samples per thread in flight; warp-aggregated shared atomics (one per
+    // distinct bin of a warp's 32 samples)
+    constexpr int U = 8;
+    for (uint64_t i0 = beg; i0 < end; i0 += U * blockDim.x) {
+      uint32_t bn[U];
+      uint2 p[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const uint64_t i = i0 + j * blockDim.x + threadIdx.x;
+        p[j] = i < end ? __ldcs(in + i) : make_uint2(0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const uint64_t i = i0 + j * blockDim.x + threadIdx.x;
+        uint2 loc;
+        const uint32_t x = bin_of(b, p[j], loc, err);
+        bn[j] = i < end ? x : 0xFFFFFFFFu;
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const uint32_t mask = __match_any_sync(kFull, bn[j]);
+        if (bn[j] != 0xFFFFFFFFu && (__ffs(mask) - 1) == static_cast<int>(threadIdx.x & 31))
+          atomicAdd(&hist[bn[j]], static_cast<uint32_t>(__popc(mask)));
+      }
     }
     __syncthreads();
     for (uint32_t q = threadIdx.x; q < bins; q += blockDim.x) cnt[q * tiles + t] = hist[q];
@@ -1108,6 +1138,108 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(
       __syncwarp();
       if (bin != 0xFFFFFFFFu && leader) wcnt[w * bins + bin] += __popc(mask);
       __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
+// Stable scatter for tiles of kFastTile samples (n <= 11): the same slots as
+// bucket_scatter_kernel, computed from registers (each warp holds its 8
+// chunks of 32 samples), then the tile is sorted by bin in shared memory and
+// written out so that consecutive threads store consecutive slots of a bin
+// (coalesced 128-byte lines instead of 8-byte scattered stores).
+constexpr uint32_t kFastTile = 2048;
+constexpr int kFastChunks = kFastTile / 256;  // chunks of 32 per warp (8 warps)
+
+__global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
+    const uint2* __restrict__ in, uint64_t count, BinCtx b, uint32_t bins, uint64_t tiles,
+    const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ dst_off,
+    uint2* const* __restrict__ outs, uint32_t bins_per_out, uint32_t* err) {
+  extern __shared__ uint64_t smem64[];
+  uint64_t* base = smem64;                                          // [bins]
+  uint2* staged = reinterpret_cast<uint2*>(base + bins);            // [kFastTile]
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(staged + kFastTile);  // [8][bins]
+  uint32_t* tstart = wcnt + 8 * bins;                               // [bins]
+  uint16_t* sbin = reinterpret_cast<uint16_t*>(tstart + bins);      // [kFastTile]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (uint32_t q = threadIdx.x; q < 8 * bins; q += blockDim.x) wcnt[q] = 0;
+    const uint64_t t0 = t * kFastTile;
+    const uint32_t valid = static_cast<uint32_t>(umin64(count - t0, kFastTile));
+    uint32_t bn[kFastChunks];
+    uint2 lc[kFastChunks];
+    uint2 pr[kFastChunks];
+#pragma unroll
+    for (int ch = 0; ch < kFastChunks; ++ch) {
+      const uint32_t k = w * (kFastTile / 8) + ch * 32 + lane;  // position in the tile
+      pr[ch] = k < valid ? __ldcs(in + t0 + k) : make_uint2(0, 0);
+    }
+#pragma unroll
+    for (int ch = 0; ch < kFastChunks; ++ch) {
+      const uint32_t k = w * (kFastTile / 8) + ch * 32 + lane;
+      const uint32_t x = bin_of(b, pr[ch], lc[ch], err);
+      bn[ch] = k < valid ? x : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ch = 0; ch < kFastChunks; ++ch) {  // per-warp bin counts
+      const uint32_t mask = __match_any_sync(kFull, bn[ch]);
+      if (bn[ch] != 0xFFFFFFFFu && (__ffs(mask) - 1) == lane) wcnt[w * bins + bn[ch]] += __popc(mask);
+      __syncwarp();
+    }
+    __syncthreads();
+    // per bin: warp prefixes, the tile's count; then tile-local bin starts
+    for (uint32_t q = threadIdx.x; q < bins; q += blockDim.x) {
+      uint32_t run = 0;
+      for (int v = 0; v < 8; ++v) {
+        const uint32_t x = wcnt[v * bins + q];
+        wcnt[v * bins + q] = run;
+        run += x;
+      }
+      tstart[q] = run;  // the tile's count of bin q (scanned below)
+      base[q] = dst_off[q] + cnt[q * tiles + t];
+    }
+    __syncthreads();
+    if (w == 0) {  // exclusive scan of the tile counts over bins (bins <= 128)
+      uint32_t v[4], sum = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t q = lane * 4 + k;
+        v[k] = q < bins ? tstart[q] : 0u;
+        sum += v[k];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      uint32_t run = incl - sum;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t q = lane * 4 + k;
+        if (q < bins) tstart[q] = run;
+        run += v[k];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ch = 0; ch < kFastChunks; ++ch) {  // sort the tile by bin (stable)
+      const uint32_t mask = __match_any_sync(kFull, bn[ch]);
+      if (bn[ch] != 0xFFFFFFFFu) {
+        const uint32_t pos = tstart[bn[ch]] + wcnt[w * bins + bn[ch]] + __popc(mask & lt_mask);
+        staged[pos] = lc[ch];
+        sbin[pos] = static_cast<uint16_t>(bn[ch]);
+      }
+      __syncwarp();
+      if (bn[ch] != 0xFFFFFFFFu && (__ffs(mask) - 1) == lane) wcnt[w * bins + bn[ch]] += __popc(mask);
+      __syncwarp();
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < valid; k += blockDim.x) {  // coalesced per bin
+      const uint32_t q = sbin[k];
+      outs[q / bins_per_out][base[q] + (k - tstart[q])] = staged[k];
     }
     __syncthreads();
   }
@@ -1308,6 +1440,19 @@ cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const uint32_t*
   const BucketScratch sc = scratch_parts(const_cast<void*>(scratch), plan);
   const unsigned grid =
       static_cast<unsigned>(umin64(plan.tiles, static_cast<uint64_t>(num_sms()) * 4));
+  if (plan.tile == kFastTile && plan.bins <= 128) {
+    const size_t smem = static_cast<size_t>(plan.bins) * (8 + 8 * 4 + 4) + kFastTile * (8 + 2);
+    static size_t fast_set = 0;
+    if (smem > 48 * 1024 && smem > fast_set) {
+      cudaFuncSetAttribute(bucket_scatter_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+      fast_set = smem;
+    }
+    bucket_scatter_fast_kernel<<<grid, 256, smem, s>>>(in, count, b, plan.bins, plan.tiles, sc.cnt,
+                                                       dst_off, outs, bins_per_out, err);
+    if (launches) *launches += 1;
+    return cudaGetLastError();
+  }
   const size_t smem = static_cast<size_t>(plan.bins) * (8 + 8 * 4);
   static size_t smem_set = 0;
   if (smem > 48 * 1024 && smem > smem_set) {
