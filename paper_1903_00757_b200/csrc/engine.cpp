@@ -1725,6 +1725,8 @@ void gv_destroy(gv_ctx* c) {
     if (c->raw_free[k]) cudaEventDestroy(c->raw_free[k]);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (auto& g : c->blocks_graveyard) cudaFree(g.first);
+  c->blocks_graveyard.clear();
   if (c->h_vertex) cudaFreeHost(c->h_vertex);
   if (c->h_context) cudaFreeHost(c->h_context);
   if (c->hp_h2d) cudaStreamDestroy(c->hp_h2d);

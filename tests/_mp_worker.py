@@ -10,22 +10,24 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000):
+def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000, grow=0):
     import synth
     from paper_1903_00757_b200 import gv as G
     d = 32
     src, dst = synth.chung_lu(nv, ne, gamma=2.1, wmax=400.0, seed=11)
-    g = G.GraphVite(nv, d, n, 1, 0.025, total_samples=pools * count, rank=rank, world_size=world,
+    sizes = [count * (4 ** e if grow else 1) for e in range(pools)]  # grow: receive buffers realloc
+    g = G.GraphVite(nv, d, n, 1, 0.025, total_samples=sum(sizes), rank=rank, world_size=world,
                     ordered=ordered, transport=0)
     G.gv_comm_init(g.ctx, bytes.fromhex(uid_hex))
     g.load_edges(src, dst)
     losses = []
     for e in range(pools):
-        pool = synth.edge_pool(src, dst, count, seed=900 + e)
-        g.push(pool[count * rank // world: count * (rank + 1) // world])
+        cnt = sizes[e]
+        pool = synth.edge_pool(src, dst, cnt, seed=900 + e)
+        g.push(pool[cnt * rank // world: cnt * (rank + 1) // world])
         st = g.train_episode()
         losses.append(st["loss_sum"])
-        assert st["samples_global"] == count, st
+        assert st["samples_global"] == cnt, st
     V, C = g.vertex(), g.context()
     perm, off = g.partition()
     m = n // world
@@ -37,4 +39,4 @@ def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000
 if __name__ == "__main__":
     a = sys.argv[1:]
     main(int(a[0]), int(a[1]), a[2], int(a[3]), int(a[4]), int(a[5]), int(a[6]), a[7],
-         *(int(x) for x in a[8:10]))
+         *(int(x) for x in a[8:11]))

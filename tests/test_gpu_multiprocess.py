@@ -1,7 +1,8 @@
 """Multi-process path (world_size > 1, one process per rank) on ONE GPU:
 the ranks are processes sharing cuda:0 and talk through the CUDA-IPC
-transport (peer copies of bucket chunks and context partitions, IPC events,
-a shared-memory handshake). In ordered mode the gathered embeddings must
+transport (the fused scatter stores samples into the owners' mapped receive
+buffers, peer copies of context partitions, IPC events, a shared-memory
+handshake). In ordered mode the gathered embeddings must
 equal the serial oracle within 1e-5 (every row sees the oracle's update
 sequence); in Hogwild mode they must be finite and training must progress."""
 import os
@@ -21,13 +22,14 @@ from paper_1903_00757_b200 import gv as G  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(tmp_path, world, n, pools, count, ordered, nv=4000, ne=20_000):
+def _run(tmp_path, world, n, pools, count, ordered, nv=4000, ne=20_000, grow=0):
     uid = G.gv_comm_unique_id().hex()
     worker = os.path.join(ROOT, "tests", "_mp_worker.py")
     outs = [str(tmp_path / f"r{r}.npz") for r in range(world)]
     env = dict(os.environ, GV_IPC_TIMEOUT="120")
     procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), uid, str(n), str(pools),
-                               str(count), str(ordered), outs[r], str(nv), str(ne)], env=env)
+                               str(count), str(ordered), outs[r], str(nv), str(ne), str(grow)],
+                              env=env)
              for r in range(world)]
     codes = [p.wait(timeout=600) for p in procs]
     assert codes == [0] * world, codes
@@ -44,11 +46,12 @@ def _run(tmp_path, world, n, pools, count, ordered, nv=4000, ne=20_000):
     return V, C, np.sum(losses, axis=0)
 
 
-def _oracle(n, pools, count, nv=4000, ne=20_000):
+def _oracle(n, pools, count, nv=4000, ne=20_000, grow=0):
     src, dst = synth.chung_lu(nv, ne, gamma=2.1, wmax=400.0, seed=11)
-    o = O.Trainer(nv, 32, n, K=1, lr0=0.025, lr_kind=1, total_samples=pools * count)
+    sizes = [count * (4 ** e if grow else 1) for e in range(pools)]
+    o = O.Trainer(nv, 32, n, K=1, lr0=0.025, lr_kind=1, total_samples=sum(sizes))
     o.load_edges(src, dst)
-    loss = [o.train_pool(synth.edge_pool(src, dst, count, seed=900 + e)) for e in range(pools)]
+    loss = [o.train_pool(synth.edge_pool(src, dst, sizes[e], seed=900 + e)) for e in range(pools)]
     return o.get("vertex"), o.get("context"), np.array(loss)
 
 
@@ -61,6 +64,18 @@ def test_processes_ordered_match_oracle(tmp_path, world, n):
     pools, count = 2, 200_001
     V, C, loss = _run(tmp_path, world, n, pools, count, ordered=1)
     Vo, Co, lo = _oracle(n, pools, count)
+    assert _rel(V, Vo) <= 1e-5 and _rel(C, Co) <= 1e-5
+    np.testing.assert_allclose(loss, lo, rtol=1e-4)
+
+
+def test_processes_growing_pools_match_oracle(tmp_path):
+    """Pools of 5e4, 2e5, 8e5 samples: every rank's receive buffer (which its
+    peers map and store into) is replaced twice; the retired buffers are
+    freed only after every peer re-opened the new handle. Ordered mode still
+    equals the oracle."""
+    pools, count = 3, 50_001
+    V, C, loss = _run(tmp_path, 2, 4, pools, count, ordered=1, grow=1)
+    Vo, Co, lo = _oracle(4, pools, count, grow=1)
     assert _rel(V, Vo) <= 1e-5 and _rel(C, Co) <= 1e-5
     np.testing.assert_allclose(loss, lo, rtol=1e-4)
 
