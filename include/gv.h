@@ -268,7 +268,9 @@ gv_status gv_augment(gv_ctx* ctx, uint32_t walk_len, uint32_t s,
  * stream, so it overlaps the training of the previous pool.
  * Errors: GV_ERR_STATE (no graph), GV_ERR_INVALID_ARG (walk_len == 0,
  * s == 0, s > walk_len, segments == 0, walk_len > 1000), GV_ERR_CAPACITY
- * (max_pool_samples), GV_ERR_CUDA. Single-rank contexts only (D == 1). */
+ * (max_pool_samples), GV_ERR_CUDA. With virtual ranks the pool is split
+ * among them as a pushed pool is; with processes (world_size > 1) it is this
+ * rank's pool segment, generated on its own GPU. */
 gv_status gv_augment_device(gv_ctx* ctx, uint32_t walk_len, uint32_t s, uint32_t segments,
                             uint64_t count, uint64_t seed);
 

@@ -169,6 +169,7 @@ struct gv_ctx {
   int sms = 148;
   uint32_t hot_rows = 0;  // L2 retention: local ids below this are evict_last
   std::string err;
+  std::mutex err_mu;  // push may fail on a producer thread while the trainer runs
   bool loaded = false;
   // graph
   gv::HostGraph graph;
@@ -239,7 +240,10 @@ struct gv_ctx {
 namespace {
 
 gv_status fail(gv_ctx* c, gv_status s, const std::string& msg) {
-  if (c) c->err = msg;
+  if (c) {
+    std::lock_guard<std::mutex> lk(c->err_mu);
+    c->err = msg;
+  }
   g_last_error = msg;
   return s;
 }
@@ -1493,7 +1497,6 @@ gv_status gv_augment_device_ex(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_
     return fail(c, GV_ERR_INVALID_ARG, "shuffle must be GV_SHUFFLE_PSEUDO, _NONE or _RANDOM");
   if (walk_len == 0 || walk_len > 1000 || s == 0 || s > walk_len || segments == 0)
     return fail(c, GV_ERR_INVALID_ARG, "need 0 < walk_len <= 1000, 0 < s <= walk_len, segments > 0");
-  if (c->D != 1) return fail(c, GV_ERR_STATE, "gv_augment_device needs a single rank");
   if (count == 0) return GV_OK;
   if (count > (UINT64_MAX / segments)) return fail(c, GV_ERR_CAPACITY, "count * segments overflows");
   CK(cudaSetDevice(c->opt.device));

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000, grow=0):
+def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000, grow=0, aug=0):
     import synth
     from paper_1903_00757_b200 import gv as G
     d = 32
@@ -23,8 +23,12 @@ def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000
     losses = []
     for e in range(pools):
         cnt = sizes[e]
-        pool = synth.edge_pool(src, dst, cnt, seed=900 + e)
-        g.push(pool[cnt * rank // world: cnt * (rank + 1) // world])
+        if aug:  # this rank's pool segment, augmented on its own GPU (NEXT-1)
+            seg = cnt * (rank + 1) // world - cnt * rank // world
+            g.augment_device(40, 2, 16, seg, 500 + 1000 * e + rank)
+        else:
+            pool = synth.edge_pool(src, dst, cnt, seed=900 + e)
+            g.push(pool[cnt * rank // world: cnt * (rank + 1) // world])
         st = g.train_episode()
         losses.append(st["loss_sum"])
         assert st["samples_global"] == cnt, st
@@ -39,4 +43,4 @@ def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000
 if __name__ == "__main__":
     a = sys.argv[1:]
     main(int(a[0]), int(a[1]), a[2], int(a[3]), int(a[4]), int(a[5]), int(a[6]), a[7],
-         *(int(x) for x in a[8:11]))
+         *(int(x) for x in a[8:12]))

@@ -22,13 +22,14 @@ from paper_1903_00757_b200 import gv as G  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(tmp_path, world, n, pools, count, ordered, nv=4000, ne=20_000, grow=0):
+def _run(tmp_path, world, n, pools, count, ordered, nv=4000, ne=20_000, grow=0, aug=0):
     uid = G.gv_comm_unique_id().hex()
     worker = os.path.join(ROOT, "tests", "_mp_worker.py")
     outs = [str(tmp_path / f"r{r}.npz") for r in range(world)]
     env = dict(os.environ, GV_IPC_TIMEOUT="120")
     procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), uid, str(n), str(pools),
-                               str(count), str(ordered), outs[r], str(nv), str(ne), str(grow)],
+                               str(count), str(ordered), outs[r], str(nv), str(ne), str(grow),
+                               str(aug)],
                               env=env)
              for r in range(world)]
     codes = [p.wait(timeout=600) for p in procs]
@@ -78,6 +79,26 @@ def test_processes_growing_pools_match_oracle(tmp_path):
     Vo, Co, lo = _oracle(4, pools, count, grow=1)
     assert _rel(V, Vo) <= 1e-5 and _rel(C, Co) <= 1e-5
     np.testing.assert_allclose(loss, lo, rtol=1e-4)
+
+
+def test_processes_device_augmentation_match_oracle(tmp_path):
+    """Each process augments its own pool segment on its GPU
+    (gv_augment_device, walk 40, s = 2, 16 segments, seed per rank and
+    pool); the pool is the concatenation of the ranks' segments in rank
+    order. Ordered mode equals the oracle trained on the oracle's
+    augmentation of the same segments."""
+    world, n, pools, count = 2, 2, 2, 200_000
+    V, C, loss = _run(tmp_path, world, n, pools, count, ordered=1, aug=1)
+    nv, ne = 4000, 20_000
+    src, dst = synth.chung_lu(nv, ne, gamma=2.1, wmax=400.0, seed=11)
+    o = O.Trainer(nv, 32, n, K=1, lr0=0.025, lr_kind=1, total_samples=pools * count)
+    o.load_edges(src, dst)
+    sampler = O.Sampler(O.Graph(nv, src, dst))
+    for e in range(pools):
+        segs = [sampler.augment(40, 2, 16, count * (r + 1) // world - count * r // world,
+                                500 + 1000 * e + r) for r in range(world)]
+        o.train_pool(np.concatenate(segs))
+    assert _rel(V, o.get("vertex")) <= 1e-5 and _rel(C, o.get("context")) <= 1e-5
 
 
 def test_processes_hogwild_runs(tmp_path):

@@ -318,16 +318,19 @@ def test_device_augmentation_shuffle_modes(c1_graph, segments, s, count):
     p.close()
 
 
-def test_device_pipeline_matches_oracle(c1_graph):
+@pytest.mark.parametrize("n,vr", [(2, 1), (4, 4)])
+def test_device_pipeline_matches_oracle(c1_graph, n, vr):
     """gv_run with device augmentation (pool k+1 generated while pool k
-    trains), ordered kernel: equals the oracle fed with its own augmentation."""
+    trains), ordered kernel: equals the oracle fed with its own augmentation
+    (also with 4 virtual ranks: the device pool is split among them)."""
     src, dst = c1_graph
     P, pools, segs = 300_000, 3, 96
-    g = G.GraphVite(C1["nv"], 64, 2, 1, 0.025, total_samples=P * pools, ordered=1)
+    g = G.GraphVite(C1["nv"], 64, n, 1, 0.025, total_samples=P * pools, ordered=1,
+                    virtual_ranks=vr)
     g.load_edges(src, dst)
     rep = G.gv_run(g.ctx, 40, 2, segs, P, 99, P * pools, device=True)
     assert rep["pools"] == pools
-    o = O.Trainer(C1["nv"], 64, 2, K=1, lr0=0.025, lr_kind=1, total_samples=P * pools)
+    o = O.Trainer(C1["nv"], 64, n, K=1, lr0=0.025, lr_kind=1, total_samples=P * pools)
     o.load_edges(src, dst)
     sampler = O.Sampler(O.Graph(C1["nv"], src, dst))
     for k in range(pools):
