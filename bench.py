@@ -72,6 +72,16 @@ def parse():
                     help="m = n / ranks partitions per rank: m >= 2 overlaps each context "
                          "rotation with the rank's remaining m - 1 blocks of the step (large "
                          "partitions, e.g. C5 over 8 GPUs)")
+    # SPEC's run flags (SURVEY §5 "Config / flags"): overrides of the config's
+    # shape and method parameters, recorded in `config`
+    ap.add_argument("--dim", type=int, default=0, help="embedding dimension d")
+    ap.add_argument("--negatives", type=int, default=0, help="negatives per sample K")
+    ap.add_argument("--neg-scale", type=float, default=0.0,
+                    help="negative weight (default 5 / K, R-NEGW)")
+    ap.add_argument("--lr", type=float, default=0.0, help="initial learning rate (default 0.025)")
+    ap.add_argument("--walk-length", type=int, default=0, help="random-walk edges (default 40)")
+    ap.add_argument("--aug-distance", type=int, default=0, help="augmentation distance s")
+    ap.add_argument("--seed", type=int, default=-1, help="negative-sampling Philox seed (default 5)")
     ap.add_argument("--vranks", type=int, default=1,
                     help="run the N-rank schedule (n = vranks) as virtual ranks on one GPU: "
                          "measures bucketing / exchange / rotation overheads, not scaling")
@@ -152,7 +162,8 @@ class OracleArm:
         from oracle import oracle as O
         self.O = O
         self.sample, self.threads = sample, threads
-        self.t = O.Trainer(CFG["nv"], CFG["d"], 1, K=CFG["K"], lr0=0.025, lr_kind=1,
+        self.t = O.Trainer(CFG["nv"], CFG["d"], 1, K=CFG["K"], lr0=CFG["lr"], lr_kind=1,
+                           neg_weight=CFG["neg_weight"], seed=CFG["seed"],
                            total_samples=64 * sample)
         self.t.load_edges(src, dst)
         self.sampler = O.Sampler(O.Graph(CFG["nv"], src, dst))
@@ -245,7 +256,8 @@ def run_ours(args):
     P = args.pool
     steps_total = args.warmup + args.steps
     total_samples = P * n * (steps_total + (0 if args.no_e2e else args.steps))
-    g = G.GraphVite(CFG["nv"], CFG["d"], n, CFG["K"], 0.025, total_samples=total_samples,
+    g = G.GraphVite(CFG["nv"], CFG["d"], n, CFG["K"], CFG["lr"], total_samples=total_samples,
+                    neg_weight=CFG["neg_weight"], seed=CFG["seed"],
                     device=dev, rank=rank, world_size=world, ordered=1 if args.ordered else 0,
                     virtual_ranks=args.vranks, host_partitions=1 if args.host_partitions else 0)
     if world > 1:
@@ -313,14 +325,16 @@ def run_ours(args):
     try:  # DRAM bytes of the same kernel from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "sgd_traffic.json")) as f:
             tr = json.load(f)[args.config]  # captured for this config (n = 1)
-        if n == 1 and world == 1:
+        default_shape = CFG["d"] == CONFIGS[args.config]["d"] and CFG["K"] == CONFIGS[args.config]["K"]
+        if n == 1 and world == 1 and default_shape:
             traffic = tr["dram_bytes_per_sample"] * per_launch_samples
     except Exception:
         pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
             "traffic_source": "profiles/sgd_traffic.json (ncu dram__bytes_read+write per sample x "
-                              "samples per launch)", "kernel": "sgd_ring_kernel<1> (d<=128 Hogwild)",
+                              "samples per launch)", "kernel": (f"sgd_ring_kernel<{CFG['K']}> (d<=128 Hogwild)" if CFG["d"] <= 128
+                       else f"sgd_hogwild_kernel<{CFG['K']}> (d>128 Hogwild)"),
             "peak_source": peak_kind, "sgd_share_of_step": sgd_ms / sum(tot_ms),
             "bytes_per_sample": bps}
     if traffic is not None:
@@ -388,6 +402,9 @@ def run_ours(args):
                        f"s={CFG['s']}, pool {P:,} samples per rank, n={n}",
                        "partitions": n, "pool_per_rank": P, "l2": "inputs > L2 (no flush)",
                        "virtual_ranks": args.vranks, "parts_per_rank": args.parts_per_rank,
+                       "method": {"d": CFG["d"], "K": CFG["K"], "walk": CFG["walk"], "s": CFG["s"],
+                                  "lr0": CFG["lr"], "neg_weight": CFG["neg_weight"],
+                                  "seed": CFG["seed"], "lr_schedule": "linear, floor 1e-4"},
                        "host_partitions": bool(args.host_partitions),
                        "mode": "ordered" if args.ordered else "hogwild"},
             "roofline": roof, "cpu_baseline": cpu, "cpu_hogwild": cpu_hog, "e2e": e2e,
@@ -413,6 +430,15 @@ def main():
     args = parse()
     CFG.clear()
     CFG.update(CONFIGS[args.config])
+    CFG.update(lr=0.025, neg_weight=None, seed=5)
+    for flag, key in [("dim", "d"), ("negatives", "K"), ("walk_length", "walk"),
+                      ("aug_distance", "s"), ("lr", "lr"), ("neg_scale", "neg_weight")]:
+        if getattr(args, flag):
+            CFG[key] = getattr(args, flag)
+    if args.seed >= 0:
+        CFG["seed"] = args.seed
+    if CFG["neg_weight"] is None:
+        CFG["neg_weight"] = 5.0 / CFG["K"]
     if args.pool == 0:
         args.pool = CFG["pool"]
     if args.impl == "reference":

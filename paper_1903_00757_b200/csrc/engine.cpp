@@ -603,6 +603,20 @@ gv_status run_steps(gv_ctx* c) {
   const uint32_t n = c->n, m = c->m;
   const uint32_t e = static_cast<uint32_t>(c->pool_index);
   const uint32_t key0 = static_cast<uint32_t>(c->opt.seed), key1 = static_cast<uint32_t>(c->opt.seed >> 32);
+  // orthogonality of every offset step (Def. 1 / P:229): over all D
+  // ranks the step's blocks use each vertex and each context partition once
+  for (uint32_t t = 0; t < n; ++t) {
+    std::vector<uint8_t> vi(n, 0), cj(n, 0);
+    for (int d = 0; d < c->D; ++d) {
+      gv_step_plan pl;
+      gv_plan_step(n, c->D, d, t, &pl);
+      for (uint32_t g = 0; g < pl.n_blocks; ++g) {
+        if (vi[pl.vpart[g]]++ || cj[pl.cpart[g]]++)
+          return fail(c, GV_ERR_STATE, "internal: offset step " + std::to_string(t) +
+                                           " is not orthogonal");
+      }
+    }
+  }
   // lr per offset step from the global sample counts (R-LR)
   std::vector<float> lr(n);
   uint64_t s_before = c->samples_done;
