@@ -576,3 +576,45 @@ def test_ring_kernel_math_matches_ordered_on_disjoint_rows(d, K):
     assert _rel(Vh[touched_v], V0[touched_v]) > 1e-4  # the update is not vacuous
     for m in (0, 1):
         ctx[m][0].close()
+
+
+@pytest.mark.parametrize("case", ["same_sample", "self_pairs", "one_block", "tiny_partitions"])
+def test_degenerate_pools_match_oracle(case):
+    """Degenerate inputs in ordered mode against the oracle (SURVEY §8(b):
+    u == v is accepted; R-DUP): a pool of one repeated sample (every update
+    hits the same three rows), a pool of self-pairs, a pool whose samples
+    all fall into one block of the grid, and n = 8 partitions of a 24-node
+    graph (three members each)."""
+    if case == "tiny_partitions":
+        nv = 24
+        src = np.arange(nv, dtype=np.uint32)
+        dst = ((src + 1) % nv).astype(np.uint32)
+        src, dst = np.concatenate([src, src[:12]]), np.concatenate([dst, (src[:12] + 5) % nv])
+        n = 8
+    else:
+        nv = 2000
+        src, dst = _graph(nv, 10_000)
+        n = 4
+    p, o = _pair(nv, src, dst, d=16, n=n, total=60_000, vranks=1)
+    rng = np.random.default_rng(3)
+    if case == "same_sample":
+        pool = np.tile(np.array([[int(src[0]), int(dst[0])]], np.uint32), (20_000, 1))
+    elif case == "self_pairs":
+        u = rng.integers(0, nv, 20_000).astype(np.uint32)
+        pool = np.stack([u, u], 1)
+    elif case == "one_block":
+        perm, off = p.partition()
+        inv = np.argsort(perm)
+        members_i = inv[off[1]:off[2]]  # original ids of partition 1
+        members_j = inv[off[3]:off[4]]  # and of partition 3: block (1, 3) only
+        pool = np.stack([rng.choice(members_i, 20_000), rng.choice(members_j, 20_000)], 1).astype(np.uint32)
+    else:
+        pool = synth.edge_pool(src, dst, 20_000, seed=7)
+    for _ in range(3):
+        p.push(pool)
+        lg = p.train_episode()["loss_sum"]
+        lo = o.train_pool(pool)
+        assert abs(lg - lo) <= 1e-4 * max(abs(lo), 1.0)
+    assert _rel(p.vertex(), o.get("vertex")) <= 1e-5
+    assert _rel(p.context(), o.get("context")) <= 1e-5
+    p.close()
