@@ -81,6 +81,9 @@ def parse():
     ap.add_argument("--lr", type=float, default=0.0, help="initial learning rate (default 0.025)")
     ap.add_argument("--walk-length", type=int, default=0, help="random-walk edges (default 40)")
     ap.add_argument("--aug-distance", type=int, default=0, help="augmentation distance s")
+    ap.add_argument("--gamma", type=float, default=0.0,
+                    help="power-law exponent of the synthetic graph (SURVEY 8(d) proposal)")
+    ap.add_argument("--wmax", type=float, default=0.0, help="expected-degree cap of the graph")
     ap.add_argument("--seed", type=int, default=-1, help="negative-sampling Philox seed (default 5)")
     ap.add_argument("--vranks", type=int, default=1,
                     help="run the N-rank schedule (n = vranks) as virtual ranks on one GPU: "
@@ -398,7 +401,7 @@ def run_ours(args):
             "config": {"workload": (f"{args.config} {CFG['name']}" if world == 1 or args.config != "C2"
                                     else "C3 youtube-shaped grid")
                        + f" synthetic power-law graph {CFG['nv']:,} nodes / {CFG['ne']:,} edges "
-                       f"(chung-lu gamma {CFG['gamma']}), d={CFG['d']}, K={CFG['K']}, walk 40, "
+                       f"(chung-lu gamma {CFG['gamma']}, wmax {CFG['wmax']:g}), d={CFG['d']}, K={CFG['K']}, walk 40, "
                        f"s={CFG['s']}, pool {P:,} samples per rank, n={n}",
                        "partitions": n, "pool_per_rank": P, "l2": "inputs > L2 (no flush)",
                        "virtual_ranks": args.vranks, "parts_per_rank": args.parts_per_rank,
@@ -432,7 +435,8 @@ def main():
     CFG.update(CONFIGS[args.config])
     CFG.update(lr=0.025, neg_weight=None, seed=5)
     for flag, key in [("dim", "d"), ("negatives", "K"), ("walk_length", "walk"),
-                      ("aug_distance", "s"), ("lr", "lr"), ("neg_scale", "neg_weight")]:
+                      ("aug_distance", "s"), ("lr", "lr"), ("neg_scale", "neg_weight"),
+                      ("gamma", "gamma"), ("wmax", "wmax")]:
         if getattr(args, flag):
             CFG[key] = getattr(args, flag)
     if args.seed >= 0:

@@ -944,6 +944,43 @@ __device__ __forceinline__ uint32_t bin_of(const BinCtx& b, uint2 p, uint2& loca
   return bad ? 0u : (a >> sh) * b.n + (c >> sh);
 }
 
+// Lanes of the warp holding the same bin as this lane (for valid bins; an
+// invalid lane, bin 0xFFFFFFFF, matches nobody valid): one ballot per bin bit
+// — a warp multisplit (measured: the n = 32 histograms 1.2-1.6x faster than
+// with __match_any_sync).
+__device__ __forceinline__ uint32_t peer_mask(uint32_t bin, int nbits) {
+  uint32_t m = __ballot_sync(kFull, bin != 0xFFFFFFFFu);
+  for (int k = 0; k < nbits; ++k) {
+    const uint32_t bit = (bin >> k) & 1u;
+    const uint32_t b = __ballot_sync(kFull, bit != 0u);
+    m &= bit ? b : ~b;
+  }
+  return m;
+}
+__device__ __forceinline__ int bin_bits(uint32_t bins) { return bins <= 1 ? 0 : 32 - __clz(bins - 1); }
+
+// Bin of a sample for one bucketing pass (MODE 0: the n x n bin and local
+// ids — the single pass; the two passes of a large grid, an LSD radix sort
+// whose second pass is stable over the first: MODE 1 bins raw ids by the
+// column (context) partition j and keeps the packed values {part|local} of
+// both endpoints; MODE 2 bins those packed values by the row (vertex)
+// partition i). Out-of-range ids raise *err and become bin 0 / (0, 0) in
+// every mode, as in bin_of.
+template <int MODE>
+__device__ __forceinline__ uint32_t pass_bin(const BinCtx& b, uint2 p, uint2& val, uint32_t* err) {
+  if (MODE == 0) return bin_of(b, p, val, err);
+  const uint32_t sh = 32 - b.pbits;
+  if (MODE == 2) {
+    val = p;
+    return p.x >> sh;
+  }
+  const bool bad = p.x >= b.nv || p.y >= b.nv;
+  const uint32_t a = __ldg(b.packed + (bad ? 0u : p.x)), c = __ldg(b.packed + (bad ? 0u : p.y));
+  if (bad) *err = 1u;
+  val = bad ? make_uint2(0, 0) : make_uint2(a, c);
+  return bad ? 0u : c >> sh;
+}
+
 __global__ void relabel_kernel(const uint2* __restrict__ in, uint64_t count, BinCtx b,
                                uint2* __restrict__ out, uint64_t* block_off, uint32_t* err) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -970,10 +1007,12 @@ __global__ void relabel_kernel(const uint2* __restrict__ in, uint64_t count, Bin
   }
 }
 
+template <int MODE>
 __global__ void bucket_hist_kernel(const uint2* __restrict__ in, uint64_t count, BinCtx b,
                                    uint32_t bins, uint32_t tile, uint64_t tiles,
                                    uint32_t* __restrict__ cnt, uint32_t* err) {
   extern __shared__ uint32_t hist[];
+  const int nbits = bin_bits(bins);
   for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     for (uint32_t q = threadIdx.x; q < bins; q += blockDim.x) hist[q] = 0;
     __syncthreads();
@@ -993,12 +1032,12 @@ __global__ void bucket_hist_kernel(const uint2* __restrict__ in, uint64_t count,
       for (int j = 0; j < U; ++j) {
         const uint64_t i = i0 + j * blockDim.x + threadIdx.x;
         uint2 loc;
-        const uint32_t x = bin_of(b, p[j], loc, err);
+        const uint32_t x = pass_bin<MODE>(b, p[j], loc, err);
         bn[j] = i < end ? x : 0xFFFFFFFFu;
       }
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        const uint32_t mask = __match_any_sync(kFull, bn[j]);
+        const uint32_t mask = peer_mask(bn[j], nbits);
         if (bn[j] != 0xFFFFFFFFu && (__ffs(mask) - 1) == static_cast<int>(threadIdx.x & 31))
           atomicAdd(&hist[bn[j]], static_cast<uint32_t>(__popc(mask)));
       }
@@ -1080,77 +1119,27 @@ __global__ void __launch_bounds__(1024) bucket_scan_totals_kernel(const uint64_t
   if (threadIdx.x == blockDim.x - 1) block_off[bins] = run;
 }
 
-// Stable scatter: the tile is split into 8 consecutive warp ranges; a sample's
-// slot = dst_off[bin] + (tile's offset in the bin) + (count of the same bin in
-// earlier warps of the tile) + (count in earlier chunks of this warp) + (rank
-// among lower lanes of its chunk, __match_any_sync). Tile order, then warp
-// order, then lane order = pool order, so the scatter is a stable counting sort.
-// The slot is in the buffer outs[bin / bins_per_out] — the owner of the
-// block row, possibly a peer GPU's memory mapped over NVLink.
-__global__ void __launch_bounds__(256) bucket_scatter_kernel(
-    const uint2* __restrict__ in, uint64_t count, BinCtx b, uint32_t bins, uint32_t tile,
-    uint64_t tiles, const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ dst_off,
-    uint2* const* __restrict__ outs, uint32_t bins_per_out, uint32_t* err) {
-  extern __shared__ uint64_t smem64[];
-  uint64_t* base = smem64;                                  // bins
-  uint32_t* wcnt = reinterpret_cast<uint32_t*>(base + bins);  // 8 x bins
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t lt_mask = (1u << lane) - 1u;
-  const uint32_t sub = tile / 8;
-  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-    for (uint32_t q = threadIdx.x; q < 8 * bins; q += blockDim.x) wcnt[q] = 0;
-    __syncthreads();
-    const uint64_t wbeg = t * tile + static_cast<uint64_t>(w) * sub;
-    const uint64_t wend = umin64(count, wbeg + sub);
-    for (uint64_t i0 = wbeg; i0 < wend; i0 += 32) {  // pass 1: per-warp bin counts
-      const uint64_t i = i0 + lane;
-      uint32_t bin = 0xFFFFFFFFu;
-      if (i < wend) {
-        uint2 loc;
-        bin = bin_of(b, __ldg(in + i), loc, err);
-      }
-      const uint32_t mask = __match_any_sync(kFull, bin);
-      if (bin != 0xFFFFFFFFu && (__ffs(mask) - 1) == lane) wcnt[w * bins + bin] += __popc(mask);
-      __syncwarp();
-    }
-    __syncthreads();
-    for (uint32_t q = threadIdx.x; q < bins; q += blockDim.x) {
-      uint32_t run = 0;
-      for (int v = 0; v < 8; ++v) {
-        const uint32_t x = wcnt[v * bins + q];
-        wcnt[v * bins + q] = run;
-        run += x;
-      }
-      base[q] = dst_off[q] + cnt[q * tiles + t];
-    }
-    __syncthreads();
-    for (uint64_t i0 = wbeg; i0 < wend; i0 += 32) {  // pass 2: place
-      const uint64_t i = i0 + lane;
-      uint32_t bin = 0xFFFFFFFFu;
-      uint2 loc = make_uint2(0, 0);
-      if (i < wend) bin = bin_of(b, __ldg(in + i), loc, err);
-      const uint32_t mask = __match_any_sync(kFull, bin);
-      const bool leader = (__ffs(mask) - 1) == lane;
-      if (bin != 0xFFFFFFFFu) {
-        const uint64_t pos = base[bin] + wcnt[w * bins + bin] + __popc(mask & lt_mask);
-        outs[bin / bins_per_out][pos] = loc;
-      }
-      __syncwarp();
-      if (bin != 0xFFFFFFFFu && leader) wcnt[w * bins + bin] += __popc(mask);
-      __syncwarp();
-    }
-    __syncthreads();
-  }
-}
-
-// Stable scatter for tiles of kFastTile samples (n <= 11): the same slots as
-// bucket_scatter_kernel, computed from registers (each warp holds its 8
-// chunks of 32 samples), then the tile is sorted by bin in shared memory and
-// written out so that consecutive threads store consecutive slots of a bin
-// (coalesced 128-byte lines instead of 8-byte scattered stores).
+// Stable scatter of tiles of kFastTile samples over at most 128 bins. A
+// sample's slot = dst_off[bin] + (the tile's offset in the bin, from the
+// scanned per-tile counts) + (count of the same bin in earlier warps of the
+// tile) + (count in earlier chunks of this warp) + (rank among lower lanes of
+// its chunk, peer_mask) — tile order, then warp order, then lane order = pool
+// order, so the scatter is a stable counting sort. Each warp holds its 8
+// chunks of 32 samples in registers; the tile is sorted by bin in shared
+// memory and written out so that consecutive threads store consecutive slots
+// of a bin (coalesced lines instead of 8-byte scattered stores). The slot is
+// in the buffer outs[bin / bins_per_out] — the owner of the block row,
+// possibly a peer GPU's memory mapped over NVLink.
 constexpr uint32_t kFastTile = 2048;
 constexpr int kFastChunks = kFastTile / 256;  // chunks of 32 per warp (8 warps)
 
+// MODE 0: one pass over the n x n bins (n <= 11). MODE 1 / 2 are the two passes of a large grid (n >= 12, see pass_bin): the
+// bins are the n column / row partitions. In MODE 2 the input is sorted by
+// column, so a sample's rank r among this segment's samples of row i is
+// (its row's samples in earlier columns) + (its rank in block (i, j)), and
+// its slot is adj[i n + j] + r with adj = dst_off(i, j) - that row prefix
+// (bucket_adjust_kernel); outs is indexed by row / bins_per_out.
+template <int MODE>
 __global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
     const uint2* __restrict__ in, uint64_t count, BinCtx b, uint32_t bins, uint64_t tiles,
     const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ dst_off,
@@ -1163,6 +1152,7 @@ __global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
   uint16_t* sbin = reinterpret_cast<uint16_t*>(tstart + bins);      // [kFastTile]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
+  const int nbits = bin_bits(bins);
   for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     for (uint32_t q = threadIdx.x; q < 8 * bins; q += blockDim.x) wcnt[q] = 0;
     const uint64_t t0 = t * kFastTile;
@@ -1178,13 +1168,13 @@ __global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
 #pragma unroll
     for (int ch = 0; ch < kFastChunks; ++ch) {
       const uint32_t k = w * (kFastTile / 8) + ch * 32 + lane;
-      const uint32_t x = bin_of(b, pr[ch], lc[ch], err);
+      const uint32_t x = pass_bin<MODE>(b, pr[ch], lc[ch], err);
       bn[ch] = k < valid ? x : 0xFFFFFFFFu;
     }
     __syncthreads();
 #pragma unroll
     for (int ch = 0; ch < kFastChunks; ++ch) {  // per-warp bin counts
-      const uint32_t mask = __match_any_sync(kFull, bn[ch]);
+      const uint32_t mask = peer_mask(bn[ch], nbits);
       if (bn[ch] != 0xFFFFFFFFu && (__ffs(mask) - 1) == lane) wcnt[w * bins + bn[ch]] += __popc(mask);
       __syncwarp();
     }
@@ -1198,7 +1188,7 @@ __global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
         run += x;
       }
       tstart[q] = run;  // the tile's count of bin q (scanned below)
-      base[q] = dst_off[q] + cnt[q * tiles + t];
+      base[q] = (MODE == 2 ? 0ull : dst_off[q]) + cnt[q * tiles + t];
     }
     __syncthreads();
     if (w == 0) {  // exclusive scan of the tile counts over bins (bins <= 128)
@@ -1226,7 +1216,7 @@ __global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
     __syncthreads();
 #pragma unroll
     for (int ch = 0; ch < kFastChunks; ++ch) {  // sort the tile by bin (stable)
-      const uint32_t mask = __match_any_sync(kFull, bn[ch]);
+      const uint32_t mask = peer_mask(bn[ch], nbits);
       if (bn[ch] != 0xFFFFFFFFu) {
         const uint32_t pos = tstart[bn[ch]] + wcnt[w * bins + bn[ch]] + __popc(mask & lt_mask);
         staged[pos] = lc[ch];
@@ -1239,9 +1229,30 @@ __global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
     __syncthreads();
     for (uint32_t k = threadIdx.x; k < valid; k += blockDim.x) {  // coalesced per bin
       const uint32_t q = sbin[k];
-      outs[q / bins_per_out][base[q] + (k - tstart[q])] = staged[k];
+      if (MODE == 2) {
+        const uint2 v = staged[k];
+        const uint32_t sh = 32 - b.pbits, mask = (1u << sh) - 1u;
+        const uint64_t slot = dst_off[q * b.n + (v.y >> sh)] + base[q] + (k - tstart[q]);
+        outs[q / bins_per_out][slot] = make_uint2(v.x & mask, v.y & mask);
+      } else {
+        outs[q / bins_per_out][base[q] + (k - tstart[q])] = staged[k];
+      }
     }
     __syncthreads();
+  }
+}
+
+// adj[i n + j] = dst_off[i n + j] - (this segment's samples of row i in
+// columns < j): the slot offsets of the second pass of a large grid.
+__global__ void bucket_adjust_kernel(const uint64_t* __restrict__ dst_off,
+                                     const uint64_t* __restrict__ bin_total, uint32_t n,
+                                     uint64_t* __restrict__ adj) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t run = 0;
+  for (uint32_t j = 0; j < n; ++j) {
+    adj[i * n + j] = dst_off[i * n + j] - run;  // modular: the row prefix is added back
+    run += bin_total[i * n + j];
   }
 }
 
@@ -1377,6 +1388,17 @@ cudaError_t launch_init_vertex(float* vertex, uint32_t stride, uint32_t dim, uin
   return cudaGetLastError();
 }
 
+// resident CTAs per SM of the bucketing kernels (GV_BUCKET_CTAS, default 8):
+// their tiles are short and barrier-bound, so more CTAs per SM hide the syncs
+static uint64_t bucket_ctas() {
+  static uint64_t v = 0;
+  if (v == 0) {
+    const char* e = getenv("GV_BUCKET_CTAS");
+    v = (e && atoi(e) > 0) ? static_cast<uint64_t>(atoi(e)) : 8;
+  }
+  return v;
+}
+
 BucketPlan make_bucket_plan(uint32_t n, uint64_t count) {
   BucketPlan p;
   p.n = n;
@@ -1385,13 +1407,39 @@ BucketPlan make_bucket_plan(uint32_t n, uint64_t count) {
   tile = (tile + 255) / 256 * 256;
   p.tile = tile;
   p.tiles = (count + tile - 1) / tile;
+  p.two_pass = p.bins > 128;
+  p.tiles2 = (count + kFastTile - 1) / kFastTile;
   return p;
 }
 
-size_t bucket_scratch_bytes(const BucketPlan& p) {
+namespace {
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+// two-pass area (large grids): output pointer of pass 1 | per-tile column /
+// row counts | column totals | column offsets | slot adjustments | the
+// column-sorted packed samples
+struct TwoPassLayout {
+  size_t outs, cnt, tot, off, adj, tmp, end;
+  TwoPassLayout(const BucketPlan& p, size_t at) {
+    const uint64_t t2 = std::max<uint64_t>(p.tiles2, 1);
+    outs = at;
+    cnt = outs + 256;
+    tot = cnt + align256(static_cast<size_t>(p.n) * t2 * 4);
+    off = tot + align256(static_cast<size_t>(p.n) * 8);
+    adj = off + align256((static_cast<size_t>(p.n) + 1) * 8);
+    tmp = adj + align256(static_cast<size_t>(p.bins) * 8);
+    end = tmp + align256(static_cast<size_t>(t2) * kFastTile * 8);
+  }
+};
+size_t base_scratch_bytes(const BucketPlan& p) {
   const size_t cnt = static_cast<size_t>(p.bins) * std::max<uint64_t>(p.tiles, 1) * 4;
   // per-tile counts | bin totals | one output pointer (launch_bucket)
-  return (cnt + 255) / 256 * 256 + (static_cast<size_t>(p.bins) * 8 + 255) / 256 * 256 + 8;
+  return align256(cnt) + align256(static_cast<size_t>(p.bins) * 8) + 8;
+}
+}  // namespace
+
+size_t bucket_scratch_bytes(const BucketPlan& p) {
+  const size_t b = base_scratch_bytes(p);
+  return p.two_pass ? TwoPassLayout(p, align256(b)).end : b;
 }
 
 namespace {
@@ -1421,9 +1469,9 @@ cudaError_t launch_bucket_count(const uint2* in, uint64_t count, const uint32_t*
     return cudaGetLastError();
   }
   const unsigned grid =
-      static_cast<unsigned>(umin64(plan.tiles, static_cast<uint64_t>(num_sms()) * 4));
-  bucket_hist_kernel<<<grid, 256, plan.bins * 4, s>>>(in, count, b, plan.bins, plan.tile,
-                                                      plan.tiles, sc.cnt, err);
+      static_cast<unsigned>(umin64(plan.tiles, static_cast<uint64_t>(num_sms()) * bucket_ctas()));
+  bucket_hist_kernel<0><<<grid, 256, plan.bins * 4, s>>>(in, count, b, plan.bins, plan.tile,
+                                                         plan.tiles, sc.cnt, err);
   bucket_scan_bins_kernel<<<plan.bins, 1024, 0, s>>>(sc.cnt, plan.tiles, sc.bin_total);
   bucket_scan_totals_kernel<<<1, 1024, 0, s>>>(sc.bin_total, plan.bins, block_off);
   if (launches) *launches += 3;
@@ -1439,31 +1487,52 @@ cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const uint32_t*
   BinCtx b{packed, nv, pbits, plan.n};
   const BucketScratch sc = scratch_parts(const_cast<void*>(scratch), plan);
   const unsigned grid =
-      static_cast<unsigned>(umin64(plan.tiles, static_cast<uint64_t>(num_sms()) * 4));
-  if (plan.tile == kFastTile && plan.bins <= 128) {
-    const size_t smem = static_cast<size_t>(plan.bins) * (8 + 8 * 4 + 4) + kFastTile * (8 + 2);
-    static size_t fast_set = 0;
-    if (smem > 48 * 1024 && smem > fast_set) {
-      cudaFuncSetAttribute(bucket_scatter_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem));
-      fast_set = smem;
-    }
-    bucket_scatter_fast_kernel<<<grid, 256, smem, s>>>(in, count, b, plan.bins, plan.tiles, sc.cnt,
-                                                       dst_off, outs, bins_per_out, err);
+      static_cast<unsigned>(umin64(plan.tiles, static_cast<uint64_t>(num_sms()) * bucket_ctas()));
+  auto fast = [&](auto kern, const uint2* src, uint32_t bins, uint64_t tiles, const uint32_t* cnt,
+                  const uint64_t* off, uint2* const* o, uint32_t per_out) {
+    const size_t smem = static_cast<size_t>(bins) * (8 + 8 * 4 + 4) + kFastTile * (8 + 2);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const unsigned g = static_cast<unsigned>(umin64(tiles, static_cast<uint64_t>(num_sms()) * bucket_ctas()));
+    kern<<<g, 256, smem, s>>>(src, count, b, bins, tiles, cnt, off, o, per_out, err);
     if (launches) *launches += 1;
+  };
+  if (plan.tile == kFastTile && plan.bins <= 128) {
+    fast(bucket_scatter_fast_kernel<0>, in, plan.bins, plan.tiles, sc.cnt, dst_off, outs,
+         bins_per_out);
     return cudaGetLastError();
   }
-  const size_t smem = static_cast<size_t>(plan.bins) * (8 + 8 * 4);
-  static size_t smem_set = 0;
-  if (smem > 48 * 1024 && smem > smem_set) {
-    cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    smem_set = smem;
+  if (plan.two_pass) {
+    // LSD radix over the grid: stable by column j into tmp (packed values),
+    // then stable by row i into the final slots — the same stable counting
+    // sort by bin = i n + j as the single pass, with n bins per pass
+    const TwoPassLayout L(plan, align256(base_scratch_bytes(plan)));
+    char* base = static_cast<char*>(const_cast<void*>(scratch));
+    uint2** tmp_out = reinterpret_cast<uint2**>(base + L.outs);
+    uint32_t* cnt2 = reinterpret_cast<uint32_t*>(base + L.cnt);
+    uint64_t* tot2 = reinterpret_cast<uint64_t*>(base + L.tot);
+    uint64_t* off2 = reinterpret_cast<uint64_t*>(base + L.off);
+    uint64_t* adj = reinterpret_cast<uint64_t*>(base + L.adj);
+    uint2* tmp = reinterpret_cast<uint2*>(base + L.tmp);
+    const uint32_t n = plan.n;
+    const unsigned g2 = static_cast<unsigned>(umin64(plan.tiles2, static_cast<uint64_t>(num_sms()) * bucket_ctas()));
+    cudaError_t e = cudaMemcpyAsync(tmp_out, &tmp, sizeof(uint2*), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    // pass 1: by column
+    bucket_hist_kernel<1><<<g2, 256, n * 4, s>>>(in, count, b, n, kFastTile, plan.tiles2, cnt2, err);
+    bucket_scan_bins_kernel<<<n, 1024, 0, s>>>(cnt2, plan.tiles2, tot2);
+    bucket_scan_totals_kernel<<<1, 1024, 0, s>>>(tot2, n, off2);
+    fast(bucket_scatter_fast_kernel<1>, in, n, plan.tiles2, cnt2, off2, tmp_out, n);
+    // pass 2: by row, slots adjusted per block (i, j)
+    bucket_hist_kernel<2><<<g2, 256, n * 4, s>>>(tmp, count, b, n, kFastTile, plan.tiles2, cnt2, err);
+    bucket_scan_bins_kernel<<<n, 1024, 0, s>>>(cnt2, plan.tiles2, tot2);
+    bucket_adjust_kernel<<<(n + 127) / 128, 128, 0, s>>>(dst_off, sc.bin_total, n, adj);
+    fast(bucket_scatter_fast_kernel<2>, tmp, n, plan.tiles2, cnt2, adj, outs, bins_per_out / n);
+    if (launches) *launches += 6;
+    (void)grid;
+    return cudaGetLastError();
   }
-  bucket_scatter_kernel<<<grid, 256, smem, s>>>(in, count, b, plan.bins, plan.tile, plan.tiles,
-                                                sc.cnt, dst_off, outs, bins_per_out, err);
-  if (launches) *launches += 1;
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;  // unreachable: every grid is single-pass (<= 128 bins) or two-pass
 }
 
 cudaError_t launch_bucket(const uint2* in, uint64_t count, const uint32_t* packed, uint32_t nv,

@@ -52,7 +52,9 @@ def test_partition_alias_init_bitexact(n):
 
 @pytest.mark.parametrize("n,vr,count", [(1, 1, 0), (1, 1, 1), (1, 1, 100_003), (2, 1, 77_777),
                                         (4, 1, 4096 * 3 + 5), (8, 1, 250_001), (5, 1, 31),
-                                        (4, 2, 100_001), (8, 4, 123_457), (8, 8, 64_000)])
+                                        (4, 2, 100_001), (8, 4, 123_457), (8, 8, 64_000),
+                                        (12, 1, 2048 * 7 + 3), (16, 4, 200_003), (24, 8, 99_999),
+                                        (16, 16, 40_000)])
 def test_bucketing_bitexact(n, vr, count):
     """a3-a6: blocks (after the block-row exchange for vr > 1) equal the
     oracle's stable counting sort, byte for byte, ragged tails included."""
@@ -89,9 +91,11 @@ def test_negative_stream_bitexact(n, vr):
         p.train_episode()  # advances the pool counter e
 
 
-def test_out_of_range_rejected_before_any_update():
+@pytest.mark.parametrize("n", [4, 16])
+def test_out_of_range_rejected_before_any_update(n):
+    """An id >= |V| fails the pool (single-pass and two-pass bucketing)."""
     src, dst = _graph()
-    p, _ = _pair(2000, src, dst, d=8, n=4)
+    p, _ = _pair(2000, src, dst, d=8, n=n)
     v0 = p.vertex()
     bad = synth.edge_pool(src, dst, 1000, seed=1)
     bad[500, 1] = 2000
@@ -156,7 +160,8 @@ def c1_graph():
 
 @pytest.mark.parametrize("n,vr,pools,count", [(1, 1, 1, C1["pool"]), (1, 1, 3, 200_000),
                                                (4, 1, 2, 400_000), (4, 2, 2, 400_000),
-                                               (8, 8, 2, 400_000), (8, 4, 1, 400_000)])
+                                               (8, 8, 2, 400_000), (8, 4, 1, 400_000),
+                                               (16, 1, 1, 400_000), (16, 4, 1, 400_000)])
 def test_ordered_mode_matches_oracle(c1_graph, n, vr, pools, count):
     """Ordered verification mode (one warp per block, block order) after
     whole pools of C1 (BASELINE configs[0]): <= 1e-5 relative Frobenius per
@@ -406,10 +411,11 @@ def test_call_order_and_argument_errors():
     h.close()
 
 
-@pytest.mark.parametrize("n,count", [(37, 300_001), (64, 500_000)])
+@pytest.mark.parametrize("n,count", [(37, 300_001), (64, 500_000), (64, 2048), (13, 1)])
 def test_bucketing_many_partitions(n, count):
-    """Maximum grid (n = 64: 4096 bins, 160 KB of scatter smem) and a
-    non-power-of-two n (6 partition bits), bit-exact."""
+    """Maximum grid (n = 64: 4096 bins) and non-power-of-two n (6 / 4
+    partition bits), through the two-pass placement (by column, then by row),
+    bit-exact; one-tile and one-sample pools."""
     src, dst = synth.chung_lu(20_000, 100_000, gamma=2.1, wmax=500.0, seed=4)
     p, o = _pair(20_000, src, dst, d=4, n=n)
     pool = synth.edge_pool(src, dst, count, seed=5)
