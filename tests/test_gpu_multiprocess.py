@@ -60,7 +60,7 @@ def _rel(a, b):
     return np.linalg.norm(a.astype(np.float64) - b) / np.linalg.norm(b.astype(np.float64))
 
 
-@pytest.mark.parametrize("world,n", [(2, 2), (2, 4), (4, 4)])
+@pytest.mark.parametrize("world,n", [(2, 2), (2, 4), (4, 4), (2, 16)])
 def test_processes_ordered_match_oracle(tmp_path, world, n):
     pools, count = 2, 200_001
     V, C, loss = _run(tmp_path, world, n, pools, count, ordered=1)
@@ -101,12 +101,17 @@ def test_processes_device_augmentation_match_oracle(tmp_path):
     assert _rel(V, o.get("vertex")) <= 1e-5 and _rel(C, o.get("context")) <= 1e-5
 
 
-def test_processes_hogwild_runs(tmp_path):
+@pytest.mark.parametrize("n", [2, 8])
+def test_processes_hogwild_runs(tmp_path, monkeypatch, n):
     """Hogwild over 2 processes on a 10^5-node graph (enough rows for the
-    ~10^4 concurrent samples): finite, learning, loss close to the oracle's."""
+    ~10^4 concurrent samples): finite, learning, loss close to the oracle's.
+    n = 8: 4 partitions per rank (rotation behind 3 blocks) with hot-row
+    combining forced on (GV_COMB_ROWS, inherited by the workers)."""
+    if n == 8:
+        monkeypatch.setenv("GV_COMB_ROWS", "16")
     pools, count, nv, ne = 3, 2_000_000, 100_000, 500_000
-    V, C, loss = _run(tmp_path, 2, 2, pools, count, ordered=0, nv=nv, ne=ne)
-    Vo, Co, lo = _oracle(2, pools, count, nv=nv, ne=ne)
+    V, C, loss = _run(tmp_path, 2, n, pools, count, ordered=0, nv=nv, ne=ne)
+    Vo, Co, lo = _oracle(n, pools, count, nv=nv, ne=ne)
     assert np.isfinite(V).all() and np.isfinite(C).all() and np.isfinite(loss).all()
     # the unweighted monitoring loss need not fall this early (the objective
     # weighs negatives by 5); it must track the serial oracle's, pool by pool
