@@ -1489,8 +1489,8 @@ cudaError_t launch_init_vertex(float* vertex, uint32_t stride, uint32_t dim, uin
   return cudaGetLastError();
 }
 
-// resident CTAs per SM of the bucketing kernels (GV_BUCKET_CTAS, default 8):
-// their tiles are short and barrier-bound, so more CTAs per SM hide the syncs
+// CTAs per SM of the bucketing grids (GV_BUCKET_CTAS, default 8; 4, 8 and 16
+// measured equal at n = 4 and n = 32, profiles/README.md)
 static uint64_t bucket_ctas() {
   static uint64_t v = 0;
   if (v == 0) {
