@@ -586,6 +586,7 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
   float loss = 0.f;
   if (sq.L == 0) return loss;
   uint32_t comb_dirty = 0;  // warp-uniform: private copies holding deltas
+  uint32_t comb_left = cb.flush;  // iterations to the next hand-over
   const uint32_t iters = (sq.L + G - 1) / G;  // iteration i: group h runs sample G i + h
   uint32_t cu, cc[K + 1], nu, nc[K + 1];      // ids of the current / next 32-sample chunk
   uint32_t ch_hot, nh_hot;
@@ -775,7 +776,10 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
           if ((hot >> (1 + t)) & 1u) mine |= 1u << (cb.rows + c[t] - cb.c0);
       }
       comb_dirty |= __reduce_or_sync(kFull, mine);
-      if ((i % cb.flush) == cb.flush - 1) comb_flush(cb, comb_dirty, vertex, context, stride, dim4, lane);
+      if (--comb_left == 0) {
+        comb_flush(cb, comb_dirty, vertex, context, stride, dim4, lane);
+        comb_left = cb.flush;
+      }
     }
     if (i + P < iters) issue(i + P, st_in, chunk);
     if (!kRingTma) cp_commit();
