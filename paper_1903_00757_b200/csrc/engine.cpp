@@ -173,7 +173,7 @@ struct gv_ctx {
   // gv_load_edges when a partition's hottest row carries >= 0.6% of the
   // partition's degree mass — then the row's atomics queue in L2 (C2 at n = 4
   // / 8: 1.2% / 2.4%, 2.38e9 -> 2.81e9 / 2.14e9 -> 2.77e9 samples/s); below
-  // it only costs (C2 at n = 1, 0.3%: 2.79e9 -> 2.45e9; C4 at n = 32: -17%).
+  // it only costs (C2 at n = 1, 0.3%: 2.79e9 -> 2.45e9; C4 at n = 32: 2.60e9 -> 2.25e9).
   // GV_COMB_ROWS (0 = off) / GV_COMB_FLUSH (iterations between hand-overs)
   // override.
   uint32_t comb_rows = 0, comb_flush = 256;
