@@ -309,7 +309,6 @@ def run_ours(args):
         launches += st["kernel_launches"]
         samples += st["samples_global"]
         tot_ms.append(st["ms_total"])
-        comb_rows = st["comb_rows"]
     ev1.record(stream)
     barrier()
     clk = clocks.stop()
@@ -410,8 +409,7 @@ def run_ours(args):
                                   "lr0": CFG["lr"], "neg_weight": CFG["neg_weight"],
                                   "seed": CFG["seed"], "lr_schedule": "linear, floor 1e-4"},
                        "host_partitions": bool(args.host_partitions),
-                       "mode": "ordered" if args.ordered else "hogwild",
-                       "hot_row_combining": comb_rows},
+                       "mode": "ordered" if args.ordered else "hogwild"},
             "roofline": roof, "cpu_baseline": cpu, "cpu_hogwild": cpu_hog, "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk, "pipeline": pipeline,

@@ -127,8 +127,6 @@ typedef struct {
   double ms_total;        /* first bucketing launch -> last kernel/transfer       */
   uint32_t sgd_launches;  /* number of block-SGD kernel launches                  */
   uint32_t kernel_launches; /* all kernels launched by this call                  */
-  uint32_t comb_rows;     /* hot rows per matrix whose deltas the ring kernel
-                             combines per warp (0 = off)            */
 } gv_episode_stats;
 
 /* ---------------------------------------------------------------------- */

@@ -119,7 +119,6 @@ struct Rank {
   DevBuf<uint64_t> counts;      // [0, bins]: block_off; [bins+1]: error flag
   DevBuf<uint64_t> all_counts;  // NCCL: gathered counts of every rank
   DevBuf<gv::BlockDesc> desc;
-  DevBuf<float> comb;  // private hot-row copies of the ring kernel's warps (zeroed)
   DevBuf<gv::CopySeg> segs;
   DevBuf<uint64_t> place_args;  // fused exchange: dst_off[bins] | outs[D] (device pointers)
   gv::BucketPlan plan{};
@@ -169,15 +168,6 @@ struct gv_ctx {
   int threads = 1;
   int sms = 148;
   uint32_t hot_rows = 0;  // L2 retention: local ids below this are evict_last
-  // ring kernel hot-row delta combining (SgdArgs::comb_*): switched on by
-  // gv_load_edges when a partition's hottest row carries >= 0.6% of the
-  // partition's degree mass — then the row's atomics queue in L2 (C2 at n = 4
-  // / 8: 1.2% / 2.4%, 2.38e9 -> 2.81e9 / 2.14e9 -> 2.77e9 samples/s); below
-  // it only costs (C2 at n = 1, 0.3%: 2.79e9 -> 2.45e9; C4 at n = 32: 2.60e9 -> 2.25e9).
-  // GV_COMB_ROWS (0 = off) / GV_COMB_FLUSH (iterations between hand-overs)
-  // override.
-  uint32_t comb_rows = 0, comb_flush = 256;
-  bool comb_env = false;
   std::string err;
   std::mutex err_mu;  // push may fail on a producer thread while the trainer runs
   bool loaded = false;
@@ -702,10 +692,6 @@ gv_status run_steps(gv_ctx* c) {
         }
       }
   }
-  // one launch per offset step over its m blocks (one rank, resident), or one
-  // per block: several ranks (rotation), out-of-core, or hot-row combining
-  // (its shared-memory slots belong to one block's partitions)
-  const bool step_launch = c->D == 1 && !c->hp() && (c->comb_rows == 0 || c->opt.ordered || m == 1);
   std::vector<int> hp_pos;  // position of block (t, i) in hp_order
   if (c->hp()) {
     hp_pos.resize(hp_order.size());
@@ -726,7 +712,7 @@ gv_status run_steps(gv_ctx* c) {
         gv::BlockDesc& d = desc[t * m + g];
         d.sample_off = r.final_off[g * n + j];
         d.count_lo = static_cast<uint32_t>(r.final_off[g * n + j + 1] - r.final_off[g * n + j]);
-        d.prefix = step_launch ? prefix : 0;
+        d.prefix = (c->D == 1 && !c->hp()) ? prefix : 0;
         prefix += d.count_lo;
         d.vrow0 = static_cast<uint32_t>(c->part.off[i] - r.vrow_first);
         d.crow0 = static_cast<uint32_t>(c->D == 1 ? c->part.off[j]
@@ -752,7 +738,7 @@ gv_status run_steps(gv_ctx* c) {
                        cudaMemcpyHostToDevice, r.compute));
     // (pageable source: the copy is staged before cudaMemcpyAsync returns)
     if (c->opt.compute_loss) CK(cudaMemsetAsync(r.loss.p, 0, sizeof(double), r.compute));
-    const size_t need = static_cast<size_t>(2) * (step_launch ? n : n * m);
+    const size_t need = static_cast<size_t>(2) * (c->D == 1 && !c->hp() ? n : n * m);
     while (r.ev_sgd.size() < need) r.ev_sgd.push_back(new_event(true));
   }
   // enqueue the steps
@@ -770,18 +756,6 @@ gv_status run_steps(gv_ctx* c) {
     a.key1 = key1;
     a.loss_acc = c->opt.compute_loss ? r.loss.p : nullptr;
     a.hot_rows = c->hot_rows;
-    a.comb_rows = (c->opt.ordered || c->dim > 128) ? 0 : c->comb_rows;  // ring kernel only
-    a.comb_flush = c->comb_flush;
-    if (a.comb_rows != 0) {
-      // copies for up to 16 warps per SM (the ring kernel keeps 8 resident)
-      a.comb_warps = static_cast<uint32_t>(c->sms > 0 ? c->sms : 148) * 16;
-      const size_t need = static_cast<size_t>(a.comb_warps) * 2 * a.comb_rows * 128;
-      if (r.comb.cap < need) {
-        CK(r.comb.ensure(need));
-        CK(cudaMemsetAsync(r.comb.p, 0, need * sizeof(float), r.compute));
-      }
-      a.comb_buf = r.comb.p;
-    }
     gv_step_plan plan;
     gv_plan_step(n, c->D, r.d, t, &plan);
     a.desc = r.desc.p + t * m + g0;
@@ -851,14 +825,9 @@ gv_status run_steps(gv_ctx* c) {
       gv_step_plan plan;
       gv_plan_step(n, c->D, r.d, t, &plan);
       auto launch = [&](uint32_t g0, uint32_t cnt_blk) { return launch_blocks(r, t, g0, cnt_blk); };
-      if (step_launch) {
+      if (c->D == 1) {
         gv_status st = launch(0, m);
         if (st) return st;
-        continue;
-      }
-      if (c->D == 1) {
-        for (uint32_t g = 0; g < m; ++g)
-          if (gv_status st = launch(g, 1)) return st;
         continue;
       }
       for (uint32_t g = 0; g < m; ++g) {
@@ -984,7 +953,6 @@ gv_status collect_stats(gv_ctx* c, gv_episode_stats* out) {
   out->pool_index = c->pool_index - 1;
   out->samples_global = c->pool_P_global;
   out->n_steps = c->n;
-  out->comb_rows = (c->opt.ordered || c->dim > 128) ? 0 : c->comb_rows;
   uint64_t before = c->samples_done - c->pool_P_global;
   out->lr_first = lr_at(c, before);
   uint64_t s = before;
@@ -1253,12 +1221,6 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
   // red.global.add write-back (DRAM reads +29%, -19% samples/s; profiles/).
   // GV_HOT_ROWS=<local-id threshold> enables them for experiments.
   if (const char* e = getenv("GV_HOT_ROWS")) c->hot_rows = static_cast<uint32_t>(atol(e));
-  if (const char* e = getenv("GV_COMB_ROWS")) {
-    c->comb_rows = static_cast<uint32_t>(atol(e));
-    c->comb_env = true;
-  }
-  if (const char* e = getenv("GV_COMB_FLUSH")) c->comb_flush = std::max<uint32_t>(1, static_cast<uint32_t>(atol(e)));
-  c->comb_rows = std::min<uint32_t>(c->comb_rows, 16);  // 2 x rows slots in a 32-bit mask
   c->ranks.resize(c->local);
   for (int v = 0; v < c->local; ++v) c->ranks[v].d = (o.world_size > 1) ? o.rank : v;
   *out = c;
@@ -1328,15 +1290,6 @@ gv_status gv_load_edges(gv_ctx* c, const uint32_t* src, const uint32_t* dst, con
     rc = gv::build_alias(w.data() + b, static_cast<uint32_t>(psize(c, p)), c->nprob.data() + b,
                          c->nalias.data() + b);
     if (rc) return fail(c, GV_ERR_EMPTY, "context partition " + std::to_string(p) + " has zero noise mass");
-  }
-  if (!c->comb_env) {  // hot-row combining where a partition's top row is hot (see gv_ctx)
-    double top = 0.0;
-    for (uint32_t p = 0; p < c->n; ++p) {
-      double mass = 0.0;
-      for (uint64_t k = c->part.off[p]; k < c->part.off[p + 1]; ++k) mass += c->graph.deg[c->part.inv_perm[k]];
-      if (mass > 0.0) top = std::max(top, c->graph.deg[c->part.inv_perm[c->part.off[p]]] / mass);
-    }
-    c->comb_rows = top >= 0.006 ? 16 : 0;
   }
   rc = gv::build_walk_tables(c->graph, c->threads, &c->walks);
   if (rc) return fail(c, static_cast<gv_status>(rc), "departure table has zero mass");
@@ -1773,7 +1726,7 @@ void gv_destroy(gv_ctx* c) {
     cudaFree(r.vertex);
     cudaFree(r.context);
     r.local_blocks.release(); r.recv.release(); r.blocks.release(); r.scratch.release();
-    r.counts.release(); r.all_counts.release(); r.desc.release(); r.comb.release(); r.segs.release(); r.loss.release();
+    r.counts.release(); r.all_counts.release(); r.desc.release(); r.segs.release(); r.loss.release();
     if (r.counts_host) cudaFreeHost(r.counts_host);
     for (cudaEvent_t e : {r.ev_start, r.ev_bucket, r.ev_exch, r.ev_end, r.ev_recv_consumed,
                           r.ev_exch_sent, r.ev_last_recv})

@@ -273,9 +273,6 @@ __device__ __forceinline__ void sample_ids(const SgdArgs& a, uint64_t qg, uint32
     if (__ldg(&a.desc[mid].prefix) <= qg) lo = mid; else hi = mid - 1;
   }
   const BlockDesc* d = a.desc + lo;
-  // hot bits: L2 hints (hot_rows), or rows combined in shared memory
-  // (comb_rows; only rows of the launch's first block have slots)
-  const uint32_t lim = a.comb_rows ? (lo == 0 ? a.comb_rows : 0u) : a.hot_rows;
   const uint32_t q = static_cast<uint32_t>(qg - __ldg(&d->prefix));
   const uint2 smp = __ldcs(a.samples + __ldg(&d->sample_off) + q);
   const uint32_t crow0 = __ldg(&d->crow0), m = __ldg(&d->m), alias0 = __ldg(&d->alias0);
@@ -290,9 +287,9 @@ __device__ __forceinline__ void sample_ids(const SgdArgs& a, uint64_t qg, uint32
     const uint2 pa = __ldg(a.alias + alias0 + slot);
     const uint32_t nl = alias_pick(pa.x, pa.y, slot, r.z);
     my_c[1 + k] = crow0 + nl;
-    if (my_hot) *my_hot |= (nl < lim ? 1u : 0u) << (2 + k);
+    if (my_hot) *my_hot |= (nl < a.hot_rows ? 1u : 0u) << (2 + k);
   }
-  if (my_hot) *my_hot |= (smp.x < lim ? 1u : 0u) | ((smp.y < lim ? 1u : 0u) << 1);
+  if (my_hot) *my_hot |= (smp.x < a.hot_rows ? 1u : 0u) | ((smp.y < a.hot_rows ? 1u : 0u) << 1);
 }
 
 // ------------------------------------------------------------------------
@@ -514,59 +511,12 @@ __device__ __forceinline__ void red_rowg(float* base, uint32_t row, uint32_t str
   }
 }
 
-// Per-warp combining of hot-row deltas (SgdArgs::comb_rows). Under the n x n
-// grid a block's rows are 1/n of a matrix while the sample rate stays the
-// GPU's, so the hottest rows of a partition take n times more updates per
-// second than at n = 1 and their red.global.add operations queue at their L2
-// lines (measured: at n = 8 on C2, dropping the deltas of the 8 hottest rows
-// per partition raises the kernel from 2.2e9 to 3.0e9 samples/s). Here each
-// warp adds the deltas of the comb_rows hottest rows of each matrix into its
-// own private copy of those rows (an L2-resident scratch line that no other
-// warp touches, so nothing queues) and every comb_flush iterations moves the
-// dirty copies into the real rows, one red per row. No delta is lost; a hot
-// row's updates reach other warps up to comb_flush iterations later — the
-// bounded staleness of asynchronous SGD, like the ring's own.
-struct CombCtx {
-  float* priv;       // this warp's [2][rows][128] floats: vertex rows, then context rows
-  uint32_t rows, flush;
-  uint32_t v0, c0;   // first rows of the launch's block
-};
-
-__device__ __forceinline__ void comb_flush(const CombCtx& cb, uint32_t& dirty, float* vertex,
-                                           float* context, uint32_t stride, int dim4, int lane) {
-  __syncwarp();  // every lane's reds into the copies are ordered before the reads below
-  constexpr int B = 8;  // copies read back to back, so one L2 round trip covers B rows
-  while (dirty != 0u) {
-    uint32_t sl[B];
-    float4 v[B];
-#pragma unroll
-    for (int k = 0; k < B; ++k) {
-      sl[k] = dirty != 0u ? static_cast<uint32_t>(__ffs(dirty) - 1) : 0xFFFFFFFFu;
-      dirty &= dirty - 1;
-      if (sl[k] != 0xFFFFFFFFu && lane < dim4)
-        v[k] = __ldcg(reinterpret_cast<const float4*>(cb.priv + sl[k] * 128) + lane);
-    }
-#pragma unroll
-    for (int k = 0; k < B; ++k) {
-      if (sl[k] == 0xFFFFFFFFu || lane >= dim4) continue;
-      __stcg(reinterpret_cast<float4*>(cb.priv + sl[k] * 128) + lane, make_float4(0.f, 0.f, 0.f, 0.f));
-      const bool ctx = sl[k] >= cb.rows;
-      const uint32_t row = ctx ? cb.c0 + (sl[k] - cb.rows) : cb.v0 + sl[k];
-      float* g = (ctx ? context : vertex) + static_cast<uint64_t>(row) * stride + 4 * lane;
-      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(g), "f"(v[k].x),
-                   "f"(v[k].y), "f"(v[k].z), "f"(v[k].w)
-                   : "memory");
-    }
-  }
-  __syncwarp();  // the zeroed copies are ordered before later reds into them
-}
-
 // The Hogwild ring pipeline with LPS lanes per sample: group g of the warp
 // processes samples g, g+G, g+2G, ... of the warp's sequence; lane gl of a
 // group owns float4 columns gl, gl+LPS, ... of every row.
 template <int K, int LPS>
 __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, float4* ring,
-                                          int dim4, int lane, bool want_loss, const CombCtx& cb) {
+                                          int dim4, int lane, bool want_loss) {
   using RC = RingCfg<K, LPS>;
   constexpr int P = kRingP, R = RC::R, T = RC::T, G = RC::G, CPL = 32 / LPS;
   constexpr int ITER_PER_CHUNK = 32 / G;
@@ -585,8 +535,6 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
   const uint32_t stride = a.stride;
   float loss = 0.f;
   if (sq.L == 0) return loss;
-  uint32_t comb_dirty = 0;  // warp-uniform: private copies holding deltas
-  uint32_t comb_left = cb.flush;  // iterations to the next hand-over
   const uint32_t iters = (sq.L + G - 1) / G;  // iteration i: group h runs sample G i + h
   uint32_t cu, cc[K + 1], nu, nc[K + 1];      // ids of the current / next 32-sample chunk
   uint32_t ch_hot, nh_hot;
@@ -595,11 +543,11 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
 #if GV_SKIP_HOT_EXPERIMENT
   // measurement-only build: the deltas of rows with local id < hot_rows are
   // dropped (wrong training) to measure what hot-row write contention costs
+  // (profiles/r01_hot_row_combining.json)
   const uint64_t pol_hot = policy_evict_normal(), pol_cold = pol_hot;
 #else
-  const bool hints = a.hot_rows != 0 && cb.rows == 0;
-  const uint64_t pol_hot = hints ? policy_evict_last() : policy_evict_normal();
-  const uint64_t pol_cold = hints ? policy_evict_first() : policy_evict_normal();
+  const uint64_t pol_hot = a.hot_rows ? policy_evict_last() : policy_evict_normal();
+  const uint64_t pol_cold = a.hot_rows ? policy_evict_first() : policy_evict_normal();
 #endif
   auto ids_of = [&](uint32_t j, uint32_t cur_chunk, uint32_t& u, uint32_t* c, uint32_t& hot) {
     const uint32_t pp = G * j + h;
@@ -683,18 +631,6 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
 #if GV_SKIP_HOT_EXPERIMENT
       if ((hot >> r) & 1u) return;
 #endif
-      if (!kRingTmaRed && cb.rows != 0 && ((hot >> r) & 1u)) {  // into the warp's private copy
-        const uint32_t sl = (r == 0 ? row - cb.v0 : cb.rows + (row - cb.c0));
-        float* pc = cb.priv + sl * 128;
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-          const int col = gl + LPS * q;
-          if (act && col < dim4)
-            red_add4_hint(pc + 4 * col,
-                          make_float4(g * x.v[q].x, g * x.v[q].y, g * x.v[q].z, g * x.v[q].w), pol);
-        }
-        return;
-      }
       if (kRingTmaRed) {
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
@@ -765,22 +701,6 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
       }
       __syncwarp();
     }
-    if (cb.rows != 0) {
-      // slots this iteration's samples used (rows with a hot bit), then the
-      // periodic hand-over to the real rows
-      uint32_t mine = 0;
-      if (act) {
-        if (hot & 1u) mine |= 1u << (u - cb.v0);
-#pragma unroll
-        for (int t = 0; t <= K; ++t)
-          if ((hot >> (1 + t)) & 1u) mine |= 1u << (cb.rows + c[t] - cb.c0);
-      }
-      comb_dirty |= __reduce_or_sync(kFull, mine);
-      if (--comb_left == 0) {
-        comb_flush(cb, comb_dirty, vertex, context, stride, dim4, lane);
-        comb_left = cb.flush;
-      }
-    }
     if (i + P < iters) issue(i + P, st_in, chunk);
     if (!kRingTma) cp_commit();
     st = (st + 1 == R) ? 0 : st + 1;
@@ -795,7 +715,6 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
   }
   if (!kRingTma) cp_wait<0>();
   if (kRingTmaRed && gl == 0) bulk_wait_all();
-  if (cb.rows != 0) comb_flush(cb, comb_dirty, vertex, context, stride, dim4, lane);
   return loss;
 }
 
@@ -814,15 +733,7 @@ __global__ void __launch_bounds__(256) sgd_ring_kernel(const SgdArgs a, int dim4
     sq.L = static_cast<uint32_t>(L);
   }
   float4* ring = smem_f4 + (threadIdx.x >> 5) * RingCfg<K, kRingLPS>::WARP_ALL;
-  CombCtx cb{};
-  if (a.comb_rows != 0) {
-    cb.priv = a.comb_buf + warp * (2 * a.comb_rows * 128);
-    cb.rows = a.comb_rows;
-    cb.flush = a.comb_flush;
-    cb.v0 = a.desc[0].vrow0;
-    cb.c0 = a.desc[0].crow0;
-  }
-  const float loss = run_ring<K, kRingLPS>(a, sq, ring, dim4, lane, a.loss_acc != nullptr, cb);
+  const float loss = run_ring<K, kRingLPS>(a, sq, ring, dim4, lane, a.loss_acc != nullptr);
   if (a.loss_acc != nullptr && (lane % kRingLPS) == 0)
     atomicAdd(a.loss_acc, static_cast<double>(loss));
 }
@@ -1435,10 +1346,8 @@ cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaSt
     const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / wb)));
     const size_t smem = wb * warps;
     static int occr[8] = {};
-    static size_t occ_smem[8] = {};
     int& o = occr[ki];
-    if (o == 0 || occ_smem[ki] != smem) {
-      occ_smem[ki] = smem;
+    if (o == 0) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, 32 * warps, smem) != cudaSuccess || o <= 0)
         o = 1;
@@ -1446,7 +1355,6 @@ cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaSt
     const uint64_t chunks = (a.total + 31) / 32;
     uint64_t grid = static_cast<uint64_t>(sms > 0 ? sms : num_sms()) * o;
     grid = std::min<uint64_t>(grid, (chunks + warps - 1) / warps);
-    if (a.comb_rows != 0) grid = std::min<uint64_t>(grid, a.comb_warps / warps);  // a copy per warp
     f<<<static_cast<unsigned>(grid), 32 * warps, smem, s>>>(a, dim / 4);
     return cudaGetLastError();
   }

@@ -33,12 +33,6 @@ struct SgdArgs {
   double* loss_acc;       // nullable
   uint32_t hot_rows;      // local ids < hot_rows are L2 evict_last, others evict_first
                           // (0 = no cache hints)
-  uint32_t comb_rows;     // ring kernel: deltas of the comb_rows (<= 16) hottest rows of
-                          // the launch's block (local id < comb_rows, both matrices) are
-                          // combined per warp in private copies (0 = off)
-  uint32_t comb_flush;    // ... moved into the rows every comb_flush iterations of a warp
-  float* comb_buf;        // zeroed [comb_warps][2][comb_rows][128] floats
-  uint32_t comb_warps;    // warps comb_buf has copies for (caps the grid)
 };
 
 struct ExplicitArgs {

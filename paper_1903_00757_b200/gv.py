@@ -48,8 +48,7 @@ class gv_episode_stats(C.Structure):
                 ("n_steps", C.c_uint32), ("lr_first", C.c_float), ("lr_last", C.c_float),
                 ("loss_sum", C.c_double), ("ms_bucket", C.c_double), ("ms_exchange", C.c_double),
                 ("ms_sgd", C.c_double), ("ms_rotate", C.c_double), ("ms_total", C.c_double),
-                ("sgd_launches", C.c_uint32), ("kernel_launches", C.c_uint32),
-                ("comb_rows", C.c_uint32)]
+                ("sgd_launches", C.c_uint32), ("kernel_launches", C.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

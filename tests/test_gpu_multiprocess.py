@@ -102,13 +102,10 @@ def test_processes_device_augmentation_match_oracle(tmp_path):
 
 
 @pytest.mark.parametrize("n", [2, 8])
-def test_processes_hogwild_runs(tmp_path, monkeypatch, n):
+def test_processes_hogwild_runs(tmp_path, n):
     """Hogwild over 2 processes on a 10^5-node graph (enough rows for the
     ~10^4 concurrent samples): finite, learning, loss close to the oracle's.
-    n = 8: 4 partitions per rank (rotation behind 3 blocks) with hot-row
-    combining forced on (GV_COMB_ROWS, inherited by the workers)."""
-    if n == 8:
-        monkeypatch.setenv("GV_COMB_ROWS", "16")
+    n = 8: 4 partitions per rank (rotation behind 3 blocks)."""
     pools, count, nv, ne = 3, 2_000_000, 100_000, 500_000
     V, C, loss = _run(tmp_path, 2, n, pools, count, ordered=0, nv=nv, ne=ne)
     Vo, Co, lo = _oracle(n, pools, count, nv=nv, ne=ne)

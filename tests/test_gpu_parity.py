@@ -269,64 +269,6 @@ def test_hogwild_auc_matches_oracle():
     assert min(v[0] for v in f1_o.values()) > 0.5  # far above chance (1/50)
 
 
-def test_hot_row_combining_switch(monkeypatch):
-    """Combining switches on when a partition's hottest row holds >= 0.6% of
-    its degree mass (a hub), stays off on a flat graph, and GV_COMB_ROWS
-    overrides; ordered mode never combines."""
-    rng = np.random.default_rng(3)
-    nv = 4000
-    ring_s = np.arange(nv, dtype=np.uint32)
-    ring_d = ((ring_s + 1) % nv).astype(np.uint32)
-    hub_s = np.zeros(2000, dtype=np.uint32)
-    hub_d = rng.integers(1, nv, 2000).astype(np.uint32)
-    cases = [((ring_s, ring_d), None, 0, 0), ((np.r_[ring_s, hub_s], np.r_[ring_d, hub_d]), None, 0, 16),
-             ((np.r_[ring_s, hub_s], np.r_[ring_d, hub_d]), "0", 0, 0), ((ring_s, ring_d), "8", 0, 8),
-             ((np.r_[ring_s, hub_s], np.r_[ring_d, hub_d]), None, 1, 0)]
-    for (src, dst), env, ordered, want in cases:
-        if env is None:
-            monkeypatch.delenv("GV_COMB_ROWS", raising=False)
-        else:
-            monkeypatch.setenv("GV_COMB_ROWS", env)
-        p = G.GraphVite(nv, 32, 4, 1, 0.025, ordered=ordered)
-        p.load_edges(src, dst)
-        p.push(synth.edge_pool(src, dst, 50_000, seed=1))
-        assert p.train_episode()["comb_rows"] == want, (env, ordered, want)
-        p.close()
-
-
-def test_hot_row_combining_quality(monkeypatch):
-    """Hot-row delta combining of the ring kernel (the default for n >= 4;
-    set explicitly here): the 16 hottest rows per partition take their
-    updates through per-warp copies handed over every 256 iterations —
-    here, with ~33 iterations per warp and block, once per block, the
-    stalest setting. Link-prediction AUC within 0.01 and Micro/Macro-F1
-    within 0.02 of the oracle on the same n = 8 schedule (the north-star
-    Hogwild bar), on the DC-SBM graph of test_hogwild_auc_matches_oracle."""
-    monkeypatch.setenv("GV_COMB_ROWS", "16")
-    monkeypatch.setenv("GV_COMB_FLUSH", "256")
-    nv, ne, n = 100_000, 1_000_000, 8
-    src, dst, comm = synth.dcsbm(nv, ne, gamma=2.1, wmax=1000.0, c=50, mu=0.1, seed=1)
-    tr_s, tr_d, pos, neg = synth.linkpred_split(src, dst, nv, holdout=0.01, seed=6)
-    pools, count = 4, 10_000_000
-    p = G.GraphVite(nv, 128, n, 1, 0.025, total_samples=pools * count, ordered=0)
-    p.load_edges(tr_s, tr_d)
-    o = O.Trainer(nv, 128, n, K=1, lr0=0.025, lr_kind=1, total_samples=pools * count)
-    o.load_edges(tr_s, tr_d)
-    for k in range(pools):
-        pool = synth.edge_pool(tr_s, tr_d, count, seed=200 + k)
-        p.push(pool)
-        p.train_episode(stats=False)
-        o.train_pool(pool)
-    V, Vo = p.vertex(), o.get("vertex")
-    assert np.isfinite(V).all() and np.isfinite(p.context()).all()
-    auc, auc_o = O.linkpred_auc(V, pos, neg), O.linkpred_auc(Vo, pos, neg)
-    f1, f1_o = _micro_f1(V, comm), _micro_f1(Vo, comm)
-    print("combining n=8: AUC gpu", auc, "oracle", auc_o, "F1 gpu", f1, "oracle", f1_o)
-    assert auc_o >= 0.8 and abs(auc - auc_o) <= 0.01, (auc, auc_o)
-    assert abs(f1[0] - f1_o[0]) <= 0.02 and abs(f1[1] - f1_o[1]) <= 0.02, (f1, f1_o)
-    p.close()
-
-
 @pytest.mark.parametrize("segments,s,count,L", [(1, 1, 1000, 40), (7, 2, 100_003, 40),
                                                 (1184, 5, 2_000_000, 40), (64, 3, 50_000, 10),
                                                 (3, 5, 17, 5)])

@@ -12,10 +12,7 @@ from paper_1903_00757_b200 import gv as G  # noqa: E402
 
 src, dst = synth.chung_lu(3000, 15_000, gamma=2.1, wmax=300.0, seed=1)
 pool = synth.edge_pool(src, dst, 50_003, seed=3)
-# (16, 4, 0): two-pass bucketing into the virtual ranks' buffers; hot-row
-# combining is forced on for every Hogwild case below
-os.environ["GV_COMB_ROWS"] = "16"
-os.environ["GV_COMB_FLUSH"] = "4"
+# (16, 4, 0): two-pass bucketing into the virtual ranks' buffers
 for n, vr, ordered in [(1, 1, 0), (4, 1, 0), (4, 2, 0), (4, 2, 1), (2, 1, 1), (16, 4, 0), (16, 1, 1)]:
     g = G.GraphVite(3000, 128, n, 1, 0.025, total_samples=200_000, virtual_ranks=vr,
                     ordered=ordered)
@@ -28,7 +25,6 @@ for n, vr, ordered in [(1, 1, 0), (4, 1, 0), (4, 2, 0), (4, 2, 1), (2, 1, 1), (1
     g.train_episode()
     assert np.isfinite(g.vertex()).all()
     g.close()
-del os.environ["GV_COMB_ROWS"], os.environ["GV_COMB_FLUSH"]
 for n in (3, 5):  # out-of-core: three slots, load / write-back streams, paired-step order
     g = G.GraphVite(3000, 128, n, 1, 0.025, host_partitions=1)
     g.load_edges(src, dst)
