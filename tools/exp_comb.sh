@@ -1,3 +1,5 @@
+# HISTORICAL: drives a hot-row combining / replica build that was withdrawn;
+# its GV_COMB_* / GV_REP_* variables do nothing in the current library. Results: profiles/r01_hot_row_combining.json
 # hot-row delta combining (on by default for n >= 4): GPU tests, then speed on C2 (n = 4, 8) and C4 (n = 32)
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/comb_tests.log 2>&1; echo "rc=$?" >> gpurun_out/comb_tests.log
 for cfg in "0 32 8" "16 16 8" "16 32 8" "16 64 8" "0 32 4" "16 32 4" "8 32 8"; do

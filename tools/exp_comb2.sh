@@ -1,3 +1,5 @@
+# HISTORICAL: drives a hot-row combining / replica build that was withdrawn;
+# its GV_COMB_* / GV_REP_* variables do nothing in the current library. Results: profiles/r01_hot_row_combining.json
 # combining: fixed flush iterations (GV_COMB_ITERS) vs per-launch count, C2 n = 8, repeated
 for rep in 1 2; do
 for cfg in "0 0" "16 256" "16 165" "16 64" "16 1024"; do  # GV_COMB_ITERS was a temporary A/B knob, now GV_COMB_FLUSH

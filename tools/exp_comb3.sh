@@ -1,3 +1,5 @@
+# HISTORICAL: drives a hot-row combining / replica build that was withdrawn;
+# its GV_COMB_* / GV_REP_* variables do nothing in the current library. Results: profiles/r01_hot_row_combining.json
 # combining option: quality test (n = 8, stalest setting), ring math on disjoint rows with it on, and n = 1 / 8 speed
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -s -k "hot_row_combining" > gpurun_out/comb3_quality.log 2>&1; echo "rc=$?" >> gpurun_out/comb3_quality.log
 GV_COMB_ROWS=16 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "disjoint_rows or degenerate" > gpurun_out/comb3_tests.log 2>&1; echo "rc=$?" >> gpurun_out/comb3_tests.log

@@ -1,3 +1,5 @@
+# HISTORICAL: drives a hot-row combining / replica build that was withdrawn;
+# its GV_COMB_* / GV_REP_* variables do nothing in the current library. Results: profiles/r01_hot_row_combining.json
 # hot-row delta replicas: full-size quality first, parity tests, then speed on C2
 #timeout 900 python -m pytest tests/test_gpu_fullsize.py -x -q -s -k quality_grid > gpurun_out/rep_quality.log 2>&1; echo "rc=$?" >> gpurun_out/rep_quality.log
 #GV_REP_ROWS=16 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "disjoint_rows or degenerate or hogwild_auc or hogwild_shapes" > gpurun_out/rep_tests.log 2>&1; echo "rc=$?" >> gpurun_out/rep_tests.log

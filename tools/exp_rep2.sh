@@ -1,3 +1,5 @@
+# HISTORICAL: drives a hot-row combining / replica build that was withdrawn;
+# its GV_COMB_* / GV_REP_* variables do nothing in the current library. Results: profiles/r01_hot_row_combining.json
 # hot-row delta replicas: merge period sweep at n = 8 (C2), then full-size quality at the longest period
 for E in 16 32 64; do
   GV_REP_EVERY=$E timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-pipeline --parts-per-rank 8 > gpurun_out/rep2_E$E.json 2> gpurun_out/rep2_E$E.err

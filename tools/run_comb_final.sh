@@ -1,3 +1,5 @@
+# HISTORICAL: drives a hot-row combining / replica build that was withdrawn;
+# its GV_COMB_* / GV_REP_* variables do nothing in the current library. Results: profiles/r01_hot_row_combining.json
 # combining on by default for n >= 4: full GPU suite, smoke, default bench (n = 1), n = 8 bench
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/cf_tests.log 2>&1; echo "rc=$?" >> gpurun_out/cf_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/cf_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/cf_smoke.log
