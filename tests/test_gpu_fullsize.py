@@ -1,6 +1,7 @@
 """GPU checks at BASELINE.json's full single-GPU size (configs[1], C2:
 1,138,499 nodes / 4,945,382 edges, d = 128, K = 1, s = 5, 2e8-sample pool) in
-the launch configuration bench.py times (Hogwild kernel, n = 1), plus the
+the launch configuration bench.py times (Hogwild kernel, n = 1; one element-wise
+check of that kernel against the ordered one on schedule-independent samples), plus the
 collaboration pipeline (gv_run).
 
 Element-wise parity of Hogwild SGD at this size is not computable (the
@@ -164,3 +165,45 @@ def test_full_size_quality_grid_matches_n1():
     print("full-size AUC by n", auc)
     assert auc[1] >= 0.8, auc
     assert abs(auc[4] - auc[1]) <= 0.01 and abs(auc[8] - auc[1]) <= 0.01, auc
+
+
+def test_full_size_ring_kernel_elementwise_in_bench_launch():
+    """The bench kernel element by element at C2's matrix size and in the
+    bench's launch configuration (persistent grid of 2 CTAs x 4 warps per SM,
+    every warp running two 32-sample chunks), against the ordered kernel:
+    75,776 samples with pairwise-distinct u and distinct v, and neg_weight = 0
+    so that the negatives (which collide at this count) contribute nothing
+    and no sample reads a row another sample writes — the schedule cannot
+    matter, so both kernels must agree to fp32 rounding (1e-5 relative on the
+    touched rows) and every other row must be bit-identical. The negative
+    path itself is pinned by test_ring_kernel_math_matches_ordered_on_disjoint_rows."""
+    nv, d = C2["nv"], C2["d"]
+    ids = np.arange(nv, dtype=np.uint32)
+    src, dst = ids, ((ids + 1) % nv).astype(np.uint32)  # a ring: alias tables only
+    rng = np.random.default_rng(7)
+    count = 2 * 32 * 4 * 2 * 148
+    u = rng.choice(nv, count, replace=False).astype(np.uint32)
+    v = rng.choice(nv, count, replace=False).astype(np.uint32)
+    pool = np.stack([u, v], axis=1)
+    C_init = (rng.standard_normal((nv, d)) * 0.1).astype(np.float32)
+    out = {}
+    for mode in (0, 1):
+        g = G.GraphVite(nv, d, 1, 1, 0.05, lr_kind=0, ordered=mode, neg_weight=0.0)
+        g.load_edges(src, dst)
+        g.set_context(C_init)
+        V0 = g.vertex()
+        g.push(pool)
+        st = g.train_episode()
+        assert st["samples_global"] == count
+        out[mode] = (g.vertex(), g.context())
+        g.close()
+    (Vh, Ch), (Vo, Co) = out[0], out[1]
+    tv = np.zeros(nv, bool); tv[u] = True
+    tc = np.zeros(nv, bool); tc[v] = True
+    assert np.array_equal(Vh[~tv], V0[~tv]) and np.array_equal(Ch[~tc], C_init[~tc])
+    assert _rel(Vh[tv], Vo[tv]) <= 1e-5 and _rel(Ch[tc], Co[tc]) <= 1e-5
+    assert _rel(Vh[tv], V0[tv]) > 1e-4 and _rel(Ch[tc], C_init[tc]) > 1e-4  # not vacuous
+
+
+def _rel(a, b):
+    return np.linalg.norm(a.astype(np.float64) - b) / np.linalg.norm(b.astype(np.float64))
