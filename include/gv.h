@@ -40,7 +40,9 @@
  * [d*m, (d+1)*m), m = n_partitions / D, and at offset step t holds the
  * context partitions (d*m + t + g) mod n, g = 0..m-1 (a sliding window that
  * moves by one partition per step). D ranks are either
- *   - D separate processes (one per GPU, world_size = D, NCCL transport), or
+ *   - D separate processes (one per GPU, world_size = D; CUDA-IPC peer memory
+ *     over NVLink / NVSwitch between them, handshake through a POSIX
+ *     shared-memory segment), or
  *   - D virtual ranks inside one process on one GPU (virtual_ranks = D,
  *     device-copy transport) — the same schedule, used to test the
  *     multi-rank path on a single device.
@@ -55,7 +57,7 @@
 extern "C" {
 #endif
 
-#define GV_ABI_VERSION 1
+#define GV_ABI_VERSION 2
 
 typedef struct gv_ctx gv_ctx; /* opaque; owned by the library */
 
@@ -68,7 +70,7 @@ typedef enum {
   GV_ERR_CAPACITY = 5,    /* block > 2^32-1 samples, pool > max_pool_samples   */
   GV_ERR_NOMEM = 6,       /* host or device allocation failed                  */
   GV_ERR_CUDA = 7,        /* CUDA runtime failure (text in gv_last_error)      */
-  GV_ERR_COMM = 8         /* NCCL failure                                      */
+  GV_ERR_COMM = 8         /* inter-process transport failure (IPC / timeout)   */
 } gv_status;
 
 /* Learning-rate schedule ("initial learning rate of 0.025 and the
@@ -98,9 +100,6 @@ typedef struct {
   int compute_loss;       /* 1 = accumulate the per-sample loss (default 1)       */
   int host_threads;       /* threads for host graph preparation (0 = all cores)   */
   uint64_t max_pool_samples; /* per rank; 0 = grow on demand                      */
-  int transport;          /* world_size > 1: 0 = CUDA IPC peer copies with a shared-
-                             memory handshake (default; also runs several ranks on
-                             one GPU), 1 = NCCL send/recv                          */
   int host_partitions;    /* 1 = out-of-core (NEXT-3, Alg. 3): both
                              matrices live in pinned host memory; the device holds
                              three partition slots per matrix, loaded and written
@@ -110,8 +109,15 @@ typedef struct {
                              Default 0. */
 } gv_options;
 
-/* Per-pool statistics of THIS process (all its virtual ranks). Times are
- * CUDA-event durations on the rank's streams, in milliseconds. */
+#define GV_MAX_RANKS 64
+
+/* Per-pool statistics. The scalar times are over THIS process's ranks (all
+ * its virtual ranks); the *_rank arrays hold every one of the D ranks of the
+ * grid (multi-process: gathered through the IPC segment, so reading the
+ * statistics of pool e is a rendezvous of all processes — every rank reads
+ * them, or none). Times are CUDA-event durations on each rank's streams, in
+ * milliseconds. The metric of BASELINE.json (edge samples/s, device-timed,
+ * max over ranks) is samples_global / ms_device_max. */
 typedef struct {
   uint64_t pool_index;    /* e: the pool counter used in the Philox counter      */
   uint64_t samples;       /* samples trained by this process in this pool         */
@@ -127,13 +133,20 @@ typedef struct {
   double ms_total;        /* first bucketing launch -> last kernel/transfer       */
   uint32_t sgd_launches;  /* number of block-SGD kernel launches                  */
   uint32_t kernel_launches; /* all kernels launched by this call                  */
+  uint32_t n_ranks;       /* D = world_size * virtual_ranks                       */
+  double ms_device_max;   /* max over the D ranks of ms_total_rank                */
+  double ms_total_rank[GV_MAX_RANKS];    /* per rank d < n_ranks: as ms_total    */
+  double ms_bucket_rank[GV_MAX_RANKS];   /* as ms_bucket                         */
+  double ms_exchange_rank[GV_MAX_RANKS]; /* as ms_exchange                       */
+  double ms_sgd_rank[GV_MAX_RANKS];      /* as ms_sgd                            */
+  double ms_rotate_rank[GV_MAX_RANKS];   /* as ms_rotate (exposed rotation)      */
 } gv_episode_stats;
 
 /* ---------------------------------------------------------------------- */
 
 /* Fills *opt with defaults: seed 5, init_seed 4 (SURVEY §8(d) seeds),
  * neg_weight 5, device 0, rank 0, world_size 1, virtual_ranks 1, ordered 0,
- * compute_loss 1, host_threads 0, max_pool_samples 0, transport 0,
+ * compute_loss 1, host_threads 0, max_pool_samples 0,
  * host_partitions 0. */
 void gv_default_options(gv_options* opt);
 
@@ -238,7 +251,11 @@ gv_status gv_set_context_embeddings(gv_ctx* ctx, const float* in, uint64_t in_le
  * negative-sample Philox stream (R-RNG) and the global sample count S_before
  * of the lr schedule (R-LR). Saving them with the embeddings and restoring
  * both into a fresh context resumes a run exactly (ordered mode: bit for bit).
- * gv_set_progress: GV_ERR_STATE while a prepared pool is pending. */
+ * gv_set_progress: GV_ERR_STATE while a prepared pool is pending. In
+ * multi-process mode (world_size > 1) the pool counter also numbers the
+ * ranks' IPC handshake epochs, so every rank must call gv_set_progress with
+ * the SAME values, after gv_load_edges and before its first pool is pushed
+ * (GV_ERR_STATE otherwise). */
 gv_status gv_get_progress(gv_ctx* ctx, uint64_t* pool_index, uint64_t* samples_done);
 gv_status gv_set_progress(gv_ctx* ctx, uint64_t pool_index, uint64_t samples_done);
 

@@ -67,56 +67,71 @@ struct or_graph {
   double* deg;
 };
 
-typedef struct {
-  uint32_t row, col;
-  uint64_t k; /* input index: keeps duplicate summation in input order */
-  double w;
-} entry_t;
-
-static int cmp_entry(const void* a, const void* b) {
-  const entry_t* x = (const entry_t*)a;
-  const entry_t* y = (const entry_t*)b;
-  if (x->row != y->row) return x->row < y->row ? -1 : 1;
-  if (x->col != y->col) return x->col < y->col ? -1 : 1;
-  if (x->k != y->k) return x->k < y->k ? -1 : 1;
-  return 0;
-}
-
+/* The symmetrised entries (row, col, input index k) are put in (row, col,
+ * k) order by two STABLE counting sorts — by col, then by row (an LSD radix
+ * sort with one digit per node id) — over the entries generated in input
+ * order (edge k gives (src,dst,k) then (dst,src,k)). That is the order a
+ * comparison sort by (row, col, k) gives, in time linear in |E| (the
+ * Friendster-sized graph has 3.6e9 entries). Runs of equal (row, col)
+ * are then merged, summing their weights in input order. Inputs with
+ * 2^32 or more edges are rejected (k is stored in 32 bits).               */
 int or_graph_build(uint32_t nv, const uint32_t* src, const uint32_t* dst,
                    const float* w, uint64_t ne, or_graph** out) {
   *out = NULL;
   if (nv == 0) return OR_ERR_INVALID_ARG;
+  if (ne >= ((uint64_t)1 << 32)) return OR_ERR_INVALID_ARG;
   for (uint64_t k = 0; k < ne; k++) {
     if (src[k] >= nv || dst[k] >= nv) return OR_ERR_OUT_OF_RANGE;
     if (w && (!isfinite(w[k]) || w[k] < 0.0f)) return OR_ERR_INVALID_ARG;
   }
+  uint64_t* cnt_col = (uint64_t*)calloc((size_t)nv + 1, sizeof(uint64_t));
+  uint64_t* cnt_row = (uint64_t*)calloc((size_t)nv + 1, sizeof(uint64_t));
+  if (!cnt_col || !cnt_row) { free(cnt_col); free(cnt_row); return OR_ERR_NOMEM; }
+  /* entry counts per column and per row (symmetric: the same numbers) */
   uint64_t n_dir = 0;
-  for (uint64_t k = 0; k < ne; k++)
-    if (src[k] != dst[k]) n_dir += 2;
-  if (n_dir == 0) return OR_ERR_EMPTY;
-  entry_t* e = (entry_t*)malloc(n_dir * sizeof(entry_t));
-  if (!e) return OR_ERR_NOMEM;
-  uint64_t p = 0;
   for (uint64_t k = 0; k < ne; k++) {
     if (src[k] == dst[k]) continue;
-    double wk = w ? (double)w[k] : 1.0;
-    e[p].row = src[k]; e[p].col = dst[k]; e[p].k = k; e[p].w = wk; p++;
-    e[p].row = dst[k]; e[p].col = src[k]; e[p].k = k; e[p].w = wk; p++;
+    cnt_col[dst[k] + 1]++; cnt_col[src[k] + 1]++;
+    cnt_row[src[k] + 1]++; cnt_row[dst[k] + 1]++;
+    n_dir += 2;
   }
-  qsort(e, n_dir, sizeof(entry_t), cmp_entry);
+  if (n_dir == 0) { free(cnt_col); free(cnt_row); return OR_ERR_EMPTY; }
+  for (uint32_t v = 0; v < nv; v++) {
+    cnt_col[v + 1] += cnt_col[v];
+    cnt_row[v + 1] += cnt_row[v];
+  }
+  /* pass 1: stable by col; by_col[] holds (row, k), its col is implied */
+  uint32_t* by_col = (uint32_t*)malloc(n_dir * 2 * sizeof(uint32_t));
+  uint64_t* fill = (uint64_t*)malloc(((size_t)nv + 1) * sizeof(uint64_t));
+  if (!by_col || !fill) { free(by_col); free(fill); free(cnt_col); free(cnt_row); return OR_ERR_NOMEM; }
+  memcpy(fill, cnt_col, ((size_t)nv + 1) * sizeof(uint64_t));
+  for (uint64_t k = 0; k < ne; k++) {
+    uint32_t a = src[k], b = dst[k];
+    if (a == b) continue;
+    uint64_t q = fill[b]++; by_col[2 * q] = a; by_col[2 * q + 1] = (uint32_t)k; /* (a, b, k) */
+    q = fill[a]++;          by_col[2 * q] = b; by_col[2 * q + 1] = (uint32_t)k; /* (b, a, k) */
+  }
+  /* pass 2: stable by row; by_row[] holds (col, k) in (row, col, k) order */
+  uint32_t* by_row = (uint32_t*)malloc(n_dir * 2 * sizeof(uint32_t));
+  if (!by_row) { free(by_col); free(fill); free(cnt_col); free(cnt_row); return OR_ERR_NOMEM; }
+  memcpy(fill, cnt_row, ((size_t)nv + 1) * sizeof(uint64_t));
+  for (uint32_t col = 0; col < nv; col++) {
+    for (uint64_t q = cnt_col[col]; q < cnt_col[col + 1]; q++) {
+      uint64_t r = fill[by_col[2 * q]]++;
+      by_row[2 * r] = col;
+      by_row[2 * r + 1] = by_col[2 * q + 1];
+    }
+  }
+  free(by_col);
+  free(fill);
+  free(cnt_col);
   /* merge runs of equal (row, col), summing weights in input order */
   uint64_t m = 0;
-  for (uint64_t a = 0; a < n_dir;) {
-    uint64_t b = a;
-    double s = 0.0;
-    while (b < n_dir && e[b].row == e[a].row && e[b].col == e[a].col) {
-      s += e[b].w;
-      b++;
-    }
-    e[m].row = e[a].row; e[m].col = e[a].col; e[m].w = s; m++;
-    a = b;
-  }
+  for (uint32_t row = 0; row < nv; row++)
+    for (uint64_t q = cnt_row[row]; q < cnt_row[row + 1]; q++)
+      if (q == cnt_row[row] || by_row[2 * q] != by_row[2 * (q - 1)]) m++;
   or_graph* g = (or_graph*)calloc(1, sizeof(or_graph));
+  if (!g) { free(by_row); free(cnt_row); return OR_ERR_NOMEM; }
   g->nv = nv;
   g->n_entries = m;
   g->off = (uint64_t*)calloc((size_t)nv + 1, sizeof(uint64_t));
@@ -124,17 +139,30 @@ int or_graph_build(uint32_t nv, const uint32_t* src, const uint32_t* dst,
   g->w = (double*)malloc(m * sizeof(double));
   g->deg = (double*)calloc(nv, sizeof(double));
   if (!g->off || !g->nbr || !g->w || !g->deg) {
-    free(e); or_graph_free(g); return OR_ERR_NOMEM;
+    free(by_row); free(cnt_row); or_graph_free(g); return OR_ERR_NOMEM;
   }
-  for (uint64_t q = 0; q < m; q++) g->off[e[q].row + 1]++;
-  for (uint32_t v = 0; v < nv; v++) g->off[v + 1] += g->off[v];
-  for (uint64_t q = 0; q < m; q++) { g->nbr[q] = e[q].col; g->w[q] = e[q].w; }
+  uint64_t o = 0;
+  for (uint32_t row = 0; row < nv; row++) {
+    g->off[row] = o;
+    for (uint64_t q = cnt_row[row]; q < cnt_row[row + 1]; q++) {
+      double wk = w ? (double)w[by_row[2 * q + 1]] : 1.0;
+      if (q == cnt_row[row] || by_row[2 * q] != by_row[2 * (q - 1)]) {
+        g->nbr[o] = by_row[2 * q];
+        g->w[o] = wk;
+        o++;
+      } else {
+        g->w[o - 1] += wk;
+      }
+    }
+  }
+  g->off[nv] = o;
   for (uint32_t v = 0; v < nv; v++) {
     double s = 0.0;
     for (uint64_t q = g->off[v]; q < g->off[v + 1]; q++) s += g->w[q];
     g->deg[v] = s;
   }
-  free(e);
+  free(by_row);
+  free(cnt_row);
   *out = g;
   return OR_OK;
 }
@@ -337,9 +365,12 @@ void or_init_vertex(uint32_t nv, uint32_t d, uint64_t seed, float* vertex) {
   uint32_t key[2];
   seed_to_key(seed, key);
   for (uint32_t v = 0; v < nv; v++) {
+    uint32_t r[4];
     for (uint32_t k = 0; k < d; k++) {
-      uint32_t ctr[4] = {v, k / 4, 0u, 0x494E4954u}, r[4];
-      or_philox4x32_10(ctr, key, r);
+      if (k % 4 == 0) { /* one Philox block serves columns k .. k+3 */
+        uint32_t ctr[4] = {v, k / 4, 0u, 0x494E4954u};
+        or_philox4x32_10(ctr, key, r);
+      }
       float u01 = (float)(r[k % 4] >> 8) * 0x1p-24f;
       vertex[(uint64_t)v * d + k] = (u01 - 0.5f) / (float)d;
     }
@@ -571,6 +602,7 @@ int or_trainer_alias(const or_trainer* t, uint32_t p, uint32_t* prob, uint32_t* 
   return OR_OK;
 }
 uint64_t or_trainer_samples_done(const or_trainer* t) { return t->samples_done; }
+const or_graph* or_trainer_graph(const or_trainer* t) { return t->g; }
 void or_trainer_free(or_trainer* t) {
   if (!t) return;
   or_graph_free(t->g);

@@ -92,6 +92,9 @@ void or_trainer_set(or_trainer* t, int which, const float* in);
 void or_trainer_partition(const or_trainer* t, uint32_t* perm, uint64_t* part_off);
 int or_trainer_alias(const or_trainer* t, uint32_t p, uint32_t* prob, uint32_t* alias);
 uint64_t or_trainer_samples_done(const or_trainer* t);
+/* The trainer's ingested graph (owned by the trainer; NULL before
+ * load_edges): a sampler can share it instead of ingesting the edges again. */
+const or_graph* or_trainer_graph(const or_trainer* t);
 void or_trainer_free(or_trainer* t);
 
 /* Embedding initialisation (step 5): vertex[v][k] in [-0.5/d, 0.5/d). */

@@ -84,6 +84,7 @@ def _declare(L):
         "or_trainer_partition": (None, [vp, u32p, u64p]),
         "or_trainer_alias": (C.c_int, [vp, C.c_uint32, u32p, u32p]),
         "or_trainer_samples_done": (C.c_uint64, [vp]),
+        "or_trainer_graph": (vp, [vp]),
         "or_trainer_free": (None, [vp]),
         "or_init_vertex": (None, [C.c_uint32, C.c_uint32, C.c_uint64, f32p]),
         "or_sampler_create": (C.c_int, [vp, C.POINTER(vp)]),
@@ -249,8 +250,16 @@ class Graph:
         return deg
 
 
+class _TrainerGraph:
+    """Borrowed view of a Trainer's ingested graph (kept alive by the trainer)."""
+
+    def __init__(self, trainer):
+        self.trainer = trainer
+        self.h = lib().or_trainer_graph(trainer.h)
+
+
 class Sampler:
-    def __init__(self, graph: Graph):
+    def __init__(self, graph):
         self.graph = graph
         h = vp()
         _check(lib().or_sampler_create(graph.h, C.byref(h)), "sampler_create")
@@ -287,6 +296,11 @@ class Trainer:
         if getattr(self, "h", None) and _lib is not None:
             _lib.or_trainer_free(self.h)
             self.h = None
+
+    def sampler(self):
+        """Online-augmentation sampler over the graph this trainer ingested
+        (no second ingest: the Friendster-shaped graph is 43 GB as CSR)."""
+        return Sampler(_TrainerGraph(self))
 
     def load_edges(self, src, dst, w=None):
         src = _u32(src)

@@ -1,8 +1,9 @@
 // engine.cpp — context, episode scheduler and C ABI (include/gv.h).
 //
 // One gv_ctx per process. It drives D ranks of Alg. 3: either
-// the single rank of this process (world_size = D, NCCL between processes)
-// or D virtual ranks on this process's GPU (virtual_ranks = D, device copies).
+// the single rank of this process (world_size = D, CUDA-IPC peer memory
+// between processes) or D virtual ranks on this process's GPU
+// (virtual_ranks = D, device copies).
 // Rank d owns vertex partitions [d m, (d+1) m), m = n / D, and at offset
 // step t holds the context window (d m + t + g) mod n, g = 0..m-1. After it
 // trains its first block of step t (context (d m + t) mod n) it sends that
@@ -10,10 +11,8 @@
 // the transfer overlaps the rank's remaining m-1 blocks.
 // With m = 1 this is Alg. 3's train -> rotate -> train ring.
 #include <cuda_runtime.h>
-#include <dlfcn.h>
 #include <nvtx3/nvToolsExt.h>
 #include <sys/mman.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -43,41 +42,6 @@ struct NvtxRange {
   explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
   ~NvtxRange() { nvtxRangePop(); }
 };
-
-// ------------------------------------------------------------------ NCCL
-// Loaded lazily so that single-process use has no NCCL dependency.
-struct NcclApi {
-  bool ok = false;
-  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*GroupStart)() = nullptr;
-  ncclResult_t (*GroupEnd)() = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
-};
-
-NcclApi& nccl() {
-  static NcclApi api;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    const char* names[] = {"libnccl.so.2", "libnccl.so"};
-    void* h = nullptr;
-    for (const char* n : names)
-      if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
-    if (!h) return;
-#define GV_SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, "nccl" #f))
-    GV_SYM(GetUniqueId); GV_SYM(CommInitRank); GV_SYM(CommDestroy); GV_SYM(Send);
-    GV_SYM(Recv); GV_SYM(AllGather); GV_SYM(GroupStart); GV_SYM(GroupEnd); GV_SYM(GetErrorString);
-#undef GV_SYM
-    api.ok = api.GetUniqueId && api.CommInitRank && api.Send && api.Recv && api.AllGather &&
-             api.GroupStart && api.GroupEnd;
-  });
-  return api;
-}
 
 // -------------------------------------------------------------- buffers
 template <class T>
@@ -114,12 +78,10 @@ struct Rank {
   uint64_t crows = 0, slot_rows = 0;
   std::vector<int> slot_of;  // partition -> context slot (D > 1)
   int free_slot = -1;
-  DevBuf<uint2> local_blocks, recv, blocks;
+  DevBuf<uint2> blocks;
   DevBuf<uint8_t> scratch;
   DevBuf<uint64_t> counts;      // [0, bins]: block_off; [bins+1]: error flag
-  DevBuf<uint64_t> all_counts;  // NCCL: gathered counts of every rank
   DevBuf<gv::BlockDesc> desc;
-  DevBuf<gv::CopySeg> segs;
   DevBuf<uint64_t> place_args;  // fused exchange: dst_off[bins] | outs[D] (device pointers)
   gv::BucketPlan plan{};
   DevBuf<double> loss;
@@ -129,7 +91,7 @@ struct Rank {
   uint64_t seg_begin = 0, seg_count = 0;
   // events
   cudaEvent_t ev_start = nullptr, ev_bucket = nullptr, ev_exch = nullptr, ev_end = nullptr;
-  cudaEvent_t ev_recv_consumed = nullptr, ev_exch_sent = nullptr;
+  cudaEvent_t ev_exch_sent = nullptr;
   std::vector<cudaEvent_t> ev_first_done, ev_recv, ev_sent;  // per step
   cudaEvent_t ev_last_recv = nullptr;  // rotation into the window of the next pool
   bool have_last_recv = false;
@@ -205,7 +167,6 @@ struct gv_ctx {
   uint64_t pool_index = 0;
   uint64_t samples_done = 0;  // global samples trained in earlier steps
   std::vector<Rank> ranks;
-  ncclComm_t comm = nullptr;
   bool comm_ready = false;
   // out-of-core mode (host_partitions): matrices in pinned host memory, three
   // device slots per matrix; loads (H2D) and write-backs (D2H) run on their
@@ -216,7 +177,7 @@ struct gv_ctx {
   uint64_t hp_clock = 0;
   cudaStream_t hp_h2d = nullptr, hp_d2h = nullptr;
   bool hp() const { return opt.host_partitions != 0; }
-  // CUDA-IPC transport (world_size > 1, transport 0)
+  // CUDA-IPC transport (world_size > 1)
   gv::IpcShm* shm = nullptr;
   std::string shm_name;
   float* peer_ctx[gv::kIpcMaxRanks] = {};
@@ -233,8 +194,8 @@ struct gv_ctx {
   // peer has moved past the pool that announced the new handle
   std::vector<std::pair<uint2*, uint64_t>> blocks_graveyard;  // (ptr, retired at pool e)
   double ipc_timeout = 300.0;
-  bool ipc() const { return opt.world_size > 1 && opt.transport == 0; }
-  bool use_nccl() const { return opt.world_size > 1 && opt.transport == 1; }
+  uint64_t ipc_epoch0 = 0;  // pool counter of this session's first pool (gv_set_progress)
+  bool ipc() const { return opt.world_size > 1; }
 };
 
 namespace {
@@ -253,15 +214,6 @@ gv_status fail(gv_ctx* c, gv_status s, const std::string& msg) {
     cudaError_t e_ = (call);                                                            \
     if (e_ != cudaSuccess)                                                              \
       return fail(c, GV_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-
-#define NK(call)                                                                         \
-  do {                                                                                   \
-    ncclResult_t r_ = (call);                                                            \
-    if (r_ != ncclSuccess)                                                               \
-      return fail(c, GV_ERR_COMM,                                                        \
-                  std::string(#call) + ": " +                                            \
-                      (nccl().GetErrorString ? nccl().GetErrorString(r_) : "nccl error")); \
   } while (0)
 
 float lr_at(const gv_ctx* c, uint64_t s_before) {
@@ -423,10 +375,10 @@ gv_status prepare(gv_ctx* c) {
   const int a = c->active;
   const uint32_t n = c->n, bins = n * n;
   const uint64_t P = c->pool_P;
-  // D > 1 without NCCL (virtual ranks, CUDA-IPC processes): the scatter of a5
-  // writes every sample straight into the receive buffer of the rank that
-  // owns its block row (a6 fused into a5); it runs after the counts are known
-  const bool fused = c->D > 1 && !c->use_nccl();
+  // D > 1 (virtual ranks, CUDA-IPC processes): the scatter of a5 writes every
+  // sample straight into the receive buffer of the rank that owns its block
+  // row (a6 fused into a5); it runs after the counts are known
+  const bool fused = c->D > 1;
   // 1) bucketing per rank (a3-a5)
   for (auto& r : c->ranks) {
     r.kernel_launches = 0;
@@ -449,11 +401,10 @@ gv_status prepare(gv_ctx* c) {
                                  c->part.pbits, r.plan, r.scratch.p, r.counts.p, err, r.compute,
                                  &r.kernel_launches));
     } else {
-      DevBuf<uint2>& out = (c->D == 1) ? r.blocks : r.local_blocks;
-      CK(out.ensure(r.seg_count));
+      CK(r.blocks.ensure(r.seg_count));
       CK(gv::launch_bucket(c->raw[a].p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
-                           c->part.pbits, r.plan, r.scratch.p, out.p, r.counts.p, err, r.compute,
-                           &r.kernel_launches));
+                           c->part.pbits, r.plan, r.scratch.p, r.blocks.p, r.counts.p, err,
+                           r.compute, &r.kernel_launches));
       CK(cudaEventRecord(r.ev_bucket, r.compute));
     }
   }
@@ -469,7 +420,7 @@ gv_status prepare(gv_ctx* c) {
   };
   if (!fused)
     if (gv_status st = release_raw()) return st;
-  // 2) counts to the host (NCCL: all-gather first)
+  // 2) counts to the host (IPC: all-gathered through the shared-memory segment)
   std::vector<std::vector<uint64_t>> cnt(c->D, std::vector<uint64_t>(bins + 2, 0));
   if (c->ipc()) {
     Rank& r = c->ranks[0];
@@ -485,15 +436,6 @@ gv_status prepare(gv_ctx* c) {
         return fail(c, GV_ERR_COMM, "IPC timeout waiting for a peer's bucket counts");
       std::memcpy(cnt[q].data(), c->shm->rank[q].counts[e & 1], sizeof(uint64_t) * (bins + 2));
     }
-  } else if (c->use_nccl()) {
-    Rank& r = c->ranks[0];
-    NK(nccl().AllGather(r.counts.p, r.all_counts.p, bins + 2, ncclUint64, c->comm, r.compute));
-    CK(cudaMemcpyAsync(r.counts_host, r.all_counts.p, sizeof(uint64_t) * (bins + 2) * c->D,
-                       cudaMemcpyDeviceToHost, r.compute));
-    CK(cudaStreamSynchronize(r.compute));
-    for (int q = 0; q < c->D; ++q)
-      std::copy(r.counts_host + q * (bins + 2), r.counts_host + (q + 1) * (bins + 2),
-                cnt[q].begin());
   } else {
     for (auto& r : c->ranks)
       CK(cudaMemcpyAsync(r.counts_host, r.counts.p, sizeof(uint64_t) * (bins + 2),
@@ -540,56 +482,6 @@ gv_status prepare(gv_ctx* c) {
   if (fused) {
     if (gv_status st = place_fused(c, bc)) return st;
     if (gv_status st = release_raw()) return st;
-  } else if (c->D > 1) {
-    // chunk from rank s to rank d = local bins of rows [d m, (d+1) m) of rank s
-    auto chunk_begin = [&](int s, int d) { return cnt[s][d * m * n]; };
-    auto chunk_len = [&](int s, int d) { return cnt[s][(d + 1) * m * n] - cnt[s][d * m * n]; };
-    for (auto& r : c->ranks) {
-      uint64_t total = 0;
-      for (int s = 0; s < c->D; ++s) total += chunk_len(s, r.d);
-      CK(r.recv.ensure(total));
-      CK(r.blocks.ensure(total));
-    }
-    if (c->use_nccl()) {
-      Rank& r = c->ranks[0];
-      NK(nccl().GroupStart());
-      uint64_t roff = 0;
-      for (int p = 0; p < c->D; ++p) {
-        if (chunk_len(r.d, p))
-          NK(nccl().Send(r.local_blocks.p + chunk_begin(r.d, p), 2 * chunk_len(r.d, p), ncclUint32,
-                         p, c->comm, r.compute));
-        if (chunk_len(p, r.d))
-          NK(nccl().Recv(r.recv.p + roff, 2 * chunk_len(p, r.d), ncclUint32, p, c->comm,
-                         r.compute));
-        roff += chunk_len(p, r.d);
-      }
-      NK(nccl().GroupEnd());
-    }
-    // placement: block (i, j) = concatenation of the sub-blocks of ranks 0..D-1
-    for (auto& r : c->ranks) {
-      std::vector<gv::CopySeg> segs;
-      const uint32_t b0 = r.d * m * n;
-      uint64_t roff = 0;
-      std::vector<uint64_t> within(m * n, 0);
-      for (int s = 0; s < c->D; ++s) {
-        const uint64_t cb = chunk_begin(s, r.d);
-        for (uint32_t q = 0; q < m * n; ++q) {
-          const uint64_t len = bc[s][b0 + q];
-          if (len) segs.push_back({roff + (cnt[s][b0 + q] - cb), r.final_off[q] + within[q], len});
-          within[q] += len;
-        }
-        roff += chunk_len(s, r.d);
-      }
-      CK(r.segs.ensure(std::max<size_t>(segs.size(), 1)));
-      if (!segs.empty()) {
-        CK(cudaMemcpyAsync(r.segs.p, segs.data(), segs.size() * sizeof(gv::CopySeg),
-                           cudaMemcpyHostToDevice, r.compute));
-        CK(gv::launch_segmented_copy(r.recv.p, r.blocks.p, r.segs.p, static_cast<int>(segs.size()),
-                                     r.compute));
-        r.kernel_launches += 1;
-      }
-      CK(cudaEventRecord(r.ev_recv_consumed, r.compute));
-    }
   }
   for (auto& r : c->ranks) CK(cudaEventRecord(r.ev_exch, r.compute));
   c->state = PoolState::Prepared;
@@ -864,7 +756,7 @@ gv_status run_steps(gv_ctx* c) {
         return fail(c, GV_ERR_COMM, "IPC timeout waiting for the successor's first block");
       const uint32_t peer_slot = ps.first_slot[gs % gv::kIpcSlotRing];
       CK(cudaStreamWaitEvent(r.comm, c->peer_ev_first[src][gs % gv::kIpcEvRing], 0));
-      if (gs > 0) {  // our free slot was pulled by the predecessor at the previous step
+      if (gs > c->ipc_epoch0 * n) {  // our free slot was pulled by the predecessor at the previous step
         if (!gv::ipc_wait(c->shm->rank[prev].rot_epoch, gs, c->ipc_timeout))
           return fail(c, GV_ERR_COMM, "IPC timeout waiting for the predecessor's rotation");
         CK(cudaStreamWaitEvent(r.comm, c->peer_ev_rot[prev][(gs - 1) % gv::kIpcEvRing], 0));
@@ -876,24 +768,6 @@ gv_status run_steps(gv_ctx* c) {
           psize(c, in_p) * c->stride * sizeof(float), cudaMemcpyDeviceToDevice, r.comm));
       CK(cudaEventRecord(c->my_ev_rot[gs % gv::kIpcEvRing], r.comm));
       c->shm->rank[r.d].rot_epoch.store(gs + 1, std::memory_order_release);
-      CK(cudaEventRecord(r.ev_recv[t], r.comm));
-      const int s_out = r.slot_of[out_p];
-      r.slot_of[in_p] = r.free_slot;
-      r.slot_of[out_p] = -1;
-      r.free_slot = s_out;
-    } else if (c->use_nccl()) {
-      Rank& r = c->ranks[0];
-      gv_step_plan plan;
-      gv_plan_step(n, c->D, r.d, t, &plan);
-      const uint32_t out_p = plan.send_part, in_p = plan.recv_part;
-      const int prev = static_cast<int>(plan.send_to), next = static_cast<int>(plan.recv_from);
-      CK(cudaStreamWaitEvent(r.comm, r.ev_first_done[t], 0));
-      NK(nccl().GroupStart());
-      NK(nccl().Send(r.context + static_cast<uint64_t>(r.slot_of[out_p]) * r.slot_rows * c->stride,
-                     psize(c, out_p) * c->stride, ncclFloat32, prev, c->comm, r.comm));
-      NK(nccl().Recv(r.context + static_cast<uint64_t>(r.free_slot) * r.slot_rows * c->stride,
-                     psize(c, in_p) * c->stride, ncclFloat32, next, c->comm, r.comm));
-      NK(nccl().GroupEnd());
       CK(cudaEventRecord(r.ev_recv[t], r.comm));
       const int s_out = r.slot_of[out_p];
       r.slot_of[in_p] = r.free_slot;
@@ -980,6 +854,37 @@ gv_status collect_stats(gv_ctx* c, gv_episode_stats* out) {
     }
   }
   out->ms_rotate = std::max(0.0, out->ms_total - out->ms_bucket - out->ms_exchange - out->ms_sgd);
+  // per-rank device times; processes exchange theirs through
+  // the IPC segment, so every rank reports all D ranks and their maximum
+  out->n_ranks = static_cast<uint32_t>(c->D);
+  auto put = [&](int d, const double* v) {
+    out->ms_total_rank[d] = v[0];
+    out->ms_bucket_rank[d] = v[1];
+    out->ms_exchange_rank[d] = v[2];
+    out->ms_sgd_rank[d] = v[3];
+    out->ms_rotate_rank[d] = v[4];
+  };
+  for (auto& r : c->ranks) {
+    const double v[5] = {r.ms_total, r.ms_bucket, r.ms_exchange, r.ms_sgd,
+                         std::max(0.0, r.ms_total - r.ms_bucket - r.ms_exchange - r.ms_sgd)};
+    put(r.d, v);
+    if (c->ipc()) {
+      const uint64_t e = c->pool_index - 1;
+      gv::IpcRankShm& me = c->shm->rank[r.d];
+      std::memcpy(me.stats[e % gv::kIpcStatRing], v, sizeof(v));
+      me.stats_epoch.store(e + 1, std::memory_order_release);
+      for (int q = 0; q < c->D; ++q) {
+        if (q == r.d) continue;
+        gv::IpcRankShm& pr = c->shm->rank[q];
+        if (!gv::ipc_wait(pr.stats_epoch, e + 1, c->ipc_timeout))
+          return fail(c, GV_ERR_COMM, "IPC timeout waiting for a peer's pool statistics");
+        double pv[5];
+        std::memcpy(pv, pr.stats[e % gv::kIpcStatRing], sizeof(pv));
+        put(q, pv);
+      }
+    }
+  }
+  for (int d = 0; d < c->D; ++d) out->ms_device_max = std::max(out->ms_device_max, out->ms_total_rank[d]);
   return GV_OK;
 }
 
@@ -1071,16 +976,13 @@ gv_status setup_device(gv_ctx* c) {
     CK(cudaMemsetAsync(r.context, 0, sizeof(float) * r.crows * c->stride, r.compute));
     }  // !hp
     CK(r.counts.ensure(n * n + 2));
-    if (c->opt.world_size > 1) CK(r.all_counts.ensure(static_cast<size_t>(n * n + 2) * c->D));
     CK(r.loss.ensure(1));
     CK(cudaMallocHost(&r.counts_host, sizeof(uint64_t) * (n * n + 2) * c->D));
     r.ev_start = new_event(true);
     r.ev_bucket = new_event(true);
     r.ev_exch = new_event(true);
     r.ev_end = new_event(true);
-    r.ev_recv_consumed = new_event(false);
     r.ev_exch_sent = new_event(false);
-    CK(cudaEventRecord(r.ev_recv_consumed, r.compute));
   }
   gv_status st = sync_all(c);
   if (st || !c->ipc()) return st;
@@ -1148,7 +1050,6 @@ void gv_default_options(gv_options* o) {
   o->compute_loss = 1;
   o->host_threads = 0;
   o->max_pool_samples = 0;
-  o->transport = 0;
   o->host_partitions = 0;
 }
 
@@ -1193,8 +1094,6 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
     return fail(nullptr, GV_ERR_INVALID_ARG, "n_partitions must be a multiple of the rank count");
   if (o.host_partitions && (o.world_size * o.virtual_ranks != 1 || n_partitions < 2))
     return fail(nullptr, GV_ERR_INVALID_ARG, "host_partitions needs one rank and n_partitions >= 2");
-  if (o.transport != 0 && o.transport != 1)
-    return fail(nullptr, GV_ERR_INVALID_ARG, "transport must be 0 (CUDA IPC) or 1 (NCCL)");
   if (alpha && (alpha->kind != GV_LR_CONSTANT && alpha->kind != GV_LR_LINEAR))
     return fail(nullptr, GV_ERR_INVALID_ARG, "bad lr schedule kind");
   int ndev = 0;
@@ -1229,16 +1128,10 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
 
 gv_status gv_comm_unique_id(uint8_t id_out[128]) {
   gv_ctx* c = nullptr;
-  if (nccl().ok) {  // an NCCL id also names the IPC segment (it carries random bytes)
-    ncclUniqueId id;
-    NK(nccl().GetUniqueId(&id));
-    std::memcpy(id_out, id.internal, 128);
-    return GV_OK;
-  }
   FILE* f = fopen("/dev/urandom", "rb");
   if (!f || fread(id_out, 1, 128, f) != 128) {
     if (f) fclose(f);
-    return fail(nullptr, GV_ERR_COMM, "no NCCL and no /dev/urandom for a unique id");
+    return fail(nullptr, GV_ERR_COMM, "no /dev/urandom for a unique id");
   }
   fclose(f);
   return GV_OK;
@@ -1249,20 +1142,12 @@ gv_status gv_comm_init(gv_ctx* c, const uint8_t id[128]) {
   if (c->opt.world_size <= 1) return fail(c, GV_ERR_STATE, "gv_comm_init needs world_size > 1");
   if (c->loaded || c->comm_ready) return fail(c, GV_ERR_STATE, "call gv_comm_init before gv_load_edges, once");
   CK(cudaSetDevice(c->opt.device));
-  if (c->ipc()) {
-    if (c->D > gv::kIpcMaxRanks || c->n * c->n + 2 > static_cast<uint32_t>(gv::kIpcMaxBins))
-      return fail(c, GV_ERR_INVALID_ARG, "IPC transport: at most 16 ranks and 64 partitions");
-    std::string err;
-    c->shm = gv::ipc_open(id, &c->shm_name, &err);
-    if (!c->shm) return fail(c, GV_ERR_COMM, err);
-    if (const char* t = getenv("GV_IPC_TIMEOUT")) c->ipc_timeout = atof(t);
-    c->comm_ready = true;
-    return GV_OK;
-  }
-  if (!nccl().ok) return fail(c, GV_ERR_COMM, "libnccl.so.2 not loadable");
-  ncclUniqueId uid;
-  std::memcpy(uid.internal, id, 128);
-  NK(nccl().CommInitRank(&c->comm, c->opt.world_size, uid, c->opt.rank));
+  if (c->D > gv::kIpcMaxRanks || c->n * c->n + 2 > static_cast<uint32_t>(gv::kIpcMaxBins))
+    return fail(c, GV_ERR_INVALID_ARG, "IPC transport: at most 16 ranks and 64 partitions");
+  std::string err;
+  c->shm = gv::ipc_open(id, &c->shm_name, &err);
+  if (!c->shm) return fail(c, GV_ERR_COMM, err);
+  if (const char* t = getenv("GV_IPC_TIMEOUT")) c->ipc_timeout = atof(t);
   c->comm_ready = true;
   return GV_OK;
 }
@@ -1475,7 +1360,14 @@ gv_status gv_get_progress(gv_ctx* c, uint64_t* pool_index, uint64_t* samples_don
 gv_status gv_set_progress(gv_ctx* c, uint64_t pool_index, uint64_t samples_done) {
   if (gv_status s = check_ctx(c, false)) return s;
   if (c->state == PoolState::Prepared) return fail(c, GV_ERR_STATE, "a prepared pool is pending");
-  if (c->ipc()) return fail(c, GV_ERR_STATE, "set progress before the first pool on every rank");
+  if (c->ipc()) {
+    // the pool counter also numbers the IPC handshake epochs: ranks may only
+    // jump to a resumed position together, before their first pool
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (c->pool_index != 0 || c->raw_count[0] != 0 || c->raw_count[1] != 0 || c->last_active >= 0)
+      return fail(c, GV_ERR_STATE, "multi-process: set progress before the first pool is pushed");
+    c->ipc_epoch0 = pool_index;
+  }
   c->pool_index = pool_index;
   c->samples_done = samples_done;
   return GV_OK;
@@ -1707,7 +1599,7 @@ gv_status gv_device_bytes(gv_ctx* c, uint64_t* bytes) {
   b += c->raw[0].bytes_total() + c->raw[1].bytes_total();
   for (auto& r : c->ranks) {
     b += (r.vrows + r.crows) * c->stride * 4;
-    b += r.local_blocks.bytes_total() + r.recv.bytes_total() + r.blocks.bytes_total() +
+    b += r.blocks.bytes_total() +
          r.scratch.bytes_total();
   }
   *bytes = b;
@@ -1722,13 +1614,23 @@ void gv_destroy(gv_ctx* c) {
     if (r.comm) cudaStreamSynchronize(r.comm);
   }
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  if (c->ipc() && c->shm && !c->ranks.empty()) {
+    // Peers pull context partitions out of this rank's exported buffer (the
+    // last rotation of a pool lands on the peer's stream after our first
+    // block of that step): free it only once every peer has drained its own
+    // streams, which it announces here after its synchronisation above.
+    c->shm->rank[c->ranks[0].d].closed.store(1, std::memory_order_release);
+    for (int q = 0; q < c->D; ++q)
+      if (!gv::ipc_wait(c->shm->rank[q].closed, 1, c->ipc_timeout))
+        fprintf(stderr, "gv_destroy: rank %d did not close within the IPC timeout\n", q);
+  }
   for (auto& r : c->ranks) {
     cudaFree(r.vertex);
     cudaFree(r.context);
-    r.local_blocks.release(); r.recv.release(); r.blocks.release(); r.scratch.release();
-    r.counts.release(); r.all_counts.release(); r.desc.release(); r.segs.release(); r.loss.release();
+    r.blocks.release(); r.scratch.release();
+    r.counts.release(); r.desc.release(); r.loss.release();
     if (r.counts_host) cudaFreeHost(r.counts_host);
-    for (cudaEvent_t e : {r.ev_start, r.ev_bucket, r.ev_exch, r.ev_end, r.ev_recv_consumed,
+    for (cudaEvent_t e : {r.ev_start, r.ev_bucket, r.ev_exch, r.ev_end,
                           r.ev_exch_sent, r.ev_last_recv})
       if (e) cudaEventDestroy(e);
     for (auto* v : {&r.ev_first_done, &r.ev_recv, &r.ev_sent, &r.ev_sgd})
@@ -1761,7 +1663,6 @@ void gv_destroy(gv_ctx* c) {
   cudaFree(c->d_walias);
   cudaFree(c->d_dalias);
   cudaFree(c->d_inv_perm);
-  if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
   for (int q = 0; q < gv::kIpcMaxRanks; ++q) {
     if (c->peer_ctx[q]) cudaIpcCloseMemHandle(c->peer_ctx[q]);
     if (c->peer_blocks[q]) cudaIpcCloseMemHandle(c->peer_blocks[q]);

@@ -20,6 +20,7 @@ constexpr int kIpcMaxRanks = 16;
 constexpr int kIpcMaxBins = 64 * 64 + 2;
 constexpr int kIpcEvRing = 4;    // per-step events are a ring: slot g % 4
 constexpr int kIpcSlotRing = 64;
+constexpr int kIpcStatRing = 4;  // per-pool statistics: slot e % 4
 
 struct IpcRankShm {
   cudaIpcMemHandle_t ctx_handle;          // context slots buffer
@@ -30,12 +31,15 @@ struct IpcRankShm {
   cudaIpcEventHandle_t ev_rot[kIpcEvRing];    // "pulled my rotation of step g" (slot g % 4)
   uint32_t first_slot[kIpcSlotRing];      // context slot of send_part at step g (g % 64)
   uint64_t counts[2][kIpcMaxBins];        // block offsets + error flag of pool e (e % 2)
+  double stats[kIpcStatRing][5];          // ms total/bucket/exchange/sgd/rotate of pool e
   std::atomic<uint64_t> counts_epoch;     // e + 1: counts/blocks of pool e published
   std::atomic<uint64_t> pull_epoch;       // e + 1: ev_pull of pool e recorded
   std::atomic<uint64_t> recv_epoch;       // e + 1: receive buffer of pool e ready (handle current)
   std::atomic<uint64_t> first_epoch;      // g + 1: ev_first of step g recorded
   std::atomic<uint64_t> rot_epoch;        // g + 1: ev_rot of step g recorded
   std::atomic<uint64_t> joined;           // init handshake
+  std::atomic<uint64_t> stats_epoch;      // e + 1: stats of pool e published
+  std::atomic<uint64_t> closed;           // 1: streams drained in gv_destroy (no more pulls)
   char pad[64];
 };
 

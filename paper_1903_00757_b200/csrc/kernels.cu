@@ -8,7 +8,6 @@
 //   KB2v sgd_ordered       the same update, one warp per block, block order
 //   KB2x sgd_explicit      caller-given negatives (hand-derived tests)
 //   KB2d negatives         dump of the negative stream of one block
-//   KC  segmented_copy     block-row exchange placement (a6)
 //
 // Data layout: embedding rows are fp32, row stride a multiple
 // of 4 floats, so lane l of a warp owns float4 columns l, l+32, ... of a row
@@ -1269,23 +1268,24 @@ __global__ void bucket_adjust_kernel(const uint64_t* __restrict__ dst_off,
   }
 }
 
-__global__ void segmented_copy_kernel(const uint2* __restrict__ src, uint2* __restrict__ dst,
-                                      const CopySeg* __restrict__ segs) {
-  const CopySeg s = segs[blockIdx.y];
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < s.len;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    dst[s.dst + i] = src[s.src + i];
+// Per-device launch caches: a process may drive contexts on several devices
+// (gv_options.device), and function attributes / occupancy are per device.
+constexpr int kMaxDev = 64;
+int cur_dev() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return (dev >= 0 && dev < kMaxDev) ? dev : 0;
 }
-
-int g_num_sms = 0;
+int g_num_sms[kMaxDev] = {};
 int num_sms() {
-  if (g_num_sms == 0) {
+  int& v = g_num_sms[cur_dev()];
+  if (v == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
   }
-  return g_num_sms;
+  return v;
 }
 
 // ------------------------------------------------------------ dispatch table
@@ -1345,8 +1345,8 @@ cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaSt
     // large K (rows per stage) fits fewer warps per CTA
     const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / wb)));
     const size_t smem = wb * warps;
-    static int occr[8] = {};
-    int& o = occr[ki];
+    static int occr[kMaxDev][8] = {};
+    int& o = occr[cur_dev()][ki];
     if (o == 0) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, 32 * warps, smem) != cudaSuccess || o <= 0)
@@ -1359,8 +1359,8 @@ cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaSt
     return cudaGetLastError();
   }
   HogFn f = kHog[ki][ci];
-  static int occ[8][4] = {};
-  int& o = occ[ki][ci];
+  static int occ[kMaxDev][8][4] = {};
+  int& o = occ[cur_dev()][ki][ci];
   if (o == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, 256, 0) != cudaSuccess || o <= 0))
     o = 1;
   const uint64_t chunks = (a.total + 31) / 32;
@@ -1570,24 +1570,17 @@ cudaError_t launch_bucket(const uint2* in, uint64_t count, const uint32_t* packe
                              plan.bins, err, s, launches);
 }
 
-cudaError_t launch_segmented_copy(const uint2* src, uint2* dst, const CopySeg* segs, int nseg,
-                                  cudaStream_t s) {
-  if (nseg == 0) return cudaSuccess;
-  dim3 grid(64, static_cast<unsigned>(nseg));
-  segmented_copy_kernel<<<grid, 256, 0, s>>>(src, dst, segs);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_augment(const WalkDev& g, uint32_t walk_len, uint32_t s, uint32_t segments,
                            uint64_t count, uint64_t seed, uint32_t shuffle, uint2* out,
                            cudaStream_t st) {
   if (count == 0 || segments == 0) return cudaSuccess;
   const size_t smem = static_cast<size_t>(kAugBlock) * (walk_len + 1) * 4 + 8 + 8 * s;
-  static size_t set = 0;
-  if (smem > 48 * 1024 && smem > set) {
+  static size_t set[kMaxDev] = {};
+  size_t& done = set[cur_dev()];
+  if (smem > 48 * 1024 && smem > done) {
     cudaFuncSetAttribute(augment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    set = smem;
+    done = smem;
   }
   const unsigned grid = std::min<uint32_t>(segments, static_cast<uint32_t>(num_sms()) * 16);
   augment_kernel<<<grid, kAugBlock, smem, st>>>(g, walk_len, s, segments, count,

@@ -123,11 +123,4 @@ cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const uint32_t*
                                 uint2* const* outs, uint32_t bins_per_out, uint32_t* err_dev,
                                 cudaStream_t s, int* launches);
 
-// Segmented copy (block-row exchange, a6): copy[k] moves len samples.
-struct CopySeg {
-  uint64_t src, dst, len;
-};
-cudaError_t launch_segmented_copy(const uint2* src, uint2* dst, const CopySeg* segs, int nseg,
-                                  cudaStream_t s);
-
 }  // namespace gv

@@ -40,7 +40,7 @@ class gv_options(C.Structure):
                 ("device", C.c_int), ("rank", C.c_int), ("world_size", C.c_int),
                 ("virtual_ranks", C.c_int), ("ordered", C.c_int), ("compute_loss", C.c_int),
                 ("host_threads", C.c_int), ("max_pool_samples", C.c_uint64),
-                ("transport", C.c_int), ("host_partitions", C.c_int)]
+                ("host_partitions", C.c_int)]
 
 
 class gv_episode_stats(C.Structure):
@@ -48,10 +48,18 @@ class gv_episode_stats(C.Structure):
                 ("n_steps", C.c_uint32), ("lr_first", C.c_float), ("lr_last", C.c_float),
                 ("loss_sum", C.c_double), ("ms_bucket", C.c_double), ("ms_exchange", C.c_double),
                 ("ms_sgd", C.c_double), ("ms_rotate", C.c_double), ("ms_total", C.c_double),
-                ("sgd_launches", C.c_uint32), ("kernel_launches", C.c_uint32)]
+                ("sgd_launches", C.c_uint32), ("kernel_launches", C.c_uint32),
+                ("n_ranks", C.c_uint32), ("ms_device_max", C.c_double),
+                ("ms_total_rank", C.c_double * 64), ("ms_bucket_rank", C.c_double * 64),
+                ("ms_exchange_rank", C.c_double * 64), ("ms_sgd_rank", C.c_double * 64),
+                ("ms_rotate_rank", C.c_double * 64)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {}
+        for k, _ in self._fields_:
+            v = getattr(self, k)
+            d[k] = list(v)[:self.n_ranks] if k.endswith("_rank") else v
+        return d
 
 
 class gv_step_plan(C.Structure):
@@ -184,9 +192,11 @@ def gv_comm_init(ctx, uid: bytes):
 
 
 def gv_load_edges(ctx, src, dst, weight=None):
-    src = _u32(src)
-    dst = _u32(dst)
-    w = None if weight is None else np.ascontiguousarray(weight, dtype=np.float32)
+    src = _u32(src).reshape(-1)
+    dst = _u32(dst).reshape(-1)
+    w = None if weight is None else np.ascontiguousarray(weight, dtype=np.float32).reshape(-1)
+    if len(dst) != len(src) or (w is not None and len(w) != len(src)):
+        raise ValueError("gv_load_edges: src, dst (and weight) must have the same length")
     _ck(lib.gv_load_edges(ctx, _ptr(src, u32p), _ptr(dst, u32p), _ptr(w, f32p), len(src)), ctx)
 
 

@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 
 import synth
+from _parity import assert_matrix_parity
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -22,19 +23,19 @@ from paper_1903_00757_b200 import gv as G  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(tmp_path, world, n, pools, count, ordered, nv=4000, ne=20_000, grow=0, aug=0):
+def _run(tmp_path, world, n, pools, count, ordered, nv=4000, ne=20_000, grow=0, aug=0, kind=0):
     uid = G.gv_comm_unique_id().hex()
     worker = os.path.join(ROOT, "tests", "_mp_worker.py")
     outs = [str(tmp_path / f"r{r}.npz") for r in range(world)]
     env = dict(os.environ, GV_IPC_TIMEOUT="120")
     procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), uid, str(n), str(pools),
                                str(count), str(ordered), outs[r], str(nv), str(ne), str(grow),
-                               str(aug)],
+                               str(aug), str(kind)],
                               env=env)
              for r in range(world)]
     codes = [p.wait(timeout=600) for p in procs]
     assert codes == [0] * world, codes
-    d = 32
+    d = 32 if kind == 0 else 128
     V = np.full((nv, d), np.nan, np.float32)
     C = np.full((nv, d), np.nan, np.float32)
     losses = []
@@ -65,7 +66,8 @@ def test_processes_ordered_match_oracle(tmp_path, world, n):
     pools, count = 2, 200_001
     V, C, loss = _run(tmp_path, world, n, pools, count, ordered=1)
     Vo, Co, lo = _oracle(n, pools, count)
-    assert _rel(V, Vo) <= 1e-5 and _rel(C, Co) <= 1e-5
+    assert_matrix_parity(V, Vo, "vertex")
+    assert_matrix_parity(C, Co, "context")
     np.testing.assert_allclose(loss, lo, rtol=1e-4)
 
 
@@ -77,7 +79,8 @@ def test_processes_growing_pools_match_oracle(tmp_path):
     pools, count = 3, 50_001
     V, C, loss = _run(tmp_path, 2, 4, pools, count, ordered=1, grow=1)
     Vo, Co, lo = _oracle(4, pools, count, grow=1)
-    assert _rel(V, Vo) <= 1e-5 and _rel(C, Co) <= 1e-5
+    assert_matrix_parity(V, Vo, "vertex")
+    assert_matrix_parity(C, Co, "context")
     np.testing.assert_allclose(loss, lo, rtol=1e-4)
 
 
@@ -98,7 +101,8 @@ def test_processes_device_augmentation_match_oracle(tmp_path):
         segs = [sampler.augment(40, 2, 16, count * (r + 1) // world - count * r // world,
                                 500 + 1000 * e + r) for r in range(world)]
         o.train_pool(np.concatenate(segs))
-    assert _rel(V, o.get("vertex")) <= 1e-5 and _rel(C, o.get("context")) <= 1e-5
+    assert_matrix_parity(V, o.get("vertex"), "vertex")
+    assert_matrix_parity(C, o.get("context"), "context")
 
 
 @pytest.mark.parametrize("n", [2, 8])
@@ -113,3 +117,27 @@ def test_processes_hogwild_runs(tmp_path, n):
     # the unweighted monitoring loss need not fall this early (the objective
     # weighs negatives by 5); it must track the serial oracle's, pool by pool
     np.testing.assert_allclose(loss, lo, rtol=0.05)
+
+
+def test_processes_hogwild_auc_matches_oracle(tmp_path):
+    """Hogwild through the CUDA-IPC transport (2 processes, n = 4: two
+    partitions per rank, so each context rotation overlaps the rank's other
+    block; fused scatter into the peer's receive buffer) reaches the
+    link-prediction AUC of the serial oracle with the same n, pools
+    and seeds within 0.01, on the AUC-parity graph of SURVEY §8(c) (DC-SBM,
+    1e5 nodes / 1e6 edges, mu = 0.1 — reading R-AUCGRAPH, 1% held out,
+    d = 128, 4 pools of 1e7 samples = 40 epochs); AUC_oracle >= 0.8."""
+    nv, ne, n, pools, count = 100_000, 1_000_000, 4, 4, 10_000_000
+    V, C, loss = _run(tmp_path, 2, n, pools, count, ordered=0, nv=nv, ne=ne, kind=1)
+    assert np.isfinite(V).all() and np.isfinite(C).all() and np.isfinite(loss).all()
+    src, dst, _ = synth.dcsbm(nv, ne, gamma=2.1, wmax=1000.0, c=50, mu=0.1, seed=1)
+    tr_s, tr_d, pos, neg = synth.linkpred_split(src, dst, nv, holdout=0.01, seed=6)
+    o = O.Trainer(nv, 128, n, K=1, lr0=0.025, lr_kind=1, total_samples=pools * count)
+    o.load_edges(tr_s, tr_d)
+    for k in range(pools):
+        o.train_pool(synth.edge_pool(tr_s, tr_d, count, seed=200 + k))
+    auc_o = O.linkpred_auc(o.get("vertex"), pos, neg)
+    auc_g = O.linkpred_auc(V, pos, neg)
+    print("AUC oracle", auc_o, "2-process gpu", auc_g)
+    assert auc_o >= 0.8, auc_o
+    assert abs(auc_g - auc_o) <= 0.01, (auc_g, auc_o)

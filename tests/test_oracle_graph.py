@@ -128,3 +128,38 @@ def test_bucket_range_error():
     perm, inv, off = O.zigzag([1.0, 1.0], 1)
     with pytest.raises(O.OracleError):
         O.bucket([[0, 2]], 2, perm, off, 1)
+
+
+def test_ingest_sums_duplicates_in_input_order():
+    """R-INGEST: duplicate weights are summed in INPUT order (double). With a
+    weight of 2^24 and 1024 weights of 2^-30 on the same undirected edge the
+    order is visible in double: small ones first gives 2^24 + 2^-20 exactly,
+    the big one first absorbs every small one. The edge appears in both
+    directions with the same sum, and degree = that sum."""
+    big, small = np.float32(2.0 ** 24), np.float32(2.0 ** -30)
+    for first_big in (False, True):
+        ws = [small] * 1024 + [big]
+        if first_big:
+            ws = [big] + [small] * 1024
+        src = np.array([0, 1] * 512 + [0], np.uint32)  # both orientations of 0-1
+        dst = np.array([1, 0] * 512 + [1], np.uint32)
+        if first_big:
+            src, dst = np.r_[src[-1:], src[:-1]], np.r_[dst[-1:], dst[:-1]]
+        src = np.r_[src, [2]].astype(np.uint32)        # a second edge 1-2 so node 2 exists
+        dst = np.r_[dst, [1]].astype(np.uint32)
+        w = np.r_[np.array(ws, np.float32), [np.float32(1.0)]]
+        off, nbr, wt = O.Graph(3, src, dst, w).csr()
+        want = 2.0 ** 24 if first_big else 2.0 ** 24 + 2.0 ** -20
+        assert list(nbr[off[0]:off[1]]) == [1] and wt[off[0]] == want
+        assert wt[off[1]] == want and O.Graph(3, src, dst, w).degree()[0] == want
+
+
+def test_sampler_over_trainer_graph_equals_fresh_graph():
+    """Trainer.sampler() walks the trainer's own ingested graph: the pool is
+    the one a Sampler over a separately ingested Graph produces."""
+    src, dst = synth.chung_lu(2000, 10_000, gamma=2.1, wmax=200.0, seed=3)
+    t = O.Trainer(2000, 8, 2)
+    t.load_edges(src, dst)
+    a = t.sampler().augment(40, 3, 5, 20_000, 11)
+    b = O.Sampler(O.Graph(2000, src, dst)).augment(40, 3, 5, 20_000, 11)
+    assert np.array_equal(a, b)

@@ -255,3 +255,46 @@ def test_cpu_hogwild_baseline_matches_serial_with_one_thread():
     assert np.array_equal(res["hog1"][2], res["serial"][2])
     assert np.isfinite(res["hog4"][1]).all()
     assert abs(res["hog4"][0] - res["serial"][0]) <= 0.02 * res["serial"][0]
+
+
+def _manual_pool(t, pool, nv, n, e, s_before, total, lr0=0.05, per_step=True):
+    """Alg. 3 written out by hand with the oracle's pinned pieces: stable
+    bucketing (O.bucket), for offset step t = 0..n-1 the blocks (i, (i+t) mod n)
+    in i order, lr from the pinned O.lr with S_before = every
+    sample trained in EARLIER offset steps (R-LR)."""
+    perm, off = t.partition()
+    lp, boff = O.bucket(pool, nv, perm, off, n)
+    lr_pool = O.lr(1, lr0, 1e-4, s_before, total)
+    for step in range(n):
+        lr_t = O.lr(1, lr0, 1e-4, s_before, total) if per_step else lr_pool
+        for i in range(n):
+            j = (i + step) % n
+            b = i * n + j
+            t.train_block(lp[int(boff[b]):int(boff[b + 1])], i, j, e, lr_t)
+            s_before += int(boff[b + 1] - boff[b])
+    return s_before
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_train_pool_applies_lr_per_offset_step(n):
+    """Where the oracle applies lr (R-LR; P:392 linear decay): train_pool over
+    two pools equals hand-driven train_block calls with lr recomputed before
+    EACH offset step from the global sample count, bit for bit. The schedule
+    is short (total = 1.5 pools) so lr changes by ~1/(1.5 n) between steps; the
+    variant with one lr per pool must then differ (the pin is not vacuous)."""
+    nv = 600
+    pools = [None, None]
+    ref, src, dst = _trainer_with_graph(n, nv=nv, lr_kind=1, total=30_000)
+    for e in range(2):
+        pools[e] = synth.edge_pool(src, dst, 20_000, seed=40 + e)
+    hand, _, _ = _trainer_with_graph(n, nv=nv, lr_kind=1, total=30_000)
+    per_pool, _, _ = _trainer_with_graph(n, nv=nv, lr_kind=1, total=30_000)
+    s_hand = s_pool = 0
+    for e in range(2):
+        ref.train_pool(pools[e])
+        s_hand = _manual_pool(hand, pools[e], nv, n, e, s_hand, 30_000)
+        s_pool = _manual_pool(per_pool, pools[e], nv, n, e, s_pool, 30_000, per_step=False)
+    assert ref.samples_done == s_hand == 40_000
+    assert np.array_equal(ref.get("vertex"), hand.get("vertex"))
+    assert np.array_equal(ref.get("context"), hand.get("context"))
+    assert not np.array_equal(ref.get("vertex"), per_pool.get("vertex"))
