@@ -107,6 +107,11 @@ typedef struct {
                              order: steps in pairs, a reordering with the same
                              result). Single rank, n_partitions >= 2.
                              Default 0. */
+  int host_pool;          /* 1 = the raw sample pool lives in pinned, mapped HOST
+                             memory; bucketing reads it over PCIe, so samples take
+                             device memory only as bucketed blocks ("the
+                             memory cost of edge samples on GPUs becomes
+                             negligible"). 0 (default) = raw pool in HBM. */
 } gv_options;
 
 #define GV_MAX_RANKS 64
@@ -195,8 +200,13 @@ gv_status gv_load_edges(gv_ctx* ctx, const uint32_t* src, const uint32_t* dst,
                         const float* weight, uint64_t num_edges);
 
 /* Append count edge samples (pairs[2k], pairs[2k+1]) = (u, v), ORIGINAL ids,
- * to the pending pool (Alg. 2's concatenated pool). Copies host ->
- * device before returning (batched transfer P:284, on a copy stream).
+ * to the pending pool (Alg. 2's concatenated pool). Copies before
+ * returning, in chunks of 2^23 samples on the library's copy stream (batched
+ * transfer); a pinned source buffer is copied by DMA at PCIe speed.
+ * The library keeps ONE raw pool buffer: a push issued after
+ * gv_train_episode(pool k) waits only until pool k has been bucketed (a few
+ * ms into its training), then copies while pool k trains — device sample
+ * memory is 2 x 8 B per sample (raw + blocks), or 8 B with host_pool = 1.
  * With virtual_ranks = D the whole pool is pushed and rank r trains on the
  * contiguous segment [r*P/D, (r+1)*P/D); with world_size = D each process
  * pushes its own segment. Ids are range-checked on the device at

@@ -11,6 +11,8 @@
 // a pure function of (graph, seed, threads) whatever the thread timing.
 #include "augment.hpp"
 
+#include <algorithm>
+#include <atomic>
 #include <thread>
 
 #include "../../include/gv.h"
@@ -20,28 +22,35 @@ namespace gv {
 
 int build_walk_tables(const HostGraph& g, int threads, WalkTables* t) {
   t->g = &g;
-  t->departure.prob.resize(g.nv);
-  t->departure.alias.resize(g.nv);
-  int rc = build_alias(g.deg.data(), g.nv, t->departure.prob.data(), t->departure.alias.data());
+  t->departure.resize(g.nv);
+  int rc = build_alias(g.deg.data(), g.nv, t->departure.data());
   if (rc) return rc;
-  t->eprob.assign(g.nbr.size(), 0);
-  t->ealias.assign(g.nbr.size(), 0);
-  parallel_for(g.nv, threads, [&](uint64_t b, uint64_t e) {
-    for (uint64_t v = b; v < e; ++v) {
-      const uint64_t o = g.off[v], m = g.off[v + 1] - o;
-      if (m == 0 || !(g.deg[v] > 0.0)) continue;  // unreachable by any walk
-      build_alias(g.w.data() + o, static_cast<uint32_t>(m), t->eprob.data() + o,
-                  t->ealias.data() + o);
-    }
-  });
+  t->edge.assign(g.nbr.size(), ProbAlias{0, 0});
+  // rows in interleaved blocks: hub rows (up to thousands of entries) sit at
+  // random ids, so contiguous thread ranges would be unbalanced
+  std::atomic<uint64_t> next{0};
+  constexpr uint64_t kRows = 4096;
+  std::vector<std::thread> pool;
+  for (int th = 0; th < std::max(1, threads); ++th)
+    pool.emplace_back([&] {
+      for (uint64_t b; (b = next.fetch_add(kRows)) < g.nv;) {
+        const uint64_t e = std::min<uint64_t>(g.nv, b + kRows);
+        for (uint64_t v = b; v < e; ++v) {
+          const uint64_t o = g.off[v], m = g.off[v + 1] - o;
+          if (m == 0 || !(g.deg[v] > 0.0)) continue;  // unreachable by any walk
+          build_alias(g.w.data() + o, static_cast<uint32_t>(m), t->edge.data() + o);
+        }
+      }
+    });
+  for (auto& x : pool) x.join();
   return GV_OK;
 }
 
 namespace {
 
-inline uint32_t draw(const uint32_t* prob, const uint32_t* alias, uint32_t m, const u32x4& r) {
+inline uint32_t draw(const ProbAlias* t, uint32_t m, const u32x4& r) {
   const uint32_t slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, m);
-  return alias_pick(prob[slot], alias[slot], slot, r.z);
+  return alias_pick(t[slot].prob, t[slot].alias, slot, r.z);
 }
 
 // Walks are generated kBatch at a time, one step of every walk of the batch
@@ -69,15 +78,14 @@ void fill_segment(const WalkTables& t, uint32_t walk_len, uint32_t s, uint32_t t
   }
   const uint64_t* off = g.off.data();
   const uint32_t* nbr = g.nbr.data();
-  const uint32_t* ep = t.eprob.data();
-  const uint32_t* ea = t.ealias.data();
+  const ProbAlias* et = t.edge.data();
   uint64_t o[kBatch], slot[kBatch];
   uint32_t rz[kBatch];
   uint64_t filled = 0;
   for (uint32_t w0 = 0; filled < cap; w0 += kBatch) {
     for (uint32_t i = 0; i < kBatch; ++i) {
       const u32x4 r = philox4x32_10(u32x4{w0 + i, 0u, thread, kTagWalk}, k0, k1);
-      const uint32_t x = draw(t.departure.prob.data(), t.departure.alias.data(), g.nv, r);
+      const uint32_t x = draw(t.departure.data(), g.nv, r);
       walks[i * W] = x;
       __builtin_prefetch(off + x);
     }
@@ -89,13 +97,12 @@ void fill_segment(const WalkTables& t, uint32_t walk_len, uint32_t s, uint32_t t
         const u32x4 r = philox4x32_10(u32x4{w0 + i, k, thread, kTagWalk}, k0, k1);
         slot[i] = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, m);
         rz[i] = r.z;
-        __builtin_prefetch(ep + o[i] + slot[i]);
-        __builtin_prefetch(ea + o[i] + slot[i]);
+        __builtin_prefetch(et + o[i] + slot[i]);
         __builtin_prefetch(nbr + o[i] + slot[i]);
       }
       for (uint32_t i = 0; i < kBatch; ++i) {
         const uint64_t q = o[i] + slot[i];
-        const uint32_t pick = alias_pick(ep[q], ea[q], static_cast<uint32_t>(slot[i]), rz[i]);
+        const uint32_t pick = alias_pick(et[q].prob, et[q].alias, static_cast<uint32_t>(slot[i]), rz[i]);
         const uint32_t x = nbr[o[i] + pick];
         walks[i * W + k] = x;
         __builtin_prefetch(off + x);

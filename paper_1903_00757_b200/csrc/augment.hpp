@@ -10,9 +10,8 @@ namespace gv {
 
 struct WalkTables {
   const HostGraph* g = nullptr;
-  AliasU32 departure;             // over nodes, weight = degree
-  std::vector<uint32_t> eprob;    // per CSR entry: neighbour alias tables
-  std::vector<uint32_t> ealias;   // (local slot within the row)
+  Arr<ProbAlias> departure;  // over nodes, weight = degree
+  Arr<ProbAlias> edge;       // per CSR entry: the row's neighbour table (local slots)
 };
 
 int build_walk_tables(const HostGraph& g, int threads, WalkTables* t);

@@ -19,6 +19,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -29,6 +30,7 @@
 
 #include "../../include/gv.h"
 #include "augment.hpp"
+#include "graph_share.hpp"
 #include "host_graph.hpp"
 #include "ipc.hpp"
 #include "kernels.cuh"
@@ -49,21 +51,27 @@ struct DevBuf {
   T* p = nullptr;
   size_t cap = 0;     // elements
   uint64_t gen = 0;   // bumped by every (re)allocation
+  bool host = false;  // pinned, mapped host memory (kernels read it over PCIe / UVA)
   size_t bytes_total() const { return cap * sizeof(T); }
   cudaError_t ensure(size_t n) {
     if (n <= cap) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-    cudaError_t e = cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T));
+    release();
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    cudaError_t e = host ? cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable)
+                         : cudaMalloc(&p, bytes);
     if (e == cudaSuccess) {
       cap = std::max<size_t>(n, 1);
       ++gen;
+    } else {
+      p = nullptr;
     }
     return e;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (host) cudaFreeHost(p);
+      else cudaFree(p);
+    }
     p = nullptr;
     cap = 0;
   }
@@ -136,7 +144,7 @@ struct gv_ctx {
   // graph
   gv::HostGraph graph;
   gv::Partitioning part;
-  std::vector<uint32_t> nprob, nalias;  // negative tables, new-id order
+  gv::Arr<gv::ProbAlias> nalias;  // negative tables {prob, alias}, new-id order
   gv::WalkTables walks;
   // device copy of the walk tables (gv_augment_device), lazily uploaded
   uint64_t* d_woff = nullptr;
@@ -148,18 +156,21 @@ struct gv_ctx {
   uint32_t* d_packed = nullptr;
   uint2* d_alias = nullptr;
   uint32_t* d_inv_perm = nullptr;
-  // pools
+  // pool (a2): ONE raw buffer. gv_train_episode takes the pending pool out of
+  // it (prepare), and the next push may refill it as soon as the bucketing
+  // kernels have read it (raw_free) — a few ms into the pool's training — so
+  // the H2D copy of pool k+1 still overlaps the SGD of pool k, and device
+  // sample memory is raw + blocks = 2 P (not 3 P as with two raw buffers).
   std::mutex mu;
-  DevBuf<uint2> raw[2];
-  uint64_t raw_count[2] = {0, 0};
-  cudaEvent_t raw_ready[2] = {nullptr, nullptr};
-  cudaEvent_t raw_free[2] = {nullptr, nullptr};
-  int pending = 0;
-  int last_active = -1;
+  std::condition_variable raw_cv;
+  bool raw_busy = false;        // prepare has taken the pool, raw_free not yet recorded
+  DevBuf<uint2> raw;
+  uint64_t raw_count = 0;       // pending samples in raw
+  cudaEvent_t raw_ready = nullptr, raw_free = nullptr;
+  bool have_last = false;       // raw still holds the last trained pool (replay)
   uint64_t last_count = 0;
   cudaStream_t copy_stream = nullptr;
   PoolState state = PoolState::Idle;
-  int active = -1;
   uint64_t pool_P = 0;        // samples of the prepared pool (this process)
   uint64_t pool_P_global = 0; // all ranks
   std::vector<uint64_t> global_counts;  // bins (sum over ranks)
@@ -195,6 +206,8 @@ struct gv_ctx {
   std::vector<std::pair<uint2*, uint64_t>> blocks_graveyard;  // (ptr, retired at pool e)
   double ipc_timeout = 300.0;
   uint64_t ipc_epoch0 = 0;  // pool counter of this session's first pool (gv_set_progress)
+  std::string graph_shm_name;  // node-shared graph segment (rank 0 prepares it)
+  gv::SharedMapping graph_map;
   bool ipc() const { return opt.world_size > 1; }
 };
 
@@ -333,7 +346,7 @@ gv_status place_fused(gv_ctx* c, const std::vector<std::vector<uint64_t>>& bc) {
     CK(r.place_args.ensure(args.size()));
     CK(cudaMemcpyAsync(r.place_args.p, args.data(), args.size() * sizeof(uint64_t),
                        cudaMemcpyHostToDevice, r.compute));  // pageable: staged before return
-    CK(gv::launch_bucket_place(c->raw[c->active].p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
+    CK(gv::launch_bucket_place(c->raw.p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
                                c->part.pbits, r.plan, r.scratch.p, r.place_args.p,
                                reinterpret_cast<uint2* const*>(r.place_args.p + bins), bpr,
                                reinterpret_cast<uint32_t*>(r.counts.p + bins + 1), r.compute,
@@ -366,13 +379,25 @@ gv_status prepare(gv_ctx* c) {
   NvtxRange nv_range("gv:prepare (bucket + exchange)");
   {
     std::lock_guard<std::mutex> lk(c->mu);
-    if (c->raw_count[c->pending] == 0) return fail(c, GV_ERR_EMPTY, "no pending samples");
-    c->active = c->pending;
-    c->pool_P = c->raw_count[c->active];
-    c->pending ^= 1;
-    c->raw_count[c->pending] = 0;
+    if (c->raw_count == 0) return fail(c, GV_ERR_EMPTY, "no pending samples");
+    c->pool_P = c->raw_count;
+    c->raw_count = 0;
+    c->raw_busy = true;  // pushes wait until raw_free is recorded below
+    c->have_last = false;
   }
-  const int a = c->active;
+  // whatever way prepare ends, pushes must not wait forever
+  struct RawGuard {
+    gv_ctx* c;
+    ~RawGuard() {
+      std::lock_guard<std::mutex> lk(c->mu);
+      if (c->raw_busy) {  // an error path: let the kernels that read the pool finish
+        for (auto& r : c->ranks) cudaStreamSynchronize(r.compute);
+        cudaEventRecord(c->raw_free, c->copy_stream);
+        c->raw_busy = false;
+        c->raw_cv.notify_all();
+      }
+    }
+  } raw_guard{c};
   const uint32_t n = c->n, bins = n * n;
   const uint64_t P = c->pool_P;
   // D > 1 (virtual ranks, CUDA-IPC processes): the scatter of a5 writes every
@@ -390,19 +415,19 @@ gv_status prepare(gv_ctx* c) {
       r.seg_begin = P * static_cast<uint64_t>(r.d) / c->D;
       r.seg_count = P * static_cast<uint64_t>(r.d + 1) / c->D - r.seg_begin;
     }
-    CK(cudaStreamWaitEvent(r.compute, c->raw_ready[a], 0));
+    CK(cudaStreamWaitEvent(r.compute, c->raw_ready, 0));
     CK(cudaEventRecord(r.ev_start, r.compute));
     r.plan = gv::make_bucket_plan(n, r.seg_count);
     CK(r.scratch.ensure(gv::bucket_scratch_bytes(r.plan)));
     CK(cudaMemsetAsync(r.counts.p + bins + 1, 0, sizeof(uint64_t), r.compute));
     uint32_t* err = reinterpret_cast<uint32_t*>(r.counts.p + bins + 1);
     if (fused) {
-      CK(gv::launch_bucket_count(c->raw[a].p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
+      CK(gv::launch_bucket_count(c->raw.p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
                                  c->part.pbits, r.plan, r.scratch.p, r.counts.p, err, r.compute,
                                  &r.kernel_launches));
     } else {
       CK(r.blocks.ensure(r.seg_count));
-      CK(gv::launch_bucket(c->raw[a].p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
+      CK(gv::launch_bucket(c->raw.p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
                            c->part.pbits, r.plan, r.scratch.p, r.blocks.p, r.counts.p, err,
                            r.compute, &r.kernel_launches));
       CK(cudaEventRecord(r.ev_bucket, r.compute));
@@ -412,10 +437,12 @@ gv_status prepare(gv_ctx* c) {
   // placed) it
   auto release_raw = [&]() -> gv_status {
     for (auto& r : c->ranks) CK(cudaStreamWaitEvent(c->copy_stream, r.ev_bucket, 0));
-    CK(cudaEventRecord(c->raw_free[a], c->copy_stream));
+    CK(cudaEventRecord(c->raw_free, c->copy_stream));
     std::lock_guard<std::mutex> lk(c->mu);
-    c->last_active = a;
+    c->raw_busy = false;
+    c->have_last = true;
     c->last_count = P;
+    c->raw_cv.notify_all();
     return GV_OK;
   };
   if (!fused)
@@ -893,17 +920,15 @@ gv_status setup_device(gv_ctx* c) {
   CK(cudaMalloc(&c->d_packed, sizeof(uint32_t) * nv));
   CK(cudaMalloc(&c->d_alias, sizeof(uint2) * nv));
   CK(cudaMalloc(&c->d_inv_perm, sizeof(uint32_t) * nv));
-  std::vector<uint2> al(nv);
-  for (uint32_t k = 0; k < nv; ++k) al[k] = make_uint2(c->nprob[k], c->nalias[k]);
+  static_assert(sizeof(gv::ProbAlias) == sizeof(uint2), "alias slots upload as uint2");
   CK(cudaMemcpy(c->d_packed, c->part.packed.data(), sizeof(uint32_t) * nv, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(c->d_alias, al.data(), sizeof(uint2) * nv, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_alias, c->nalias.data(), sizeof(uint2) * nv, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_inv_perm, c->part.inv_perm.data(), sizeof(uint32_t) * nv,
                 cudaMemcpyHostToDevice));
   CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-  for (int k = 0; k < 2; ++k) {
-    c->raw_ready[k] = new_event(false);
-    c->raw_free[k] = new_event(false);
-  }
+  c->raw_ready = new_event(false);
+  c->raw_free = new_event(false);
+  c->raw.host = c->opt.host_pool != 0;
   const uint32_t key0 = static_cast<uint32_t>(c->opt.init_seed);
   const uint32_t key1 = static_cast<uint32_t>(c->opt.init_seed >> 32);
   const uint64_t max_part = c->part.max_part();
@@ -1022,7 +1047,44 @@ gv_status setup_device(gv_ctx* c) {
       if (!gv::ipc_wait(c->shm->rank[q].joined, 2, c->ipc_timeout))
         return fail(c, GV_ERR_COMM, "IPC timeout in the init handshake");
     shm_unlink(c->shm_name.c_str());
+    gv::graph_share_unlink(c->graph_shm_name);
   }
+  return GV_OK;
+}
+
+// Graph preparation (gv_load_edges): ingest (R-INGEST), zig-zag partition
+// (R-ZIGZAG), the partitions' negative alias tables over deg^0.75 (P:231,
+// P:392; R-ALIAS) and the walk tables of the augmentation.
+template <class Lap>
+gv_status prepare_graph(gv_ctx* c, const uint32_t* src, const uint32_t* dst, const float* weight,
+                        uint64_t num_edges, Lap& lap) {
+  std::string msg;
+  int rc = gv::build_graph(c->nv, src, dst, weight, num_edges, c->threads, &c->graph, &msg);
+  if (rc) return fail(c, static_cast<gv_status>(rc), msg);
+  lap("graph");
+  rc = gv::build_partitioning(c->graph, c->n, &c->part, &msg);
+  if (rc) return fail(c, static_cast<gv_status>(rc), msg);
+  lap("zig-zag partition");
+  // negative tables: deg^0.75 over each partition in local order (P:231, P:392)
+  c->nalias.assign(c->nv, gv::ProbAlias{0, 0});
+  std::vector<double> w(c->nv);
+  gv::parallel_for(c->nv, c->threads, [&](uint64_t b, uint64_t e) {
+    for (uint64_t k = b; k < e; ++k) w[k] = std::pow(c->graph.deg[c->part.inv_perm[k]], 0.75);
+  });
+  std::vector<int> prc(c->n, 0);
+  gv::parallel_for(c->n, c->n >= 2 ? std::min<int>(c->threads, static_cast<int>(c->n)) : 1,
+                   [&](uint64_t b, uint64_t e) {
+    for (uint64_t p = b; p < e; ++p)
+      prc[p] = gv::build_alias(w.data() + c->part.off[p], static_cast<uint32_t>(psize(c, p)),
+                               c->nalias.data() + c->part.off[p]);
+  });
+  for (uint32_t p = 0; p < c->n; ++p)
+    if (prc[p]) return fail(c, GV_ERR_EMPTY, "context partition " + std::to_string(p) + " has zero noise mass");
+  lap("negative alias tables");
+  rc = gv::build_walk_tables(c->graph, c->threads, &c->walks);
+  if (rc) return fail(c, static_cast<gv_status>(rc), "departure table has zero mass");
+  c->graph.w.release();  // merged weights: only the alias tables needed them
+  lap("walk alias tables");
   return GV_OK;
 }
 
@@ -1157,77 +1219,128 @@ gv_status gv_load_edges(gv_ctx* c, const uint32_t* src, const uint32_t* dst, con
   if (gv_status s = check_ctx(c, false)) return s;
   if (c->loaded) return fail(c, GV_ERR_STATE, "gv_load_edges called twice");
   if (c->opt.world_size > 1 && !c->comm_ready) return fail(c, GV_ERR_STATE, "gv_comm_init first");
-  if (num_edges && (!src || !dst)) return fail(c, GV_ERR_INVALID_ARG, "null edge arrays");
+  // multi-process: rank 0 prepares the graph once for the node and shares it
+  const bool shared = c->ipc();
+  const bool builder = !shared || c->opt.rank == 0;
+  if (builder && num_edges && (!src || !dst)) return fail(c, GV_ERR_INVALID_ARG, "null edge arrays");
   CK(cudaSetDevice(c->opt.device));
   NvtxRange nv_range("gv:load_edges");
-  std::string msg;
-  int rc = gv::build_graph(c->nv, src, dst, weight, num_edges, c->threads, &c->graph, &msg);
-  if (rc) return fail(c, static_cast<gv_status>(rc), msg);
-  rc = gv::build_partitioning(c->graph, c->n, &c->part, &msg);
-  if (rc) return fail(c, static_cast<gv_status>(rc), msg);
-  // negative tables: deg^0.75 over each partition in local order (P:231, P:392)
-  c->nprob.assign(c->nv, 0);
-  c->nalias.assign(c->nv, 0);
-  std::vector<double> w(c->nv);
-  for (uint32_t k = 0; k < c->nv; ++k) w[k] = std::pow(c->graph.deg[c->part.inv_perm[k]], 0.75);
-  for (uint32_t p = 0; p < c->n; ++p) {
-    const uint64_t b = c->part.off[p];
-    rc = gv::build_alias(w.data() + b, static_cast<uint32_t>(psize(c, p)), c->nprob.data() + b,
-                         c->nalias.data() + b);
-    if (rc) return fail(c, GV_ERR_EMPTY, "context partition " + std::to_string(p) + " has zero noise mass");
+  const bool timing = getenv("GV_INGEST_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[load_edges] %s %.0f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
+  gv::GraphParts parts{&c->graph, &c->part, &c->nalias, &c->walks};
+  if (shared) c->graph_shm_name = c->shm_name + "_graph";
+  if (builder) {
+    gv_status st = prepare_graph(c, src, dst, weight, num_edges, lap);
+    if (st == GV_OK && shared) {
+      std::string msg;
+      if (int rc = gv::graph_share_publish(c->graph_shm_name, parts, &c->graph_map, &msg))
+        st = fail(c, static_cast<gv_status>(rc), msg);
+      lap("publish the node-shared graph");
+    }
+    if (shared) c->shm->graph_state.store(st == GV_OK ? 1 : 2 + st, std::memory_order_release);
+    if (st) return st;
+  } else {
+    // a graph preparation takes minutes on the largest graphs: wait longer
+    if (!gv::ipc_wait(c->shm->graph_state, 1, std::max(c->ipc_timeout, 3600.0)))
+      return fail(c, GV_ERR_COMM, "IPC timeout waiting for rank 0 to prepare the graph");
+    const uint64_t state = c->shm->graph_state.load(std::memory_order_acquire);
+    if (state >= 2)
+      return fail(c, static_cast<gv_status>(state - 2), "rank 0 failed to prepare the graph");
+    c->graph.nv = c->nv;
+    c->part.n = c->n;
+    std::string msg;
+    if (int rc = gv::graph_share_attach(c->graph_shm_name, parts, &c->graph_map, &msg))
+      return fail(c, static_cast<gv_status>(rc), msg);
+    lap("attach the node-shared graph");
   }
-  rc = gv::build_walk_tables(c->graph, c->threads, &c->walks);
-  if (rc) return fail(c, static_cast<gv_status>(rc), "departure table has zero mass");
   gv_status st = setup_device(c);
   if (st) return st;
+  lap("device setup");
   c->loaded = true;
   return GV_OK;
 }
 
-static gv_status push_impl(gv_ctx* c, const uint32_t* pairs, uint64_t count, cudaMemcpyKind kind) {
+// a2, batched transfer ("we transfer the sample block by a small
+// granularity"): pairs are appended to the raw pool in chunks of
+// kPushChunk samples on the copy stream. With host_pool the raw pool itself
+// lives in pinned, mapped host memory (the bucketing kernels read it over
+// PCIe), so edge samples cost no device memory beyond the bucketed blocks.
+constexpr uint64_t kPushChunk = uint64_t(1) << 23;  // 64 MiB of pairs
+
+// Makes room for `count` more pending samples: waits (host) while a
+// prepare holds the pool; orders the copy stream (or, host_pool, the host)
+// after the bucketing kernels that read the buffer last; grows the buffer,
+// keeping the samples already pending. Returns the pending count.
+static gv_status reserve_raw(gv_ctx* c, std::unique_lock<std::mutex>& lk, uint64_t count,
+                             uint64_t* have_out) {
+  c->raw_cv.wait(lk, [&] { return !c->raw_busy; });
+  const uint64_t have = c->raw_count;
+  if (c->opt.max_pool_samples && have + count > c->opt.max_pool_samples)
+    return fail(c, GV_ERR_CAPACITY, "pending pool would exceed max_pool_samples");
+  if (c->raw.host) CK(cudaEventSynchronize(c->raw_free));
+  else CK(cudaStreamWaitEvent(c->copy_stream, c->raw_free, 0));
+  if (have + count > c->raw.cap) {
+    DevBuf<uint2> bigger;
+    bigger.host = c->raw.host;
+    CK(bigger.ensure(std::max<uint64_t>(have + count, c->raw.cap + c->raw.cap / 2)));
+    if (have) CK(cudaMemcpyAsync(bigger.p, c->raw.p, have * sizeof(uint2), cudaMemcpyDefault,
+                                 c->copy_stream));
+    CK(cudaStreamSynchronize(c->copy_stream));
+    c->raw.release();
+    c->raw = bigger;
+  }
+  c->have_last = false;  // the buffer is being refilled: no replay of the last pool
+  *have_out = have;
+  return GV_OK;
+}
+
+static gv_status push_impl(gv_ctx* c, const uint32_t* pairs, uint64_t count, bool from_device) {
   if (gv_status s = check_ctx(c, true)) return s;
   if (count == 0) return GV_OK;
   if (!pairs) return fail(c, GV_ERR_INVALID_ARG, "null pairs");
   CK(cudaSetDevice(c->opt.device));
-  std::lock_guard<std::mutex> lk(c->mu);
-  const int k = c->pending;
-  const uint64_t have = c->raw_count[k];
-  if (c->opt.max_pool_samples && have + count > c->opt.max_pool_samples)
-    return fail(c, GV_ERR_CAPACITY, "pending pool would exceed max_pool_samples");
-  CK(cudaStreamWaitEvent(c->copy_stream, c->raw_free[k], 0));
-  if (have + count > c->raw[k].cap) {
-    // grow, keeping what was already pushed
-    DevBuf<uint2> bigger;
-    CK(bigger.ensure(std::max<uint64_t>(have + count, c->raw[k].cap + c->raw[k].cap / 2)));
-    if (have)
-      CK(cudaMemcpyAsync(bigger.p, c->raw[k].p, have * sizeof(uint2), cudaMemcpyDeviceToDevice,
-                         c->copy_stream));
-    CK(cudaStreamSynchronize(c->copy_stream));
-    c->raw[k].release();
-    c->raw[k] = bigger;
+  std::unique_lock<std::mutex> lk(c->mu);
+  uint64_t have = 0;
+  if (gv_status st = reserve_raw(c, lk, count, &have)) return st;
+  const uint2* src = reinterpret_cast<const uint2*>(pairs);
+  uint2* dst = c->raw.p + have;
+  if (c->raw.host && !from_device) {
+    // host pool: a plain parallel copy into the pinned buffer
+    gv::parallel_for(count, std::min(c->threads, 16), [&](uint64_t b, uint64_t e) {
+      std::memcpy(dst + b, src + b, (e - b) * sizeof(uint2));
+    });
+  } else {
+    for (uint64_t off = 0; off < count; off += kPushChunk)
+      CK(cudaMemcpyAsync(dst + off, src + off, std::min(kPushChunk, count - off) * sizeof(uint2),
+                         cudaMemcpyDefault, c->copy_stream));
   }
-  CK(cudaMemcpyAsync(c->raw[k].p + have, pairs, count * sizeof(uint2), kind, c->copy_stream));
-  CK(cudaEventRecord(c->raw_ready[k], c->copy_stream));
-  CK(cudaStreamSynchronize(c->copy_stream));
-  c->raw_count[k] = have + count;
+  CK(cudaEventRecord(c->raw_ready, c->copy_stream));
+  CK(cudaStreamSynchronize(c->copy_stream));  // the caller may reuse `pairs` on return
+  c->raw_count = have + count;
   return GV_OK;
 }
 
 gv_status gv_push_sample_pool(gv_ctx* c, const uint32_t* pairs, uint64_t count) {
-  return push_impl(c, pairs, count, cudaMemcpyHostToDevice);
+  return push_impl(c, pairs, count, false);
 }
 
 gv_status gv_push_sample_pool_device(gv_ctx* c, const uint32_t* pairs_dev, uint64_t count) {
-  return push_impl(c, pairs_dev, count, cudaMemcpyDeviceToDevice);
+  return push_impl(c, pairs_dev, count, true);
 }
 
 gv_status gv_replay_pool(gv_ctx* c) {
   if (gv_status s = check_ctx(c, true)) return s;
   std::lock_guard<std::mutex> lk(c->mu);
-  if (c->state == PoolState::Prepared || c->last_active < 0 || c->raw_count[c->pending] != 0)
+  if (c->state == PoolState::Prepared || !c->have_last || c->raw_busy || c->raw_count != 0)
     return fail(c, GV_ERR_STATE, "no trained pool to replay, or a pool is pending");
-  c->pending = c->last_active;
-  c->raw_count[c->pending] = c->last_count;
+  c->raw_count = c->last_count;
   return GV_OK;
 }
 
@@ -1364,7 +1477,7 @@ gv_status gv_set_progress(gv_ctx* c, uint64_t pool_index, uint64_t samples_done)
     // the pool counter also numbers the IPC handshake epochs: ranks may only
     // jump to a resumed position together, before their first pool
     std::lock_guard<std::mutex> lk(c->mu);
-    if (c->pool_index != 0 || c->raw_count[0] != 0 || c->raw_count[1] != 0 || c->last_active >= 0)
+    if (c->pool_index != 0 || c->raw_count != 0 || c->have_last)
       return fail(c, GV_ERR_STATE, "multi-process: set progress before the first pool is pushed");
     c->ipc_epoch0 = pool_index;
   }
@@ -1413,43 +1526,27 @@ gv_status gv_augment_device_ex(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_
     CK(cudaMalloc(&c->d_wnbr, sizeof(uint32_t) * std::max<size_t>(ne, 1)));
     CK(cudaMalloc(&c->d_walias, sizeof(uint2) * std::max<size_t>(ne, 1)));
     CK(cudaMalloc(&c->d_dalias, sizeof(uint2) * g.nv));
-    std::vector<uint2> ea(ne), da(g.nv);
-    for (size_t q = 0; q < ne; ++q) ea[q] = make_uint2(c->walks.eprob[q], c->walks.ealias[q]);
-    for (uint32_t q = 0; q < g.nv; ++q)
-      da[q] = make_uint2(c->walks.departure.prob[q], c->walks.departure.alias[q]);
     CK(cudaMemcpy(c->d_woff, g.off.data(), sizeof(uint64_t) * (g.nv + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_wnbr, g.nbr.data(), sizeof(uint32_t) * ne, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->d_walias, ea.data(), sizeof(uint2) * ne, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->d_dalias, da.data(), sizeof(uint2) * g.nv, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_walias, c->walks.edge.data(), sizeof(uint2) * ne, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_dalias, c->walks.departure.data(), sizeof(uint2) * g.nv,
+                  cudaMemcpyHostToDevice));
   }
-  std::lock_guard<std::mutex> lk(c->mu);
-  const int k = c->pending;
-  const uint64_t have = c->raw_count[k];
-  if (c->opt.max_pool_samples && have + count > c->opt.max_pool_samples)
-    return fail(c, GV_ERR_CAPACITY, "pending pool would exceed max_pool_samples");
-  CK(cudaStreamWaitEvent(c->copy_stream, c->raw_free[k], 0));
-  if (have + count > c->raw[k].cap) {
-    DevBuf<uint2> bigger;
-    CK(bigger.ensure(std::max<uint64_t>(have + count, c->raw[k].cap + c->raw[k].cap / 2)));
-    if (have)
-      CK(cudaMemcpyAsync(bigger.p, c->raw[k].p, have * sizeof(uint2), cudaMemcpyDeviceToDevice,
-                         c->copy_stream));
-    CK(cudaStreamSynchronize(c->copy_stream));
-    c->raw[k].release();
-    c->raw[k] = bigger;
-  }
+  std::unique_lock<std::mutex> lk(c->mu);
+  uint64_t have = 0;
+  if (gv_status st = reserve_raw(c, lk, count, &have)) return st;
   gv::WalkDev wd{c->d_woff, c->d_wnbr, c->d_walias, c->d_dalias, c->nv};
   if (shuffle == GV_SHUFFLE_RANDOM) {  // walk order into scratch, then a keyed permutation
     CK(c->shuf_tmp.ensure(count));
     CK(gv::launch_augment(wd, walk_len, s, segments, count, seed, 1, c->shuf_tmp.p,
                           c->copy_stream));
-    CK(gv::launch_random_permute(c->shuf_tmp.p, count, seed, c->raw[k].p + have, c->copy_stream));
+    CK(gv::launch_random_permute(c->shuf_tmp.p, count, seed, c->raw.p + have, c->copy_stream));
   } else {
     CK(gv::launch_augment(wd, walk_len, s, segments, count, seed,
-                          shuffle == GV_SHUFFLE_NONE ? 1 : 0, c->raw[k].p + have, c->copy_stream));
+                          shuffle == GV_SHUFFLE_NONE ? 1 : 0, c->raw.p + have, c->copy_stream));
   }
-  CK(cudaEventRecord(c->raw_ready[k], c->copy_stream));
-  c->raw_count[k] = have + count;
+  CK(cudaEventRecord(c->raw_ready, c->copy_stream));
+  c->raw_count = have + count;
   return GV_OK;
 }
 
@@ -1457,12 +1554,11 @@ gv_status gv_debug_get_pending(gv_ctx* c, uint32_t* out, uint64_t cap, uint64_t*
   if (gv_status st = check_ctx(c, true)) return st;
   CK(cudaSetDevice(c->opt.device));
   std::lock_guard<std::mutex> lk(c->mu);
-  const int k = c->pending;
-  if (count) *count = c->raw_count[k];
+  if (count) *count = c->raw_count;
   if (!out) return GV_OK;
-  if (cap < c->raw_count[k]) return fail(c, GV_ERR_CAPACITY, "cap < pending pool size");
+  if (cap < c->raw_count) return fail(c, GV_ERR_CAPACITY, "cap < pending pool size");
   CK(cudaStreamSynchronize(c->copy_stream));
-  CK(cudaMemcpy(out, c->raw[k].p, sizeof(uint2) * c->raw_count[k], cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out, c->raw.p, sizeof(uint2) * c->raw_count, cudaMemcpyDefault));
   return GV_OK;
 }
 
@@ -1477,15 +1573,19 @@ gv_status gv_get_alias(gv_ctx* c, uint32_t p, uint32_t* prob, uint32_t* alias, u
   if (gv_status s = check_ctx(c, true)) return s;
   if (p == UINT32_MAX) {
     if (cap < c->nv) return fail(c, GV_ERR_CAPACITY, "cap < num_nodes");
-    std::memcpy(prob, c->walks.departure.prob.data(), sizeof(uint32_t) * c->nv);
-    std::memcpy(alias, c->walks.departure.alias.data(), sizeof(uint32_t) * c->nv);
+    for (uint32_t k = 0; k < c->nv; ++k) {
+      prob[k] = c->walks.departure[k].prob;
+      alias[k] = c->walks.departure[k].alias;
+    }
     return GV_OK;
   }
   if (p >= c->n) return fail(c, GV_ERR_INVALID_ARG, "bad partition");
   const uint64_t b = c->part.off[p], sz = psize(c, p);
   if (cap < sz) return fail(c, GV_ERR_CAPACITY, "cap < partition size");
-  std::memcpy(prob, c->nprob.data() + b, sizeof(uint32_t) * sz);
-  std::memcpy(alias, c->nalias.data() + b, sizeof(uint32_t) * sz);
+  for (uint64_t k = 0; k < sz; ++k) {
+    prob[k] = c->nalias[b + k].prob;
+    alias[k] = c->nalias[b + k].alias;
+  }
   return GV_OK;
 }
 
@@ -1596,7 +1696,7 @@ gv_status gv_plan_step(uint32_t n, uint32_t D, uint32_t d, uint32_t t, gv_step_p
 gv_status gv_device_bytes(gv_ctx* c, uint64_t* bytes) {
   if (gv_status s = check_ctx(c, true)) return s;
   uint64_t b = static_cast<uint64_t>(c->nv) * (4 + 8 + 4);
-  b += c->raw[0].bytes_total() + c->raw[1].bytes_total();
+  if (!c->raw.host) b += c->raw.bytes_total();
   for (auto& r : c->ranks) {
     b += (r.vrows + r.crows) * c->stride * 4;
     b += r.blocks.bytes_total() +
@@ -1638,11 +1738,9 @@ void gv_destroy(gv_ctx* c) {
     if (r.compute) cudaStreamDestroy(r.compute);
     if (r.comm) cudaStreamDestroy(r.comm);
   }
-  for (int k = 0; k < 2; ++k) {
-    c->raw[k].release();
-    if (c->raw_ready[k]) cudaEventDestroy(c->raw_ready[k]);
-    if (c->raw_free[k]) cudaEventDestroy(c->raw_free[k]);
-  }
+  c->raw.release();
+  if (c->raw_ready) cudaEventDestroy(c->raw_ready);
+  if (c->raw_free) cudaEventDestroy(c->raw_free);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (auto& g : c->blocks_graveyard) cudaFree(g.first);
   c->blocks_graveyard.clear();
@@ -1671,6 +1769,8 @@ void gv_destroy(gv_ctx* c) {
   for (cudaEvent_t e : c->my_ev_first) if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->my_ev_rot) if (e) cudaEventDestroy(e);
   if (c->shm) gv::ipc_close(c->shm, c->shm_name, false);
+  if (c->opt.rank == 0 && !c->graph_shm_name.empty()) gv::graph_share_unlink(c->graph_shm_name);
+  gv::graph_share_unmap(&c->graph_map);
   delete c;
 }
 

@@ -10,7 +10,6 @@
 #include <cstdlib>
 #include <cmath>
 #include <memory>
-#include <deque>
 #include <numeric>
 
 #include "../../include/gv.h"
@@ -46,26 +45,37 @@ int build_graph(uint32_t nv, const uint32_t* src, const uint32_t* dst, const flo
     *msg = "at most 2^32-1 input edges";
     return GV_ERR_CAPACITY;
   }
-  for (uint64_t k = 0; k < ne; ++k) {
-    if (src[k] >= nv || dst[k] >= nv) {
-      *msg = "edge " + std::to_string(k) + " has a node id >= num_nodes";
-      return GV_ERR_OUT_OF_RANGE;
-    }
-    if (w && (!std::isfinite(w[k]) || w[k] < 0.0f)) {
-      *msg = "edge " + std::to_string(k) + " has a negative or non-finite weight";
-      return GV_ERR_INVALID_ARG;
-    }
-  }
-  // 1) row counts of the symmetrised multigraph (parallel, atomic counters)
+  // 1) validation and row counts of the symmetrised multigraph (parallel;
+  //    atomic counters). The first invalid edge (lowest k) is reported.
   std::vector<std::atomic<uint32_t>> deg_cnt(nv);
   for (auto& x : deg_cnt) x.store(0, std::memory_order_relaxed);
+  std::atomic<uint64_t> bad_range{UINT64_MAX}, bad_weight{UINT64_MAX};
+  auto lower_to = [](std::atomic<uint64_t>& a, uint64_t k) {
+    uint64_t cur = a.load(std::memory_order_relaxed);
+    while (k < cur && !a.compare_exchange_weak(cur, k, std::memory_order_relaxed)) {
+    }
+  };
   parallel_for(ne, threads, [&](uint64_t b, uint64_t e) {
     for (uint64_t k = b; k < e; ++k) {
-      if (src[k] == dst[k]) continue;
-      deg_cnt[src[k]].fetch_add(1, std::memory_order_relaxed);
-      deg_cnt[dst[k]].fetch_add(1, std::memory_order_relaxed);
+      const uint32_t a = src[k], c = dst[k];
+      if (a >= nv || c >= nv) {
+        lower_to(bad_range, k);
+        continue;
+      }
+      if (w && (!std::isfinite(w[k]) || w[k] < 0.0f)) lower_to(bad_weight, k);
+      if (a == c) continue;
+      deg_cnt[a].fetch_add(1, std::memory_order_relaxed);
+      deg_cnt[c].fetch_add(1, std::memory_order_relaxed);
     }
   });
+  if (bad_range.load() != UINT64_MAX || bad_weight.load() != UINT64_MAX) {
+    if (bad_range.load() <= bad_weight.load()) {
+      *msg = "edge " + std::to_string(bad_range.load()) + " has a node id >= num_nodes";
+      return GV_ERR_OUT_OF_RANGE;
+    }
+    *msg = "edge " + std::to_string(bad_weight.load()) + " has a negative or non-finite weight";
+    return GV_ERR_INVALID_ARG;
+  }
   lap("validate + count");
   std::vector<uint64_t> cnt(static_cast<size_t>(nv) + 1, 0);
   for (uint32_t v = 0; v < nv; ++v) cnt[v + 1] = cnt[v] + deg_cnt[v].load(std::memory_order_relaxed);
@@ -81,24 +91,19 @@ int build_graph(uint32_t nv, const uint32_t* src, const uint32_t* dst, const flo
   };
   std::unique_ptr<Ent[]> ent(new Ent[total]);
   {
-    // thread t owns rows [t nv / T, (t+1) nv / T): it scans every edge and
-    // writes only its own rows — no atomics, no shared cache lines, and each
-    // row receives its entries in input order
-    const int T = std::max(1, std::min<int>(threads, 64));
-    std::vector<std::thread> pool;
-    for (int t = 0; t < T; ++t)
-      pool.emplace_back([&, t] {
-        const uint32_t lo = static_cast<uint32_t>(static_cast<uint64_t>(nv) * t / T);
-        const uint32_t hi = static_cast<uint32_t>(static_cast<uint64_t>(nv) * (t + 1) / T);
-        std::vector<uint32_t> fill(hi - lo, 0);
-        for (uint64_t k = 0; k < ne; ++k) {
-          const uint32_t a = src[k], c = dst[k];
-          if (a == c) continue;
-          if (a >= lo && a < hi) ent[cnt[a] + fill[a - lo]++] = Ent{c, static_cast<uint32_t>(k)};
-          if (c >= lo && c < hi) ent[cnt[c] + fill[c - lo]++] = Ent{a, static_cast<uint32_t>(k)};
-        }
-      });
-    for (auto& th : pool) th.join();
+    // parallel over the edges; each entry takes the next slot of its row
+    // (atomic cursor). The order inside a row depends on the thread timing;
+    // the per-row sort below by (column, input index) makes it canonical.
+    std::vector<std::atomic<uint64_t>> cursor(nv);
+    for (uint32_t v = 0; v < nv; ++v) cursor[v].store(cnt[v], std::memory_order_relaxed);
+    parallel_for(ne, threads, [&](uint64_t b, uint64_t e) {
+      for (uint64_t k = b; k < e; ++k) {
+        const uint32_t a = src[k], c = dst[k];
+        if (a == c) continue;
+        ent[cursor[a].fetch_add(1, std::memory_order_relaxed)] = Ent{c, static_cast<uint32_t>(k)};
+        ent[cursor[c].fetch_add(1, std::memory_order_relaxed)] = Ent{a, static_cast<uint32_t>(k)};
+      }
+    });
   }
   lap("scatter");
   // 3) per row: sort by (column, input index) — deterministic whatever the
@@ -208,14 +213,22 @@ int build_partitioning(const HostGraph& g, uint32_t n, Partitioning* p, std::str
 // Integer Vose (R-ALIAS): a_i = trunc(w_i m 2^32 / W); the residual
 // m 2^32 - sum(a) goes to the first maximal a_i; FIFO worklists of
 // under-full (< 2^32) and over-full slots in index order.
-int build_alias(const double* w, uint32_t m, uint32_t* prob, uint32_t* alias) {
+int build_alias(const double* w, uint32_t m, ProbAlias* out) {
   if (m == 0) return GV_ERR_EMPTY;
   double total = 0.0;
   for (uint32_t i = 0; i < m; ++i) total += w[i];
   if (!(total > 0.0)) return GV_ERR_EMPTY;
   constexpr uint64_t kOne = uint64_t(1) << 32;
   const double scale = static_cast<double>(m) * 4294967296.0 / total;
-  std::vector<uint64_t> a(m);
+  // per-thread scratch: the walk tables build one table per node (65.6 M on
+  // the Friendster-shaped graph), so no allocation per table
+  thread_local std::vector<uint64_t> a;
+  thread_local std::vector<uint32_t> under, over;  // FIFO queues: [head, tail)
+  if (a.size() < m) {
+    a.resize(m);
+    under.resize(m);
+    over.resize(m);
+  }
   uint64_t sum = 0;
   uint32_t top = 0;
   for (uint32_t i = 0; i < m; ++i) {
@@ -224,22 +237,29 @@ int build_alias(const double* w, uint32_t m, uint32_t* prob, uint32_t* alias) {
     if (a[i] > a[top]) top = i;
   }
   a[top] += (static_cast<uint64_t>(m) << 32) - sum;
-  std::deque<uint32_t> under, over;
-  for (uint32_t i = 0; i < m; ++i) (a[i] < kOne ? under : over).push_back(i);
-  while (!under.empty() && !over.empty()) {
-    const uint32_t s = under.front();
-    under.pop_front();
-    const uint32_t l = over.front();
-    prob[s] = static_cast<uint32_t>(a[s]);
-    alias[s] = l;
+  uint32_t uh = 0, ut = 0, oh = 0, ot = 0;
+  for (uint32_t i = 0; i < m; ++i) {
+    if (a[i] < kOne) under[ut++] = i;
+    else over[ot++] = i;
+  }
+  while (uh < ut && oh < ot) {
+    const uint32_t s = under[uh++];
+    const uint32_t l = over[oh];
+    out[s] = ProbAlias{static_cast<uint32_t>(a[s]), l};
     a[l] -= kOne - a[s];
     if (a[l] < kOne) {
-      over.pop_front();
-      under.push_back(l);
+      ++oh;
+      under[ut++] = l;  // at most m entries are ever queued: ut <= m
     }
   }
-  for (uint32_t s : under) prob[s] = 0xFFFFFFFFu, alias[s] = s;
-  for (uint32_t l : over) prob[l] = 0xFFFFFFFFu, alias[l] = l;
+  while (uh < ut) {
+    const uint32_t s = under[uh++];
+    out[s] = ProbAlias{0xFFFFFFFFu, s};
+  }
+  while (oh < ot) {
+    const uint32_t l = over[oh++];
+    out[l] = ProbAlias{0xFFFFFFFFu, l};
+  }
   return GV_OK;
 }
 

@@ -52,7 +52,10 @@ bool ipc_wait(const std::atomic<uint64_t>& v, uint64_t target, double timeout_s)
       const double dt =
           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       if (dt > timeout_s) return false;
-      sched_yield();
+      // short waits spin (step handshakes are microseconds apart); long ones
+      // (a peer preparing the graph) sleep instead of burning a core
+      if (dt > 0.01) usleep(100);
+      else sched_yield();
     }
   }
 }

@@ -46,6 +46,7 @@ struct IpcRankShm {
 struct IpcShm {
   std::atomic<uint64_t> magic;
   std::atomic<uint64_t> arrived;
+  std::atomic<uint64_t> graph_state;  // rank 0's shared graph: 0 preparing, 1 ready, 2 + status failed
   IpcRankShm rank[kIpcMaxRanks];
 };
 

@@ -20,11 +20,11 @@ def _graph(nv=2000, ne=10_000, seed=1, wmax=None):
 
 
 def _pair(nv, src, dst, d=16, n=1, K=1, lr0=0.025, total=0, lr_kind=1, vranks=1, ordered=1,
-          seed=5, init_seed=4, neg_weight=5.0):
+          seed=5, init_seed=4, neg_weight=5.0, host_pool=0):
     """(product, oracle) trainers over the same graph and hyper-parameters."""
     p = G.GraphVite(nv, d, n, K, lr0, total_samples=total, lr_kind=lr_kind, seed=seed,
                     init_seed=init_seed, neg_weight=neg_weight, virtual_ranks=vranks,
-                    ordered=ordered)
+                    ordered=ordered, host_pool=host_pool)
     p.load_edges(src, dst)
     o = O.Trainer(nv, d, n, K=K, lr0=lr0, lr_kind=lr_kind, total_samples=total, seed=seed,
                   init_seed=init_seed, neg_weight=neg_weight)
@@ -643,4 +643,39 @@ def test_degenerate_pools_match_oracle(case):
         assert abs(lg - lo) <= 1e-4 * max(abs(lo), 1.0)
     assert_matrix_parity(p.vertex(), o.get("vertex"))
     assert_matrix_parity(p.context(), o.get("context"))
+    p.close()
+
+
+@pytest.mark.parametrize("host_pool,vr", [(0, 1), (1, 1), (1, 2)])
+def test_push_overlapping_training_single_raw_buffer(c1_graph, host_pool, vr):
+    """a2 with ONE raw pool buffer: pool B is pushed right
+    after gv_train_episode(A) returns, while A trains — the push waits only
+    for A's bucketing, so A's blocks are intact and B is not mixed into A.
+    host_pool = 1 keeps the raw pool in pinned, mapped host memory (P:284:
+    no device memory for raw samples; bucketing reads it over PCIe). Ordered
+    mode equals the oracle trained on A then B; replay of A is refused once B
+    is pending; the device-byte count excludes a host pool."""
+    src, dst = c1_graph
+    P = 300_000
+    A = synth.edge_pool(src, dst, P, seed=31)
+    B = synth.edge_pool(src, dst, P, seed=32)
+    p, o = _pair(C1["nv"], src, dst, d=64, n=4, vranks=vr, total=2 * P, host_pool=host_pool)
+    b0 = G.gv_device_bytes(p.ctx)
+    p.push(A)
+    p.train_episode(stats=False)
+    p.push(B)
+    with pytest.raises(G.GVError):
+        p.replay()
+    st_a = p.read_stats()
+    st_b = p.train_episode()
+    assert st_a["samples_global"] == P and st_b["samples_global"] == P and st_b["pool_index"] == 1
+    o.train_pool(A)
+    o.train_pool(B)
+    assert_matrix_parity(p.vertex(), o.get("vertex"), "vertex")
+    assert_matrix_parity(p.context(), o.get("context"), "context")
+    grown = G.gv_device_bytes(p.ctx) - b0  # pool buffers: blocks (+ raw unless host_pool)
+    if host_pool:
+        assert grown < 1.25 * 8 * P + (4 << 20), grown
+    else:
+        assert grown >= 16 * P, grown
     p.close()

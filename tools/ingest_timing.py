@@ -14,8 +14,8 @@ from paper_1903_00757_b200 import gv as G  # noqa: E402
 
 
 def main(name):
-    cfg = bench.CONFIGS[name]
-    bench.CFG.update(cfg)
+    bench.set_config(name)
+    cfg = bench.CFG
     t0 = time.perf_counter()
     src, dst = bench.make_graph()
     print(f"generate {time.perf_counter() - t0:.1f} s", flush=True)
