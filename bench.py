@@ -319,7 +319,13 @@ def measure(args, world, rank, dev, n, *, steps, warmup, e2e=True, pipeline=True
 
     threads = args.threads or max(1, (os.cpu_count() or 16) // max(1, world))
     t0 = time.perf_counter()
-    src, dst = make_graph()
+    if world > 1 and rank != 0:
+        # multi-process: rank 0 prepares the graph once for the node and the
+        # other ranks map it (gv_load_edges, node-shared graph): they need no
+        # edge list (C5's is 14 GB per copy)
+        src = dst = np.empty(0, dtype=np.uint32)
+    else:
+        src, dst = make_graph()
     t_gen = time.perf_counter() - t0
     P = CFG["pool"]
     total_samples = P * n * (warmup + steps + (steps if e2e else 0) + 1)

@@ -7,6 +7,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -25,6 +26,13 @@ struct Header {
   uint64_t off[kArrays];    // byte offset of each array in the segment
   uint64_t count[kArrays];  // elements of each array
 };
+
+// fallback location of segment `name` (a POSIX shm name starts with '/')
+std::string share_file(const std::string& name) {
+  const char* dir = getenv("GV_SHARE_DIR");
+  std::string d = dir && *dir ? dir : "/tmp";
+  return d + "/gv_share" + (name.empty() || name[0] != '/' ? "_" + name : name.substr(1));
+}
 
 size_t align64(size_t x) { return (x + 63) & ~size_t(63); }
 
@@ -75,21 +83,35 @@ int graph_share_publish(const std::string& name, GraphParts p, SharedMapping* ma
     h.count[k] = kSlots[k].count(p);
     at = align64(at + h.count[k] * kSlots[k].elem);
   }
-  const int fd = shm_open(name.c_str(), O_CREAT | O_RDWR | O_TRUNC, 0600);
-  if (fd < 0) {
-    *err = "shm_open failed for the shared graph segment " + name;
-    return GV_ERR_COMM;
-  }
-  if (ftruncate(fd, static_cast<off_t>(at)) != 0) {
+  // POSIX shared memory (tmpfs) when it has room, else a file under
+  // GV_SHARE_DIR (default /tmp): a container's /dev/shm is often 64 MB.
+  // posix_fallocate reserves every page up front, so a full tmpfs is an
+  // error here instead of a SIGBUS while copying.
+  int fd = shm_open(name.c_str(), O_CREAT | O_RDWR | O_TRUNC, 0600);
+  if (fd >= 0 && posix_fallocate(fd, 0, static_cast<off_t>(at)) != 0) {
     close(fd);
     shm_unlink(name.c_str());
-    *err = "cannot size the shared graph segment (host shared memory)";
-    return GV_ERR_NOMEM;
+    fd = -1;
+  }
+  if (fd < 0) {
+    const std::string path = share_file(name);
+    fd = open(path.c_str(), O_CREAT | O_RDWR | O_TRUNC, 0600);
+    if (fd < 0) {
+      *err = "cannot create the shared graph segment (/dev/shm or " + path + ")";
+      return GV_ERR_NOMEM;
+    }
+    if (posix_fallocate(fd, 0, static_cast<off_t>(at)) != 0) {
+      close(fd);
+      unlink(path.c_str());
+      *err = "no room for the shared graph segment (" + std::to_string(at >> 20) +
+             " MiB) in /dev/shm or " + path;
+      return GV_ERR_NOMEM;
+    }
   }
   void* base = mmap(nullptr, at, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
   close(fd);
   if (base == MAP_FAILED) {
-    shm_unlink(name.c_str());
+    graph_share_unlink(name);
     *err = "mmap of the shared graph segment failed";
     return GV_ERR_NOMEM;
   }
@@ -110,7 +132,8 @@ int graph_share_publish(const std::string& name, GraphParts p, SharedMapping* ma
 
 int graph_share_attach(const std::string& name, GraphParts p, SharedMapping* map,
                        std::string* err) {
-  const int fd = shm_open(name.c_str(), O_RDONLY, 0600);
+  int fd = shm_open(name.c_str(), O_RDONLY, 0600);
+  if (fd < 0) fd = open(share_file(name).c_str(), O_RDONLY);
   if (fd < 0) {
     *err = "shm_open failed for the shared graph segment " + name;
     return GV_ERR_COMM;
@@ -146,6 +169,9 @@ void graph_share_unmap(SharedMapping* map) {
   map->bytes = 0;
 }
 
-void graph_share_unlink(const std::string& name) { shm_unlink(name.c_str()); }
+void graph_share_unlink(const std::string& name) {
+  shm_unlink(name.c_str());
+  unlink(share_file(name).c_str());
+}
 
 }  // namespace gv
