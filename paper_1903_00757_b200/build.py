@@ -24,10 +24,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3,-Wall",
           "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
-SOURCES = ["kernels.cu", "engine.cpp", "host_graph.cpp", "augment.cpp", "run.cpp", "ipc.cpp",
-           "graph_share.cpp"]
+SOURCES = ["kernels.cu", "engine.cpp", "transport_local.cpp", "transport_ipc.cpp", "outofcore.cpp",
+           "host_graph.cpp", "augment.cpp", "run.cpp", "ipc.cpp", "graph_share.cpp"]
 HEADERS = ["kernels.cuh", "philox.cuh", "host_graph.hpp", "augment.hpp", "ipc.hpp",
-           "graph_share.hpp"]
+           "graph_share.hpp", "engine.hpp", "transport.hpp"]
 
 
 def _newest_dep():

@@ -1,9 +1,11 @@
-// engine.cpp — context, episode scheduler and C ABI (include/gv.h).
+// engine.cpp — pool preparation, episode scheduler, statistics and the C ABI
+// (include/gv.h). State: engine.hpp; exchanges between ranks: transport.hpp;
+// host-resident partitions: outofcore.cpp.
 //
 // One gv_ctx per process. It drives D ranks of Alg. 3: either
-// the single rank of this process (world_size = D, CUDA-IPC peer memory
-// between processes) or D virtual ranks on this process's GPU
-// (virtual_ranks = D, device copies).
+// the single rank of this process (world_size = D, IpcTransport between
+// processes) or D virtual ranks on this process's GPU (virtual_ranks = D,
+// LocalTransport).
 // Rank d owns vertex partitions [d m, (d+1) m), m = n / D, and at offset
 // step t holds the context window (d m + t + g) mod n, g = 0..m-1. After it
 // trains its first block of step t (context (d m + t) mod n) it sends that
@@ -11,207 +13,40 @@
 // the transfer overlaps the rank's remaining m-1 blocks.
 // With m = 1 this is Alg. 3's train -> rotate -> train ring.
 #include <cuda_runtime.h>
-#include <nvtx3/nvToolsExt.h>
 #include <sys/mman.h>
 
 #include <algorithm>
-#include <cmath>
-#include <atomic>
+#include <array>
 #include <chrono>
-#include <condition_variable>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
-#include <mutex>
 #include <string>
-#include <thread>
 #include <vector>
 
-#include "../../include/gv.h"
-#include "augment.hpp"
-#include "graph_share.hpp"
-#include "host_graph.hpp"
-#include "ipc.hpp"
-#include "kernels.cuh"
+#include "engine.hpp"
+#include "transport.hpp"
+
+using gv::DevBuf;
+using gv::fail;
+using gv::HpMat;
+using gv::PoolState;
+using gv::psize;
+using gv::Rank;
+using gv::elapsed;
+using gv::new_event;
+using gv::NvtxRange;
+using gv::sync_all;
+
+#define CK GV_CK
 
 namespace {
-
 thread_local std::string g_last_error;
-
-// NVTX ranges around the stages (visible in Nsight Systems timelines)
-struct NvtxRange {
-  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
-  ~NvtxRange() { nvtxRangePop(); }
-};
-
-// -------------------------------------------------------------- buffers
-template <class T>
-struct DevBuf {
-  T* p = nullptr;
-  size_t cap = 0;     // elements
-  uint64_t gen = 0;   // bumped by every (re)allocation
-  bool host = false;  // pinned, mapped host memory (kernels read it over PCIe / UVA)
-  size_t bytes_total() const { return cap * sizeof(T); }
-  cudaError_t ensure(size_t n) {
-    if (n <= cap) return cudaSuccess;
-    release();
-    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
-    cudaError_t e = host ? cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable)
-                         : cudaMalloc(&p, bytes);
-    if (e == cudaSuccess) {
-      cap = std::max<size_t>(n, 1);
-      ++gen;
-    } else {
-      p = nullptr;
-    }
-    return e;
-  }
-  void release() {
-    if (p) {
-      if (host) cudaFreeHost(p);
-      else cudaFree(p);
-    }
-    p = nullptr;
-    cap = 0;
-  }
-};
-
-struct Rank {
-  int d = 0;  // global rank index
-  cudaStream_t compute = nullptr, comm = nullptr;
-  float* vertex = nullptr;
-  uint64_t vrow_first = 0, vrows = 0;  // new-id range of the vertex shard
-  float* context = nullptr;
-  uint64_t crows = 0, slot_rows = 0;
-  std::vector<int> slot_of;  // partition -> context slot (D > 1)
-  int free_slot = -1;
-  DevBuf<uint2> blocks;
-  DevBuf<uint8_t> scratch;
-  DevBuf<uint64_t> counts;      // [0, bins]: block_off; [bins+1]: error flag
-  DevBuf<gv::BlockDesc> desc;
-  DevBuf<uint64_t> place_args;  // fused exchange: dst_off[bins] | outs[D] (device pointers)
-  gv::BucketPlan plan{};
-  DevBuf<double> loss;
-  uint64_t* counts_host = nullptr;  // pinned
-  std::vector<uint64_t> local_off;  // this rank's local block_off (bins + 1)
-  std::vector<uint64_t> final_off;  // m*n + 1: layout of blocks (g, j) in `blocks`
-  uint64_t seg_begin = 0, seg_count = 0;
-  // events
-  cudaEvent_t ev_start = nullptr, ev_bucket = nullptr, ev_exch = nullptr, ev_end = nullptr;
-  cudaEvent_t ev_exch_sent = nullptr;
-  std::vector<cudaEvent_t> ev_first_done, ev_recv, ev_sent;  // per step
-  cudaEvent_t ev_last_recv = nullptr;  // rotation into the window of the next pool
-  bool have_last_recv = false;
-  std::vector<cudaEvent_t> ev_sgd;  // pairs (begin, end) per launch
-  int sgd_launches = 0;
-  int kernel_launches = 0;
-  double ms_bucket = 0, ms_exchange = 0, ms_sgd = 0, ms_total = 0;
-};
-
-enum class PoolState { Idle, Prepared };
-
 }  // namespace
 
-// Residency of one matrix (vertex or context) in out-of-core mode.
-struct HpMat {
-  static constexpr int S = 3;  // device slots
-  int part[S] = {-1, -1, -1};  // partition held by each slot
-  bool dirty[S] = {};          // device copy newer than the host copy
-  uint64_t stamp[S] = {};      // last use (LRU)
-  int last_block[S] = {-1, -1, -1};  // last block of this episode using the slot
-  int prev = -1;               // slot of the previous block
-  cudaEvent_t free_[S] = {}, saved[S] = {}, loaded[S] = {};
-  std::vector<cudaEvent_t> part_saved;  // per partition: its last write-back done
-};
-
-struct gv_ctx {
-  // parameters
-  uint32_t nv = 0, dim = 0, n = 1, K = 1;
-  float lr0 = 0.025f;
-  gv_lr_schedule alpha{GV_LR_LINEAR, 1e-4, 0};
-  gv_options opt{};
-  int D = 1;       // total ranks
-  int local = 1;   // ranks driven by this process
-  uint32_t m = 1;  // partitions per rank
-  uint32_t stride = 0;
-  int threads = 1;
-  int sms = 148;
-  uint32_t hot_rows = 0;  // L2 retention: local ids below this are evict_last
-  std::string err;
-  std::mutex err_mu;  // push may fail on a producer thread while the trainer runs
-  bool loaded = false;
-  // graph
-  gv::HostGraph graph;
-  gv::Partitioning part;
-  gv::Arr<gv::ProbAlias> nalias;  // negative tables {prob, alias}, new-id order
-  gv::WalkTables walks;
-  // device copy of the walk tables (gv_augment_device), lazily uploaded
-  uint64_t* d_woff = nullptr;
-  uint32_t* d_wnbr = nullptr;
-  uint2* d_walias = nullptr;
-  uint2* d_dalias = nullptr;
-  DevBuf<uint2> shuf_tmp;  // random-shuffle ablation scratch
-  // shared device tables
-  uint32_t* d_packed = nullptr;
-  uint2* d_alias = nullptr;
-  uint32_t* d_inv_perm = nullptr;
-  // pool (a2): ONE raw buffer. gv_train_episode takes the pending pool out of
-  // it (prepare), and the next push may refill it as soon as the bucketing
-  // kernels have read it (raw_free) — a few ms into the pool's training — so
-  // the H2D copy of pool k+1 still overlaps the SGD of pool k, and device
-  // sample memory is raw + blocks = 2 P (not 3 P as with two raw buffers).
-  std::mutex mu;
-  std::condition_variable raw_cv;
-  bool raw_busy = false;        // prepare has taken the pool, raw_free not yet recorded
-  DevBuf<uint2> raw;
-  uint64_t raw_count = 0;       // pending samples in raw
-  cudaEvent_t raw_ready = nullptr, raw_free = nullptr;
-  bool have_last = false;       // raw still holds the last trained pool (replay)
-  uint64_t last_count = 0;
-  cudaStream_t copy_stream = nullptr;
-  PoolState state = PoolState::Idle;
-  uint64_t pool_P = 0;        // samples of the prepared pool (this process)
-  uint64_t pool_P_global = 0; // all ranks
-  std::vector<uint64_t> global_counts;  // bins (sum over ranks)
-  // progress
-  uint64_t pool_index = 0;
-  uint64_t samples_done = 0;  // global samples trained in earlier steps
-  std::vector<Rank> ranks;
-  bool comm_ready = false;
-  // out-of-core mode (host_partitions): matrices in pinned host memory, three
-  // device slots per matrix; loads (H2D) and write-backs (D2H) run on their
-  // own streams so the two PCIe directions overlap each other and the SGD
-  float* h_vertex = nullptr;
-  float* h_context = nullptr;
-  HpMat hpv, hpc;
-  uint64_t hp_clock = 0;
-  cudaStream_t hp_h2d = nullptr, hp_d2h = nullptr;
-  bool hp() const { return opt.host_partitions != 0; }
-  // CUDA-IPC transport (world_size > 1)
-  gv::IpcShm* shm = nullptr;
-  std::string shm_name;
-  float* peer_ctx[gv::kIpcMaxRanks] = {};
-  uint2* peer_blocks[gv::kIpcMaxRanks] = {};
-  uint64_t peer_blocks_gen[gv::kIpcMaxRanks] = {};
-  cudaEvent_t peer_ev_pull[gv::kIpcMaxRanks][2] = {};
-  cudaEvent_t peer_ev_first[gv::kIpcMaxRanks][gv::kIpcEvRing] = {};
-  cudaEvent_t peer_ev_rot[gv::kIpcMaxRanks][gv::kIpcEvRing] = {};
-  cudaEvent_t my_ev_pull[2] = {};
-  cudaEvent_t my_ev_first[gv::kIpcEvRing] = {};
-  cudaEvent_t my_ev_rot[gv::kIpcEvRing] = {};
-  uint64_t exported_blocks_gen = 0;
-  // receive buffers replaced while peers had them mapped: freed once every
-  // peer has moved past the pool that announced the new handle
-  std::vector<std::pair<uint2*, uint64_t>> blocks_graveyard;  // (ptr, retired at pool e)
-  double ipc_timeout = 300.0;
-  uint64_t ipc_epoch0 = 0;  // pool counter of this session's first pool (gv_set_progress)
-  std::string graph_shm_name;  // node-shared graph segment (rank 0 prepares it)
-  gv::SharedMapping graph_map;
-  bool ipc() const { return opt.world_size > 1; }
-};
-
-namespace {
+namespace gv {
 
 gv_status fail(gv_ctx* c, gv_status s, const std::string& msg) {
   if (c) {
@@ -221,22 +56,6 @@ gv_status fail(gv_ctx* c, gv_status s, const std::string& msg) {
   g_last_error = msg;
   return s;
 }
-
-#define CK(call)                                                                        \
-  do {                                                                                  \
-    cudaError_t e_ = (call);                                                            \
-    if (e_ != cudaSuccess)                                                              \
-      return fail(c, GV_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-
-float lr_at(const gv_ctx* c, uint64_t s_before) {
-  if (c->alpha.kind == GV_LR_CONSTANT || c->alpha.total_samples == 0) return c->lr0;
-  double r = 1.0 - static_cast<double>(s_before) / static_cast<double>(c->alpha.total_samples);
-  if (r < c->alpha.floor_ratio) r = c->alpha.floor_ratio;
-  return static_cast<float>(static_cast<double>(c->lr0) * r);
-}
-
-uint64_t psize(const gv_ctx* c, uint32_t p) { return c->part.off[p + 1] - c->part.off[p]; }
 
 cudaEvent_t new_event(bool timing) {
   cudaEvent_t e = nullptr;
@@ -250,12 +69,6 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-// Context row of local id 0 of partition j on rank r (valid while held).
-uint64_t crow0(const gv_ctx* c, const Rank& r, uint32_t j) {
-  if (c->D == 1) return c->part.off[j];
-  return static_cast<uint64_t>(r.slot_of[j]) * r.slot_rows;
-}
-
 gv_status sync_all(gv_ctx* c) {
   for (auto& r : c->ranks) {
     CK(cudaStreamSynchronize(r.compute));
@@ -265,6 +78,17 @@ gv_status sync_all(gv_ctx* c) {
   if (c->hp_h2d) CK(cudaStreamSynchronize(c->hp_h2d));
   if (c->hp_d2h) CK(cudaStreamSynchronize(c->hp_d2h));
   return GV_OK;
+}
+
+}  // namespace gv
+
+namespace {
+
+float lr_at(const gv_ctx* c, uint64_t s_before) {
+  if (c->alpha.kind == GV_LR_CONSTANT || c->alpha.total_samples == 0) return c->lr0;
+  double r = 1.0 - static_cast<double>(s_before) / static_cast<double>(c->alpha.total_samples);
+  if (r < c->alpha.floor_ratio) r = c->alpha.floor_ratio;
+  return static_cast<float>(static_cast<double>(c->lr0) * r);
 }
 
 // --------------------------------------------------------------- prepare
@@ -277,63 +101,16 @@ gv_status sync_all(gv_ctx* c) {
 gv_status place_fused(gv_ctx* c, const std::vector<std::vector<uint64_t>>& bc) {
   const uint32_t n = c->n, m = c->m, bins = n * n, bpr = m * n;
   const int D = c->D;
-  const uint64_t e = c->pool_index;
   // final layout of every rank's rows (all ranks: sources need the owners')
   std::vector<std::vector<uint64_t>> final_off(D, std::vector<uint64_t>(bpr + 1, 0));
   for (int d = 0; d < D; ++d)
     for (uint32_t q = 0; q < bpr; ++q)
       final_off[d][q + 1] = final_off[d][q] + c->global_counts[d * bpr + q];
-  // receive buffers (headroom: pool sizes fluctuate)
-  for (auto& r : c->ranks) {
-    const uint64_t total = final_off[r.d][bpr];
-    if (total > r.blocks.cap) {
-      if (c->ipc() && r.blocks.p) {  // peers may still map it: retire, free later
-        c->blocks_graveyard.push_back({r.blocks.p, e});
-        r.blocks.p = nullptr;
-        r.blocks.cap = 0;
-      }
-      CK(r.blocks.ensure(total + total / 8));
-    }
-  }
+  // receive buffers, then every rank's, addressable from this process
+  for (auto& r : c->ranks)
+    if (gv_status st = c->tr->reserve_blocks(c, r, final_off[r.d][bpr])) return st;
   std::vector<uint2*> outs(D, nullptr);
-  if (c->ipc()) {
-    Rank& r = c->ranks[0];
-    gv::IpcRankShm& me = c->shm->rank[r.d];
-    if (c->exported_blocks_gen != r.blocks.gen) {  // (re)allocated: export again
-      CK(cudaIpcGetMemHandle(&me.blocks_handle, r.blocks.p));
-      me.blocks_gen = me.blocks_gen + 1;
-      c->exported_blocks_gen = r.blocks.gen;
-    }
-    me.recv_epoch.store(e + 1, std::memory_order_release);
-    for (int q = 0; q < D; ++q) {
-      if (q == r.d) {
-        outs[q] = r.blocks.p;
-        continue;
-      }
-      gv::IpcRankShm& pr = c->shm->rank[q];
-      if (!gv::ipc_wait(pr.recv_epoch, e + 1, c->ipc_timeout))
-        return fail(c, GV_ERR_COMM, "IPC timeout waiting for a peer's receive buffer");
-      if (c->peer_blocks_gen[q] != pr.blocks_gen) {
-        if (c->peer_blocks[q]) CK(cudaIpcCloseMemHandle(c->peer_blocks[q]));
-        void* ptr = nullptr;
-        CK(cudaIpcOpenMemHandle(&ptr, pr.blocks_handle, cudaIpcMemLazyEnablePeerAccess));
-        c->peer_blocks[q] = static_cast<uint2*>(ptr);
-        c->peer_blocks_gen[q] = pr.blocks_gen;
-      }
-      outs[q] = c->peer_blocks[q];
-    }
-    // every peer has moved past the pools that announced newer handles
-    for (auto it = c->blocks_graveyard.begin(); it != c->blocks_graveyard.end();) {
-      if (it->second + 1 < e + 1) {
-        CK(cudaFree(it->first));
-        it = c->blocks_graveyard.erase(it);
-      } else {
-        ++it;
-      }
-    }
-  } else {
-    for (auto& r : c->ranks) outs[r.d] = r.blocks.p;
-  }
+  if (gv_status st = c->tr->scatter_targets(c, outs)) return st;
   for (auto& r : c->ranks) {
     std::vector<uint64_t> args(bins + D);
     for (uint32_t q = 0; q < bins; ++q) {
@@ -355,22 +132,7 @@ gv_status place_fused(gv_ctx* c, const std::vector<std::vector<uint64_t>>& bc) {
     CK(cudaEventRecord(r.ev_exch_sent, r.compute));
   }
   // an owner trains its rows only after every source has placed its samples
-  if (c->ipc()) {
-    Rank& r = c->ranks[0];
-    CK(cudaEventRecord(c->my_ev_pull[e & 1], r.compute));
-    c->shm->rank[r.d].pull_epoch.store(e + 1, std::memory_order_release);
-    for (int q = 0; q < D; ++q) {
-      if (q == r.d) continue;
-      if (!gv::ipc_wait(c->shm->rank[q].pull_epoch, e + 1, c->ipc_timeout))
-        return fail(c, GV_ERR_COMM, "IPC timeout waiting for a peer's scatter");
-      CK(cudaStreamWaitEvent(r.compute, c->peer_ev_pull[q][e & 1], 0));
-    }
-  } else {
-    for (auto& d : c->ranks)
-      for (auto& s2 : c->ranks)
-        if (s2.d != d.d) CK(cudaStreamWaitEvent(d.compute, s2.ev_exch_sent, 0));
-  }
-  return GV_OK;
+  return c->tr->scatter_done(c);
 }
 
 // a3-a6: bucket every local rank's pool segment, exchange block rows.
@@ -447,31 +209,9 @@ gv_status prepare(gv_ctx* c) {
   };
   if (!fused)
     if (gv_status st = release_raw()) return st;
-  // 2) counts to the host (IPC: all-gathered through the shared-memory segment)
+  // 2) counts of every rank to the host (a4)
   std::vector<std::vector<uint64_t>> cnt(c->D, std::vector<uint64_t>(bins + 2, 0));
-  if (c->ipc()) {
-    Rank& r = c->ranks[0];
-    const uint64_t e = c->pool_index;
-    CK(cudaMemcpyAsync(r.counts_host, r.counts.p, sizeof(uint64_t) * (bins + 2),
-                       cudaMemcpyDeviceToHost, r.compute));
-    CK(cudaStreamSynchronize(r.compute));
-    gv::IpcRankShm& me = c->shm->rank[r.d];
-    std::memcpy(me.counts[e & 1], r.counts_host, sizeof(uint64_t) * (bins + 2));
-    me.counts_epoch.store(e + 1, std::memory_order_release);
-    for (int q = 0; q < c->D; ++q) {
-      if (!gv::ipc_wait(c->shm->rank[q].counts_epoch, e + 1, c->ipc_timeout))
-        return fail(c, GV_ERR_COMM, "IPC timeout waiting for a peer's bucket counts");
-      std::memcpy(cnt[q].data(), c->shm->rank[q].counts[e & 1], sizeof(uint64_t) * (bins + 2));
-    }
-  } else {
-    for (auto& r : c->ranks)
-      CK(cudaMemcpyAsync(r.counts_host, r.counts.p, sizeof(uint64_t) * (bins + 2),
-                         cudaMemcpyDeviceToHost, r.compute));
-    for (auto& r : c->ranks) {
-      CK(cudaStreamSynchronize(r.compute));
-      std::copy(r.counts_host, r.counts_host + bins + 2, cnt[r.d].begin());
-    }
-  }
+  if (gv_status st = c->tr->gather_counts(c, cnt)) return st;
   bool bad = false;
   for (int q = 0; q < c->D; ++q) bad |= cnt[q][bins + 1] != 0;
   if (bad) {
@@ -546,77 +286,8 @@ gv_status run_steps(gv_ctx* c) {
   // descriptors: D == 1 -> one launch per step over all n blocks;
   //              D > 1  -> one launch per block (g), so the first block of a
   //              step can release its context partition early.
-  struct HpUse {  // out-of-core: one matrix's slot for a block and the load before it
-    int s, load;       // slot; partition to load into it (-1: resident)
-    bool wait_saved;   // the slot's old contents are written back first
-  };
-  struct HpWb { int mat, s, p; };  // write-back of slot s (partition p) of matrix mat
-  std::vector<HpUse> hp_use[2];          // per position in hp_order
-  std::vector<std::vector<HpWb>> hp_wb;  // hp_wb[k + 1]: write-backs issued after the k-th block
-  std::vector<std::pair<uint32_t, uint32_t>> hp_order;  // (offset step t, vertex partition i)
-  if (c->hp()) {
-    // Block order: Alg. 3 orders blocks by offset step; a block (i, i+t)
-    // depends only on the blocks sharing its rows, (i, i+t-1) and (i+1, i+t)
-    // of step t-1, so any order respecting those edges gives the same result.
-    // Steps are taken in pairs (t, t+1) as A_{n-1}, A_{n-2}, B_{n-2}, ...,
-    // A_0, B_0, B_{n-1} (A_i = (i, i+t), B_i = (i, i+t+1)): B_i shares its
-    // vertex partition with A_i and its context partition with A_{i+1}, so
-    // with three slots per matrix a block loads one partition instead of two.
-    for (uint32_t t = 0; t < n; t += 2) {
-      if (t + 1 == n) {
-        for (uint32_t i = 0; i < n; ++i) hp_order.push_back({t, i});
-        break;
-      }
-      hp_order.push_back({t, n - 1});
-      for (uint32_t i = n - 1; i-- > 0;) {
-        hp_order.push_back({t, i});
-        hp_order.push_back({t + 1, i});
-      }
-      hp_order.push_back({t + 1, n - 1});
-    }
-    // LRU over three slots, never the previous block's slot (it may still
-    // run). A victim's write-back is issued right after its last use, so it
-    // runs during the next block while another slot loads (PCIe duplex).
-    hp_wb.assign(static_cast<size_t>(n) * n + 1, {});
-    HpMat* mats[2] = {&c->hpv, &c->hpc};
-    for (HpMat* M : mats)
-      for (int sl = 0; sl < HpMat::S; ++sl) M->last_block[sl] = -1;
-    for (int mt = 0; mt < 2; ++mt) hp_use[mt].resize(static_cast<size_t>(n) * n);
-    for (size_t k = 0; k < hp_order.size(); ++k) {
-        const uint32_t t = hp_order[k].first, i = hp_order[k].second;
-        const int b = static_cast<int>(k);
-        const int need[2] = {static_cast<int>(i), static_cast<int>((i + t) % n)};
-        for (int mt = 0; mt < 2; ++mt) {
-          HpMat& M = *mats[mt];
-          HpUse& u = hp_use[mt][b];
-          u.s = -1;
-          u.load = -1;
-          u.wait_saved = false;
-          for (int sl = 0; sl < HpMat::S; ++sl)
-            if (M.part[sl] == need[mt]) u.s = sl;
-          if (u.s < 0) {
-            for (int sl = 0; sl < HpMat::S; ++sl)
-              if (sl != M.prev && (u.s < 0 || M.stamp[sl] < M.stamp[u.s])) u.s = sl;
-            if (M.part[u.s] >= 0 && M.dirty[u.s]) {
-              hp_wb[M.last_block[u.s] + 1].push_back({mt, u.s, M.part[u.s]});
-              u.wait_saved = true;
-            }
-            u.load = need[mt];
-            M.part[u.s] = need[mt];
-          }
-          M.dirty[u.s] = true;
-          M.stamp[u.s] = ++c->hp_clock;
-          M.last_block[u.s] = b;
-          M.prev = u.s;
-        }
-      }
-  }
-  std::vector<int> hp_pos;  // position of block (t, i) in hp_order
-  if (c->hp()) {
-    hp_pos.resize(hp_order.size());
-    for (size_t k = 0; k < hp_order.size(); ++k)
-      hp_pos[hp_order[k].first * n + hp_order[k].second] = static_cast<int>(k);
-  }
+  gv::HpPlan hp;  // out-of-core: residency order, slots, loads and write-backs
+  if (c->hp()) gv::hp_plan(c, &hp);
   for (auto& r : c->ranks) {
     std::vector<gv::BlockDesc> desc(static_cast<size_t>(n) * m);
     // slot bookkeeping is simulated here exactly as the rotation will move data
@@ -637,8 +308,8 @@ gv_status run_steps(gv_ctx* c) {
         d.crow0 = static_cast<uint32_t>(c->D == 1 ? c->part.off[j]
                                                   : static_cast<uint64_t>(slot_of[j]) * r.slot_rows);
         if (c->hp()) {
-          d.vrow0 = static_cast<uint32_t>(hp_use[0][hp_pos[t * n + i]].s * r.slot_rows);
-          d.crow0 = static_cast<uint32_t>(hp_use[1][hp_pos[t * n + i]].s * r.slot_rows);
+          d.vrow0 = static_cast<uint32_t>(hp.use[0][hp.pos[t * n + i]].s * r.slot_rows);
+          d.crow0 = static_cast<uint32_t>(hp.use[1][hp.pos[t * n + i]].s * r.slot_rows);
         }
         d.alias0 = static_cast<uint32_t>(c->part.off[j]);
         d.m = static_cast<uint32_t>(psize(c, j));
@@ -699,45 +370,8 @@ gv_status run_steps(gv_ctx* c) {
     // context partitions are loaded into device slots; the load and
     // write-back streams run ahead of the compute stream
     Rank& r = c->ranks[0];
-    const size_t row_bytes = sizeof(float) * c->stride;
-    HpMat* mats[2] = {&c->hpv, &c->hpc};
-    float* devs[2] = {r.vertex, r.context};
-    float* hosts[2] = {c->h_vertex, c->h_context};
-    auto slot_ptr = [&](int mt, int sl) {
-      return devs[mt] + static_cast<uint64_t>(sl) * r.slot_rows * c->stride;
-    };
-    auto write_back = [&](const HpWb& w) -> gv_status {
-      HpMat& M = *mats[w.mat];
-      CK(cudaStreamWaitEvent(c->hp_d2h, M.free_[w.s], 0));
-      CK(cudaMemcpyAsync(hosts[w.mat] + c->part.off[w.p] * c->stride, slot_ptr(w.mat, w.s),
-                         row_bytes * psize(c, w.p), cudaMemcpyDeviceToHost, c->hp_d2h));
-      CK(cudaEventRecord(M.saved[w.s], c->hp_d2h));
-      CK(cudaEventRecord(M.part_saved[w.p], c->hp_d2h));
-      return GV_OK;
-    };
-    for (const HpWb& w : hp_wb[0])  // victims last used in an earlier episode
-      if (gv_status st = write_back(w)) return st;
-    for (size_t k = 0; k < hp_order.size(); ++k) {
-      for (int mt = 0; mt < 2; ++mt) {
-        const HpUse& u = hp_use[mt][k];
-        HpMat& M = *mats[mt];
-        if (u.load >= 0) {
-          CK(cudaStreamWaitEvent(c->hp_h2d, M.free_[u.s], 0));
-          if (u.wait_saved) CK(cudaStreamWaitEvent(c->hp_h2d, M.saved[u.s], 0));
-          // the host copy of the partition is current (a per-partition event:
-          // a slot's own event is re-recorded by later write-backs)
-          CK(cudaStreamWaitEvent(c->hp_h2d, M.part_saved[u.load], 0));
-          CK(cudaMemcpyAsync(slot_ptr(mt, u.s), hosts[mt] + c->part.off[u.load] * c->stride,
-                             row_bytes * psize(c, u.load), cudaMemcpyHostToDevice, c->hp_h2d));
-          CK(cudaEventRecord(M.loaded[u.s], c->hp_h2d));
-        }
-        CK(cudaStreamWaitEvent(r.compute, M.loaded[u.s], 0));
-      }
-      if (gv_status st = launch_blocks(r, hp_order[k].first, hp_order[k].second, 1)) return st;
-      for (int mt = 0; mt < 2; ++mt) CK(cudaEventRecord(mats[mt]->free_[hp_use[mt][k].s], r.compute));
-      for (const HpWb& w : hp_wb[k + 1])
-        if (gv_status st = write_back(w)) return st;
-    }
+    gv_status st = gv::hp_enqueue(c, hp, [&](uint32_t t, uint32_t i) { return launch_blocks(r, t, i, 1); });
+    if (st) return st;
   }
   for (uint32_t t = 0; t < n && !c->hp(); ++t) {
     for (auto& r : c->ranks) {
@@ -759,77 +393,13 @@ gv_status run_steps(gv_ctx* c) {
         if (st) return st;
         if (g == 0) {
           CK(cudaEventRecord(r.ev_first_done[t], r.compute));
-          if (c->ipc()) {  // publish "block 0 of global step gs done" and the slot to pull
-            const uint64_t gs = c->pool_index * n + t;
-            CK(cudaEventRecord(c->my_ev_first[gs % gv::kIpcEvRing], r.compute));
-            gv::IpcRankShm& me = c->shm->rank[r.d];
-            me.first_slot[gs % gv::kIpcSlotRing] = static_cast<uint32_t>(r.slot_of[plan.send_part]);
-            me.first_epoch.store(gs + 1, std::memory_order_release);
-          }
+          if (gv_status st2 = c->tr->first_block_done(c, r, t)) return st2;
         }
       }
     }
     if (c->D == 1) continue;
     // rotation of step t (a8): rank d sends partition (d m + t) to rank d-1
-    if (c->ipc()) {
-      // receiver pulls: rank d copies recv_part out of rank d+1's context slots
-      Rank& r = c->ranks[0];
-      gv_step_plan plan;
-      gv_plan_step(n, c->D, r.d, t, &plan);
-      const uint64_t gs = c->pool_index * n + t;
-      const int src = static_cast<int>(plan.recv_from), prev = static_cast<int>(plan.send_to);
-      gv::IpcRankShm& ps = c->shm->rank[src];
-      if (!gv::ipc_wait(ps.first_epoch, gs + 1, c->ipc_timeout))
-        return fail(c, GV_ERR_COMM, "IPC timeout waiting for the successor's first block");
-      const uint32_t peer_slot = ps.first_slot[gs % gv::kIpcSlotRing];
-      CK(cudaStreamWaitEvent(r.comm, c->peer_ev_first[src][gs % gv::kIpcEvRing], 0));
-      if (gs > c->ipc_epoch0 * n) {  // our free slot was pulled by the predecessor at the previous step
-        if (!gv::ipc_wait(c->shm->rank[prev].rot_epoch, gs, c->ipc_timeout))
-          return fail(c, GV_ERR_COMM, "IPC timeout waiting for the predecessor's rotation");
-        CK(cudaStreamWaitEvent(r.comm, c->peer_ev_rot[prev][(gs - 1) % gv::kIpcEvRing], 0));
-      }
-      const uint32_t out_p = plan.send_part, in_p = plan.recv_part;
-      CK(cudaMemcpyAsync(
-          r.context + static_cast<uint64_t>(r.free_slot) * r.slot_rows * c->stride,
-          c->peer_ctx[src] + static_cast<uint64_t>(peer_slot) * r.slot_rows * c->stride,
-          psize(c, in_p) * c->stride * sizeof(float), cudaMemcpyDeviceToDevice, r.comm));
-      CK(cudaEventRecord(c->my_ev_rot[gs % gv::kIpcEvRing], r.comm));
-      c->shm->rank[r.d].rot_epoch.store(gs + 1, std::memory_order_release);
-      CK(cudaEventRecord(r.ev_recv[t], r.comm));
-      const int s_out = r.slot_of[out_p];
-      r.slot_of[in_p] = r.free_slot;
-      r.slot_of[out_p] = -1;
-      r.free_slot = s_out;
-    } else {
-      // device copies between virtual ranks; slot moves computed first
-      std::vector<int> dst_slot(c->D), src_slot(c->D);
-      std::vector<gv_step_plan> plans(c->D);
-      for (auto& r : c->ranks) {
-        gv_plan_step(n, c->D, r.d, t, &plans[r.d]);
-        src_slot[r.d] = r.slot_of[plans[r.d].send_part];
-        dst_slot[r.d] = r.free_slot;  // where rank r receives
-      }
-      for (auto& r : c->ranks) {
-        Rank& prev = c->ranks[plans[r.d].send_to];
-        const uint32_t out_p = plans[r.d].send_part;
-        CK(cudaStreamWaitEvent(r.comm, r.ev_first_done[t], 0));
-        // prev's free slot was released by prev's own send of step t-1
-        if (t > 0) CK(cudaStreamWaitEvent(r.comm, prev.ev_sent[t - 1], 0));
-        else if (prev.have_last_recv) CK(cudaStreamWaitEvent(r.comm, prev.ev_last_recv, 0));
-        CK(cudaMemcpyAsync(
-            prev.context + static_cast<uint64_t>(dst_slot[prev.d]) * prev.slot_rows * c->stride,
-            r.context + static_cast<uint64_t>(src_slot[r.d]) * r.slot_rows * c->stride,
-            psize(c, out_p) * c->stride * sizeof(float), cudaMemcpyDeviceToDevice, r.comm));
-        CK(cudaEventRecord(r.ev_sent[t], r.comm));
-        CK(cudaEventRecord(prev.ev_recv[t], r.comm));
-      }
-      for (auto& r : c->ranks) {
-        const uint32_t out_p = plans[r.d].send_part, in_p = plans[r.d].recv_part;
-        r.slot_of[in_p] = dst_slot[r.d];
-        r.slot_of[out_p] = -1;
-        r.free_slot = src_slot[r.d];
-      }
-    }
+    if (gv_status st = c->tr->rotate(c, t)) return st;
   }
   for (auto& r : c->ranks) {
     if (c->D > 1) {
@@ -882,7 +452,7 @@ gv_status collect_stats(gv_ctx* c, gv_episode_stats* out) {
   }
   out->ms_rotate = std::max(0.0, out->ms_total - out->ms_bucket - out->ms_exchange - out->ms_sgd);
   // per-rank device times; processes exchange theirs through
-  // the IPC segment, so every rank reports all D ranks and their maximum
+  // the transport, so every rank reports all D ranks and their maximum
   out->n_ranks = static_cast<uint32_t>(c->D);
   auto put = [&](int d, const double* v) {
     out->ms_total_rank[d] = v[0];
@@ -891,26 +461,12 @@ gv_status collect_stats(gv_ctx* c, gv_episode_stats* out) {
     out->ms_sgd_rank[d] = v[3];
     out->ms_rotate_rank[d] = v[4];
   };
-  for (auto& r : c->ranks) {
-    const double v[5] = {r.ms_total, r.ms_bucket, r.ms_exchange, r.ms_sgd,
-                         std::max(0.0, r.ms_total - r.ms_bucket - r.ms_exchange - r.ms_sgd)};
-    put(r.d, v);
-    if (c->ipc()) {
-      const uint64_t e = c->pool_index - 1;
-      gv::IpcRankShm& me = c->shm->rank[r.d];
-      std::memcpy(me.stats[e % gv::kIpcStatRing], v, sizeof(v));
-      me.stats_epoch.store(e + 1, std::memory_order_release);
-      for (int q = 0; q < c->D; ++q) {
-        if (q == r.d) continue;
-        gv::IpcRankShm& pr = c->shm->rank[q];
-        if (!gv::ipc_wait(pr.stats_epoch, e + 1, c->ipc_timeout))
-          return fail(c, GV_ERR_COMM, "IPC timeout waiting for a peer's pool statistics");
-        double pv[5];
-        std::memcpy(pv, pr.stats[e % gv::kIpcStatRing], sizeof(pv));
-        put(q, pv);
-      }
-    }
-  }
+  std::vector<std::array<double, 5>> v(c->D, std::array<double, 5>{});
+  for (auto& r : c->ranks)
+    v[r.d] = {r.ms_total, r.ms_bucket, r.ms_exchange, r.ms_sgd,
+              std::max(0.0, r.ms_total - r.ms_bucket - r.ms_exchange - r.ms_sgd)};
+  if (gv_status st2 = c->tr->exchange_stats(c, v)) return st2;
+  for (int d = 0; d < c->D; ++d) put(d, v[d].data());
   for (int d = 0; d < c->D; ++d) out->ms_device_max = std::max(out->ms_device_max, out->ms_total_rank[d]);
   return GV_OK;
 }
@@ -938,41 +494,8 @@ gv_status setup_device(gv_ctx* c) {
     r.vrow_first = c->part.off[r.d * m];
     r.vrows = c->part.off[(r.d + 1) * m] - r.vrow_first;
     if (c->hp()) {
-      // out-of-core: host arrays in relabelled order, two device slots each
-      const size_t hbytes = sizeof(float) * static_cast<size_t>(nv) * c->stride;
-      CK(cudaHostAlloc(&c->h_vertex, hbytes, cudaHostAllocDefault));
-      CK(cudaHostAlloc(&c->h_context, hbytes, cudaHostAllocDefault));
-      std::memset(c->h_context, 0, hbytes);
-      r.slot_rows = max_part;
-      r.vrows = HpMat::S * max_part;
-      r.crows = HpMat::S * max_part;
-      CK(cudaMalloc(&r.vertex, sizeof(float) * r.vrows * c->stride));
-      CK(cudaMalloc(&r.context, sizeof(float) * r.crows * c->stride));
-      CK(cudaMemset(r.vertex, 0, sizeof(float) * r.vrows * c->stride));
-      for (uint32_t p = 0; p < n; ++p) {  // Philox init partition by partition
-        CK(gv::launch_init_vertex(r.vertex, c->stride, c->dim, c->part.off[p], psize(c, p),
-                                  c->d_inv_perm, key0, key1, r.compute));
-        CK(cudaMemcpyAsync(c->h_vertex + c->part.off[p] * c->stride, r.vertex,
-                           sizeof(float) * psize(c, p) * c->stride, cudaMemcpyDeviceToHost,
-                           r.compute));
-        CK(cudaStreamSynchronize(r.compute));
-      }
-      CK(cudaStreamCreateWithFlags(&c->hp_h2d, cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&c->hp_d2h, cudaStreamNonBlocking));
-      for (HpMat* M : {&c->hpv, &c->hpc}) {
-        M->part_saved.resize(n);
-        for (cudaEvent_t& e : M->part_saved) {
-          e = new_event(false);
-          CK(cudaEventRecord(e, r.compute));
-        }
-        for (int k = 0; k < HpMat::S; ++k) {
-          for (cudaEvent_t* e : {&M->free_[k], &M->saved[k], &M->loaded[k]}) {
-            *e = new_event(false);
-            CK(cudaEventRecord(*e, r.compute));
-          }
-        }
-      }
-      r.vrow_first = 0;
+      // out-of-core: host arrays in relabelled order, device slots
+      if (gv_status st = gv::hp_setup(c, r)) return st;
     } else {
     CK(cudaMalloc(&r.vertex, sizeof(float) * std::max<uint64_t>(r.vrows, 1) * c->stride));
     CK(cudaMemsetAsync(r.vertex, 0, sizeof(float) * r.vrows * c->stride, r.compute));
@@ -1010,46 +533,8 @@ gv_status setup_device(gv_ctx* c) {
     r.ev_exch_sent = new_event(false);
   }
   gv_status st = sync_all(c);
-  if (st || !c->ipc()) return st;
-  // IPC transport: export the context buffer and the events, map the peers'
-  Rank& r = c->ranks[0];
-  gv::IpcRankShm& me = c->shm->rank[r.d];
-  const unsigned fl = cudaEventInterprocess | cudaEventDisableTiming;
-  for (int k = 0; k < 2; ++k) {
-    CK(cudaEventCreateWithFlags(&c->my_ev_pull[k], fl));
-    CK(cudaIpcGetEventHandle(&me.ev_pull[k], c->my_ev_pull[k]));
-  }
-  for (int k = 0; k < gv::kIpcEvRing; ++k) {
-    CK(cudaEventCreateWithFlags(&c->my_ev_first[k], fl));
-    CK(cudaEventCreateWithFlags(&c->my_ev_rot[k], fl));
-    CK(cudaIpcGetEventHandle(&me.ev_first[k], c->my_ev_first[k]));
-    CK(cudaIpcGetEventHandle(&me.ev_rot[k], c->my_ev_rot[k]));
-  }
-  CK(cudaIpcGetMemHandle(&me.ctx_handle, r.context));
-  me.joined.store(1, std::memory_order_release);
-  for (int q = 0; q < c->D; ++q) {
-    if (!gv::ipc_wait(c->shm->rank[q].joined, 1, c->ipc_timeout))
-      return fail(c, GV_ERR_COMM, "IPC timeout waiting for the peers to load the graph");
-    if (q == r.d) continue;
-    gv::IpcRankShm& pr = c->shm->rank[q];
-    void* ptr = nullptr;
-    CK(cudaIpcOpenMemHandle(&ptr, pr.ctx_handle, cudaIpcMemLazyEnablePeerAccess));
-    c->peer_ctx[q] = static_cast<float*>(ptr);
-    for (int k = 0; k < 2; ++k) CK(cudaIpcOpenEventHandle(&c->peer_ev_pull[q][k], pr.ev_pull[k]));
-    for (int k = 0; k < gv::kIpcEvRing; ++k) {
-      CK(cudaIpcOpenEventHandle(&c->peer_ev_first[q][k], pr.ev_first[k]));
-      CK(cudaIpcOpenEventHandle(&c->peer_ev_rot[q][k], pr.ev_rot[k]));
-    }
-  }
-  me.joined.store(2, std::memory_order_release);
-  if (r.d == 0) {  // everyone mapped everything: the name is no longer needed
-    for (int q = 0; q < c->D; ++q)
-      if (!gv::ipc_wait(c->shm->rank[q].joined, 2, c->ipc_timeout))
-        return fail(c, GV_ERR_COMM, "IPC timeout in the init handshake");
-    shm_unlink(c->shm_name.c_str());
-    gv::graph_share_unlink(c->graph_shm_name);
-  }
-  return GV_OK;
+  if (st) return st;
+  return c->tr->connect(c);
 }
 
 // Graph preparation (gv_load_edges): ingest (R-INGEST), zig-zag partition
@@ -1184,12 +669,12 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
   if (const char* e = getenv("GV_HOT_ROWS")) c->hot_rows = static_cast<uint32_t>(atol(e));
   c->ranks.resize(c->local);
   for (int v = 0; v < c->local; ++v) c->ranks[v].d = (o.world_size > 1) ? o.rank : v;
+  if (o.world_size == 1) c->tr = gv::make_local_transport();  // processes: gv_comm_init
   *out = c;
   return GV_OK;
 }
 
 gv_status gv_comm_unique_id(uint8_t id_out[128]) {
-  gv_ctx* c = nullptr;
   FILE* f = fopen("/dev/urandom", "rb");
   if (!f || fread(id_out, 1, 128, f) != 128) {
     if (f) fclose(f);
@@ -1202,26 +687,18 @@ gv_status gv_comm_unique_id(uint8_t id_out[128]) {
 gv_status gv_comm_init(gv_ctx* c, const uint8_t id[128]) {
   if (gv_status s = check_ctx(c, false)) return s;
   if (c->opt.world_size <= 1) return fail(c, GV_ERR_STATE, "gv_comm_init needs world_size > 1");
-  if (c->loaded || c->comm_ready) return fail(c, GV_ERR_STATE, "call gv_comm_init before gv_load_edges, once");
+  if (c->loaded || c->tr) return fail(c, GV_ERR_STATE, "call gv_comm_init before gv_load_edges, once");
   CK(cudaSetDevice(c->opt.device));
-  if (c->D > gv::kIpcMaxRanks || c->n * c->n + 2 > static_cast<uint32_t>(gv::kIpcMaxBins))
-    return fail(c, GV_ERR_INVALID_ARG, "IPC transport: at most 16 ranks and 64 partitions");
-  std::string err;
-  c->shm = gv::ipc_open(id, &c->shm_name, &err);
-  if (!c->shm) return fail(c, GV_ERR_COMM, err);
-  if (const char* t = getenv("GV_IPC_TIMEOUT")) c->ipc_timeout = atof(t);
-  c->comm_ready = true;
-  return GV_OK;
+  return gv::make_ipc_transport(c, id, &c->tr);
 }
 
 gv_status gv_load_edges(gv_ctx* c, const uint32_t* src, const uint32_t* dst, const float* weight,
                         uint64_t num_edges) {
   if (gv_status s = check_ctx(c, false)) return s;
   if (c->loaded) return fail(c, GV_ERR_STATE, "gv_load_edges called twice");
-  if (c->opt.world_size > 1 && !c->comm_ready) return fail(c, GV_ERR_STATE, "gv_comm_init first");
+  if (!c->tr) return fail(c, GV_ERR_STATE, "gv_comm_init first");
   // multi-process: rank 0 prepares the graph once for the node and shares it
-  const bool shared = c->ipc();
-  const bool builder = !shared || c->opt.rank == 0;
+  const bool builder = !c->ipc() || c->opt.rank == 0;
   if (builder && num_edges && (!src || !dst)) return fail(c, GV_ERR_INVALID_ARG, "null edge arrays");
   CK(cudaSetDevice(c->opt.device));
   NvtxRange nv_range("gv:load_edges");
@@ -1234,33 +711,10 @@ gv_status gv_load_edges(gv_ctx* c, const uint32_t* src, const uint32_t* dst, con
             std::chrono::duration<double, std::milli>(now - t_last).count());
     t_last = now;
   };
-  gv::GraphParts parts{&c->graph, &c->part, &c->nalias, &c->walks};
-  if (shared) c->graph_shm_name = c->shm_name + "_graph";
-  if (builder) {
-    gv_status st = prepare_graph(c, src, dst, weight, num_edges, lap);
-    if (st == GV_OK && shared) {
-      std::string msg;
-      if (int rc = gv::graph_share_publish(c->graph_shm_name, parts, &c->graph_map, &msg))
-        st = fail(c, static_cast<gv_status>(rc), msg);
-      lap("publish the node-shared graph");
-    }
-    if (shared) c->shm->graph_state.store(st == GV_OK ? 1 : 2 + st, std::memory_order_release);
-    if (st) return st;
-  } else {
-    // a graph preparation takes minutes on the largest graphs: wait longer
-    if (!gv::ipc_wait(c->shm->graph_state, 1, std::max(c->ipc_timeout, 3600.0)))
-      return fail(c, GV_ERR_COMM, "IPC timeout waiting for rank 0 to prepare the graph");
-    const uint64_t state = c->shm->graph_state.load(std::memory_order_acquire);
-    if (state >= 2)
-      return fail(c, static_cast<gv_status>(state - 2), "rank 0 failed to prepare the graph");
-    c->graph.nv = c->nv;
-    c->part.n = c->n;
-    std::string msg;
-    if (int rc = gv::graph_share_attach(c->graph_shm_name, parts, &c->graph_map, &msg))
-      return fail(c, static_cast<gv_status>(rc), msg);
-    lap("attach the node-shared graph");
-  }
-  gv_status st = setup_device(c);
+  gv_status st = c->tr->load_graph(c, [&] { return prepare_graph(c, src, dst, weight, num_edges, lap); });
+  if (st) return st;
+  lap(builder ? "graph ready" : "attach the node-shared graph");
+  st = setup_device(c);
   if (st) return st;
   lap("device setup");
   c->loaded = true;
@@ -1385,29 +839,7 @@ static gv_status embeddings_io(gv_ctx* c, bool context, float* out, const float*
   gv_status st = sync_all(c);
   if (st) return st;
   const uint32_t dim = c->dim, stride = c->stride, m = c->m;
-  if (c->hp()) {
-    // out-of-core: flush the resident (dirty) partitions, then use the host copy
-    Rank& r = c->ranks[0];
-    float* host = context ? c->h_context : c->h_vertex;
-    float* dev = context ? r.context : r.vertex;
-    HpMat& M = context ? c->hpc : c->hpv;
-    for (int sl = 0; sl < HpMat::S; ++sl) {
-      const int p = M.part[sl];
-      if (p < 0) continue;
-      float* slot = dev + static_cast<uint64_t>(sl) * r.slot_rows * stride;
-      if (out && M.dirty[sl])
-        CK(cudaMemcpy(host + c->part.off[p] * stride, slot, sizeof(float) * psize(c, p) * stride,
-                      cudaMemcpyDeviceToHost));
-      M.dirty[sl] = false;
-      if (!out) M.part[sl] = -1;  // overwritten below: drop the device copy
-    }
-    for (uint32_t id = 0; id < c->nv; ++id) {
-      const uint64_t o = static_cast<uint64_t>(c->part.inv_perm[id]) * dim;
-      if (out) std::memcpy(out + o, host + static_cast<uint64_t>(id) * stride, dim * sizeof(float));
-      else std::memcpy(host + static_cast<uint64_t>(id) * stride, in + o, dim * sizeof(float));
-    }
-    return GV_OK;
-  }
+  if (c->hp()) return gv::hp_embeddings_io(c, context, out, in);
   std::vector<float> buf;
   for (auto& r : c->ranks) {
     // list of (device base row, first new id, rows)
@@ -1473,14 +905,8 @@ gv_status gv_get_progress(gv_ctx* c, uint64_t* pool_index, uint64_t* samples_don
 gv_status gv_set_progress(gv_ctx* c, uint64_t pool_index, uint64_t samples_done) {
   if (gv_status s = check_ctx(c, false)) return s;
   if (c->state == PoolState::Prepared) return fail(c, GV_ERR_STATE, "a prepared pool is pending");
-  if (c->ipc()) {
-    // the pool counter also numbers the IPC handshake epochs: ranks may only
-    // jump to a resumed position together, before their first pool
-    std::lock_guard<std::mutex> lk(c->mu);
-    if (c->pool_index != 0 || c->raw_count != 0 || c->have_last)
-      return fail(c, GV_ERR_STATE, "multi-process: set progress before the first pool is pushed");
-    c->ipc_epoch0 = pool_index;
-  }
+  if (c->tr)
+    if (gv_status st = c->tr->set_progress(c, pool_index)) return st;
   c->pool_index = pool_index;
   c->samples_done = samples_done;
   return GV_OK;
@@ -1714,16 +1140,7 @@ void gv_destroy(gv_ctx* c) {
     if (r.comm) cudaStreamSynchronize(r.comm);
   }
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
-  if (c->ipc() && c->shm && !c->ranks.empty()) {
-    // Peers pull context partitions out of this rank's exported buffer (the
-    // last rotation of a pool lands on the peer's stream after our first
-    // block of that step): free it only once every peer has drained its own
-    // streams, which it announces here after its synchronisation above.
-    c->shm->rank[c->ranks[0].d].closed.store(1, std::memory_order_release);
-    for (int q = 0; q < c->D; ++q)
-      if (!gv::ipc_wait(c->shm->rank[q].closed, 1, c->ipc_timeout))
-        fprintf(stderr, "gv_destroy: rank %d did not close within the IPC timeout\n", q);
-  }
+  if (c->tr) c->tr->close(c);  // peers may read this rank's exported memory until here
   for (auto& r : c->ranks) {
     cudaFree(r.vertex);
     cudaFree(r.context);
@@ -1742,18 +1159,7 @@ void gv_destroy(gv_ctx* c) {
   if (c->raw_ready) cudaEventDestroy(c->raw_ready);
   if (c->raw_free) cudaEventDestroy(c->raw_free);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
-  for (auto& g : c->blocks_graveyard) cudaFree(g.first);
-  c->blocks_graveyard.clear();
-  if (c->h_vertex) cudaFreeHost(c->h_vertex);
-  if (c->h_context) cudaFreeHost(c->h_context);
-  if (c->hp_h2d) cudaStreamDestroy(c->hp_h2d);
-  if (c->hp_d2h) cudaStreamDestroy(c->hp_d2h);
-  for (HpMat* M : {&c->hpv, &c->hpc})
-    for (int k = 0; k < HpMat::S; ++k)
-      for (cudaEvent_t e : {M->free_[k], M->saved[k], M->loaded[k]})
-        if (e) cudaEventDestroy(e);
-  for (HpMat* M : {&c->hpv, &c->hpc})
-    for (cudaEvent_t e : M->part_saved) cudaEventDestroy(e);
+  gv::hp_destroy(c);
   cudaFree(c->d_packed);
   cudaFree(c->d_alias);
   cudaFree(c->d_woff);
@@ -1761,15 +1167,6 @@ void gv_destroy(gv_ctx* c) {
   cudaFree(c->d_walias);
   cudaFree(c->d_dalias);
   cudaFree(c->d_inv_perm);
-  for (int q = 0; q < gv::kIpcMaxRanks; ++q) {
-    if (c->peer_ctx[q]) cudaIpcCloseMemHandle(c->peer_ctx[q]);
-    if (c->peer_blocks[q]) cudaIpcCloseMemHandle(c->peer_blocks[q]);
-  }
-  for (cudaEvent_t e : c->my_ev_pull) if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : c->my_ev_first) if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : c->my_ev_rot) if (e) cudaEventDestroy(e);
-  if (c->shm) gv::ipc_close(c->shm, c->shm_name, false);
-  if (c->opt.rank == 0 && !c->graph_shm_name.empty()) gv::graph_share_unlink(c->graph_shm_name);
   gv::graph_share_unmap(&c->graph_map);
   delete c;
 }
