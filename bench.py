@@ -79,6 +79,10 @@ def parse():
     ap.add_argument("--ordered", action="store_true", help="ordered verification kernel (slow)")
     ap.add_argument("--host-partitions", type=int, default=0,
                     help="out-of-core (NEXT-3): n host-resident partitions on one GPU")
+    ap.add_argument("--pool-ids", default="relabeled", choices=["relabeled", "original"],
+                    help="id space of the pools the samplers write (gv_options.pool_ids): "
+                         "relabeled (default; a3 needs no relabel gather, and at n = 1 the "
+                         "pool is trained where it lies) or the caller's original ids")
     ap.add_argument("--host-pool", action="store_true",
                     help="raw pool in pinned host memory (P:284), read over PCIe by bucketing")
     ap.add_argument("--parts-per-rank", type=int, default=0,
@@ -333,7 +337,8 @@ def measure(args, world, rank, dev, n, *, steps, warmup, e2e=True, pipeline=True
                     neg_weight=CFG["neg_weight"], seed=CFG["seed"],
                     device=dev, rank=rank, world_size=world, ordered=1 if args.ordered else 0,
                     virtual_ranks=args.vranks, host_partitions=1 if args.host_partitions else 0,
-                    host_pool=1 if args.host_pool else 0)
+                    host_pool=1 if args.host_pool else 0,
+                    pool_ids=G.GV_IDS_RELABELED if args.pool_ids == "relabeled" else G.GV_IDS_ORIGINAL)
     if world > 1:
         uid = [G.gv_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -550,7 +555,7 @@ def run_ours(args):
                                   "lr0": CFG["lr"], "neg_weight": CFG["neg_weight"],
                                   "seed": CFG["seed"], "lr_schedule": "linear, floor 1e-4"},
                        "host_partitions": bool(args.host_partitions),
-                       "host_pool": bool(args.host_pool),
+                       "host_pool": bool(args.host_pool), "pool_ids": args.pool_ids,
                        "mode": "ordered" if args.ordered else "hogwild"},
             "roofline": r["roofline"], "cpu_baseline": cpu, "cpu_hogwild": cpu_hog,
             "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "clocks": r["clocks"],

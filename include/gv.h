@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define GV_ABI_VERSION 2
+#define GV_ABI_VERSION 3
 
 typedef struct gv_ctx gv_ctx; /* opaque; owned by the library */
 
@@ -112,7 +112,22 @@ typedef struct {
                              device memory only as bucketed blocks ("the
                              memory cost of edge samples on GPUs becomes
                              negligible"). 0 (default) = raw pool in HBM. */
+  int pool_ids;           /* id space of sample pools (pushed, and written by
+                             gv_augment / gv_augment_device / gv_run):
+                             GV_IDS_ORIGINAL (default) = the caller's node ids;
+                             GV_IDS_RELABELED = the library's relabelled ids,
+                             new = perm[orig] of gv_get_partition (zig-zag order,
+                             R-ZIGZAG). With relabelled ids a3 needs no relabel
+                             gather; at n_partitions = 1 (one rank, HBM pool) a3
+                             is the range check alone and the pool is trained
+                             where it lies — the raw buffer and the block buffer
+                             swap roles ("skipped (identity) at
+                             n = 1 with relabeled input"). Same samples, same
+                             training; only the ids' encoding differs. */
 } gv_options;
+
+#define GV_IDS_ORIGINAL 0
+#define GV_IDS_RELABELED 1
 
 #define GV_MAX_RANKS 64
 
@@ -199,14 +214,16 @@ gv_status gv_comm_init(gv_ctx* ctx, const uint8_t id[128]);
 gv_status gv_load_edges(gv_ctx* ctx, const uint32_t* src, const uint32_t* dst,
                         const float* weight, uint64_t num_edges);
 
-/* Append count edge samples (pairs[2k], pairs[2k+1]) = (u, v), ORIGINAL ids,
- * to the pending pool (Alg. 2's concatenated pool). Copies before
+/* Append count edge samples (pairs[2k], pairs[2k+1]) = (u, v), ORIGINAL ids
+ * (relabelled ids when gv_options.pool_ids = GV_IDS_RELABELED), to the pending pool (Alg. 2's concatenated pool). Copies before
  * returning, in chunks of 2^23 samples on the library's copy stream (batched
  * transfer); a pinned source buffer is copied by DMA at PCIe speed.
  * The library keeps ONE raw pool buffer: a push issued after
  * gv_train_episode(pool k) waits only until pool k has been bucketed (a few
  * ms into its training), then copies while pool k trains — device sample
  * memory is 2 x 8 B per sample (raw + blocks), or 8 B with host_pool = 1.
+ * (Relabelled ids at n = 1: the two buffers alternate; a push waits until
+ * the pool trained before the last one has finished.)
  * With virtual_ranks = D the whole pool is pushed and rank r trains on the
  * contiguous segment [r*P/D, (r+1)*P/D); with world_size = D each process
  * pushes its own segment. Ids are range-checked on the device at
@@ -277,7 +294,8 @@ gv_status gv_get_stream(gv_ctx* ctx, int vrank, uintptr_t* stream_out);
  * each filled by random walks of walk_len edges from departures drawn
  * proportional to degree, pairs (w_a, w_b) with 0 < b-a <= s and w_a != w_b,
  * pseudo-shuffled into s sub-blocks, segments concatenated.
- * Writes exactly `count` pairs (ORIGINAL ids) to out_pairs[2*count].
+ * Writes exactly `count` pairs (ORIGINAL ids, or relabelled ids when
+ * gv_options.pool_ids = GV_IDS_RELABELED) to out_pairs[2*count].
  * Deterministic given (seed, threads): walks draw from a Philox stream with
  * counter (walk, step, thread, 0x57414C4B) and key = seed (SURVEY §8(c),
  * reading R-AUG in DESIGN.md).

@@ -65,7 +65,7 @@ inline uint32_t draw(const ProbAlias* t, uint32_t m, const u32x4& r) {
 constexpr uint32_t kBatch = 16;
 
 void fill_segment(const WalkTables& t, uint32_t walk_len, uint32_t s, uint32_t thread,
-                  uint64_t cap, uint64_t seed, uint32_t* out) {
+                  uint64_t cap, uint64_t seed, const uint32_t* relabel, uint32_t* out) {
   const HostGraph& g = *t.g;
   const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
   const uint32_t W = walk_len + 1;
@@ -108,6 +108,10 @@ void fill_segment(const WalkTables& t, uint32_t walk_len, uint32_t s, uint32_t t
         __builtin_prefetch(off + x);
       }
     }
+    if (relabel) {  // pairs in the pool's id space (a bijection: w_a != w_b is unchanged)
+      for (uint32_t q = 0; q < kBatch * W; ++q) __builtin_prefetch(relabel + walks[q]);
+      for (uint32_t q = 0; q < kBatch * W; ++q) walks[q] = relabel[walks[q]];
+    }
     // pairs within distance s, walk by walk, by increasing start then end position
     for (uint32_t i = 0; i < kBatch && filled < cap; ++i) {
       const uint32_t* walk = walks.data() + static_cast<size_t>(i) * W;
@@ -128,13 +132,14 @@ void fill_segment(const WalkTables& t, uint32_t walk_len, uint32_t s, uint32_t t
 }  // namespace
 
 void augment(const WalkTables& t, uint32_t walk_len, uint32_t s, uint32_t threads,
-             uint64_t count, uint64_t seed, uint32_t* out) {
+             uint64_t count, uint64_t seed, uint32_t* out, const uint32_t* relabel) {
   std::vector<std::thread> pool;
   for (uint32_t th = 0; th < threads; ++th) {
     const uint64_t b = static_cast<uint64_t>((static_cast<unsigned __int128>(count) * th) / threads);
     const uint64_t e =
         static_cast<uint64_t>((static_cast<unsigned __int128>(count) * (th + 1)) / threads);
-    pool.emplace_back(fill_segment, std::cref(t), walk_len, s, th, e - b, seed, out + 2 * b);
+    pool.emplace_back(fill_segment, std::cref(t), walk_len, s, th, e - b, seed, relabel,
+                      out + 2 * b);
   }
   for (auto& x : pool) x.join();
 }

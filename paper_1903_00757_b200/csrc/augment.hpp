@@ -17,8 +17,9 @@ struct WalkTables {
 int build_walk_tables(const HostGraph& g, int threads, WalkTables* t);
 
 // Fills out[2*count] with `threads` pseudo-shuffled walk segments (R-AUG).
-// Thread t owns [count*t/threads, count*(t+1)/threads).
+// Thread t owns [count*t/threads, count*(t+1)/threads). relabel (nullable):
+// ids are emitted as relabel[id] (the relabelled pool id space).
 void augment(const WalkTables& t, uint32_t walk_len, uint32_t s, uint32_t threads,
-             uint64_t count, uint64_t seed, uint32_t* out);
+             uint64_t count, uint64_t seed, uint32_t* out, const uint32_t* relabel = nullptr);
 
 }  // namespace gv

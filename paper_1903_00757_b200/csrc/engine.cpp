@@ -123,8 +123,10 @@ gv_status place_fused(gv_ctx* c, const std::vector<std::vector<uint64_t>>& bc) {
     CK(r.place_args.ensure(args.size()));
     CK(cudaMemcpyAsync(r.place_args.p, args.data(), args.size() * sizeof(uint64_t),
                        cudaMemcpyHostToDevice, r.compute));  // pageable: staged before return
-    CK(gv::launch_bucket_place(c->raw.p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
-                               c->part.pbits, r.plan, r.scratch.p, r.place_args.p,
+    const gv::IdMap ids{c->d_packed, c->relabeled() ? c->d_part_off : nullptr, c->nv,
+                        c->part.pbits};
+    CK(gv::launch_bucket_place(c->raw.p + r.seg_begin, r.seg_count, ids, r.plan, r.scratch.p,
+                               r.place_args.p,
                                reinterpret_cast<uint2* const*>(r.place_args.p + bins), bpr,
                                reinterpret_cast<uint32_t*>(r.counts.p + bins + 1), r.compute,
                                &r.kernel_launches));
@@ -166,6 +168,8 @@ gv_status prepare(gv_ctx* c) {
   // sample straight into the receive buffer of the rank that owns its block
   // row (a6 fused into a5); it runs after the counts are known
   const bool fused = c->D > 1;
+  const gv::IdMap ids{c->d_packed, c->relabeled() ? c->d_part_off : nullptr, c->nv, c->part.pbits};
+  const bool swap = c->swap_mode();
   // 1) bucketing per rank (a3-a5)
   for (auto& r : c->ranks) {
     r.kernel_launches = 0;
@@ -183,15 +187,23 @@ gv_status prepare(gv_ctx* c) {
     CK(r.scratch.ensure(gv::bucket_scratch_bytes(r.plan)));
     CK(cudaMemsetAsync(r.counts.p + bins + 1, 0, sizeof(uint64_t), r.compute));
     uint32_t* err = reinterpret_cast<uint32_t*>(r.counts.p + bins + 1);
-    if (fused) {
-      CK(gv::launch_bucket_count(c->raw.p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
-                                 c->part.pbits, r.plan, r.scratch.p, r.counts.p, err, r.compute,
-                                 &r.kernel_launches));
+    if (swap) {
+      // relabelled pool, n = 1: range check where the pool lies, then the
+      // raw buffer becomes the block buffer (no copy); the old block buffer
+      // becomes the raw buffer once the previous pool's SGD, enqueued before
+      // this check on the same stream, has read it (raw_free below)
+      const uint2* pool = c->pending_in_blocks ? r.blocks.p : c->raw.p;
+      CK(gv::launch_validate(pool, P, c->nv, r.counts.p, err, r.compute, &r.kernel_launches));
+      CK(cudaEventRecord(r.ev_bucket, r.compute));
+      if (!c->pending_in_blocks) std::swap(c->raw, r.blocks);
+      c->pending_in_blocks = false;
+    } else if (fused) {
+      CK(gv::launch_bucket_count(c->raw.p + r.seg_begin, r.seg_count, ids, r.plan, r.scratch.p,
+                                 r.counts.p, err, r.compute, &r.kernel_launches));
     } else {
       CK(r.blocks.ensure(r.seg_count));
-      CK(gv::launch_bucket(c->raw.p + r.seg_begin, r.seg_count, c->d_packed, c->nv,
-                           c->part.pbits, r.plan, r.scratch.p, r.blocks.p, r.counts.p, err,
-                           r.compute, &r.kernel_launches));
+      CK(gv::launch_bucket(c->raw.p + r.seg_begin, r.seg_count, ids, r.plan, r.scratch.p,
+                           r.blocks.p, r.counts.p, err, r.compute, &r.kernel_launches));
       CK(cudaEventRecord(r.ev_bucket, r.compute));
     }
   }
@@ -476,6 +488,8 @@ gv_status setup_device(gv_ctx* c) {
   CK(cudaMalloc(&c->d_packed, sizeof(uint32_t) * nv));
   CK(cudaMalloc(&c->d_alias, sizeof(uint2) * nv));
   CK(cudaMalloc(&c->d_inv_perm, sizeof(uint32_t) * nv));
+  CK(cudaMalloc(&c->d_part_off, sizeof(uint64_t) * (n + 1)));
+  CK(cudaMemcpy(c->d_part_off, c->part.off.data(), sizeof(uint64_t) * (n + 1), cudaMemcpyHostToDevice));
   static_assert(sizeof(gv::ProbAlias) == sizeof(uint2), "alias slots upload as uint2");
   CK(cudaMemcpy(c->d_packed, c->part.packed.data(), sizeof(uint32_t) * nv, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_alias, c->nalias.data(), sizeof(uint2) * nv, cudaMemcpyHostToDevice));
@@ -641,6 +655,8 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
     return fail(nullptr, GV_ERR_INVALID_ARG, "n_partitions must be a multiple of the rank count");
   if (o.host_partitions && (o.world_size * o.virtual_ranks != 1 || n_partitions < 2))
     return fail(nullptr, GV_ERR_INVALID_ARG, "host_partitions needs one rank and n_partitions >= 2");
+  if (o.pool_ids != GV_IDS_ORIGINAL && o.pool_ids != GV_IDS_RELABELED)
+    return fail(nullptr, GV_ERR_INVALID_ARG, "pool_ids must be GV_IDS_ORIGINAL or GV_IDS_RELABELED");
   if (alpha && (alpha->kind != GV_LR_CONSTANT && alpha->kind != GV_LR_LINEAR))
     return fail(nullptr, GV_ERR_INVALID_ARG, "bad lr schedule kind");
   int ndev = 0;
@@ -735,6 +751,8 @@ constexpr uint64_t kPushChunk = uint64_t(1) << 23;  // 64 MiB of pairs
 static gv_status reserve_raw(gv_ctx* c, std::unique_lock<std::mutex>& lk, uint64_t count,
                              uint64_t* have_out) {
   c->raw_cv.wait(lk, [&] { return !c->raw_busy; });
+  if (c->pending_in_blocks)
+    return fail(c, GV_ERR_STATE, "a replayed pool is pending: train it before pushing");
   const uint64_t have = c->raw_count;
   if (c->opt.max_pool_samples && have + count > c->opt.max_pool_samples)
     return fail(c, GV_ERR_CAPACITY, "pending pool would exceed max_pool_samples");
@@ -795,6 +813,7 @@ gv_status gv_replay_pool(gv_ctx* c) {
   if (c->state == PoolState::Prepared || !c->have_last || c->raw_busy || c->raw_count != 0)
     return fail(c, GV_ERR_STATE, "no trained pool to replay, or a pool is pending");
   c->raw_count = c->last_count;
+  c->pending_in_blocks = c->swap_mode();  // swap mode: the last pool lies in the block buffer
   return GV_OK;
 }
 
@@ -926,7 +945,8 @@ gv_status gv_augment(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_t threads,
   if (walk_len == 0 || s == 0 || s > walk_len || threads == 0)
     return fail(c, GV_ERR_INVALID_ARG, "need walk_len > 0, 0 < s <= walk_len, threads > 0");
   if (count && !out_pairs) return fail(c, GV_ERR_INVALID_ARG, "null out_pairs");
-  gv::augment(c->walks, walk_len, s, threads, count, seed, out_pairs);
+  gv::augment(c->walks, walk_len, s, threads, count, seed, out_pairs,
+              c->relabeled() ? c->part.perm.data() : nullptr);
   return GV_OK;
 }
 
@@ -961,7 +981,12 @@ gv_status gv_augment_device_ex(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_
   std::unique_lock<std::mutex> lk(c->mu);
   uint64_t have = 0;
   if (gv_status st = reserve_raw(c, lk, count, &have)) return st;
-  gv::WalkDev wd{c->d_woff, c->d_wnbr, c->d_walias, c->d_dalias, c->nv};
+  if (c->relabeled() && !c->d_perm) {
+    CK(cudaMalloc(&c->d_perm, sizeof(uint32_t) * c->nv));
+    CK(cudaMemcpy(c->d_perm, c->part.perm.data(), sizeof(uint32_t) * c->nv, cudaMemcpyHostToDevice));
+  }
+  gv::WalkDev wd{c->d_woff, c->d_wnbr, c->d_walias, c->d_dalias, c->nv,
+                 c->relabeled() ? c->d_perm : nullptr};
   if (shuffle == GV_SHUFFLE_RANDOM) {  // walk order into scratch, then a keyed permutation
     CK(c->shuf_tmp.ensure(count));
     CK(gv::launch_augment(wd, walk_len, s, segments, count, seed, 1, c->shuf_tmp.p,
@@ -984,7 +1009,8 @@ gv_status gv_debug_get_pending(gv_ctx* c, uint32_t* out, uint64_t cap, uint64_t*
   if (!out) return GV_OK;
   if (cap < c->raw_count) return fail(c, GV_ERR_CAPACITY, "cap < pending pool size");
   CK(cudaStreamSynchronize(c->copy_stream));
-  CK(cudaMemcpy(out, c->raw.p, sizeof(uint2) * c->raw_count, cudaMemcpyDefault));
+  const uint2* pool = c->pending_in_blocks ? c->ranks[0].blocks.p : c->raw.p;
+  CK(cudaMemcpy(out, pool, sizeof(uint2) * c->raw_count, cudaMemcpyDefault));
   return GV_OK;
 }
 
@@ -1167,6 +1193,8 @@ void gv_destroy(gv_ctx* c) {
   cudaFree(c->d_walias);
   cudaFree(c->d_dalias);
   cudaFree(c->d_inv_perm);
+  cudaFree(c->d_part_off);
+  cudaFree(c->d_perm);
   gv::graph_share_unmap(&c->graph_map);
   delete c;
 }

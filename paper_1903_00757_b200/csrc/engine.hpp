@@ -141,9 +141,12 @@ struct gv_ctx {
   uint2* d_dalias = nullptr;
   gv::DevBuf<uint2> shuf_tmp;  // random-shuffle ablation scratch
   // shared device tables
-  uint32_t* d_packed = nullptr;
+  uint32_t* d_packed = nullptr;    // original id -> part | local (ORIGINAL pool ids)
+  uint64_t* d_part_off = nullptr;  // n + 1 partition offsets (RELABELED pool ids)
   uint2* d_alias = nullptr;
   uint32_t* d_inv_perm = nullptr;
+  uint32_t* d_perm = nullptr;      // original -> new (device augmentation, RELABELED), lazily
+  bool relabeled() const { return opt.pool_ids == GV_IDS_RELABELED; }
   // pool (a2): ONE raw buffer. gv_train_episode takes the pending pool out of
   // it (prepare), and the next push may refill it as soon as the bucketing
   // kernels have read it (raw_free) — a few ms into the pool's training — so
@@ -157,6 +160,14 @@ struct gv_ctx {
   cudaEvent_t raw_ready = nullptr, raw_free = nullptr;
   bool have_last = false;       // raw still holds the last trained pool (replay)
   uint64_t last_count = 0;
+  // Relabelled ids at n = 1 on one rank (swap_mode): a3 is the range check
+  // alone, and the pool is trained where it was pushed — prepare swaps the
+  // raw and block buffers instead of copying, so the last pool lives in the
+  // block buffer and a replay re-arms it there (pending_in_blocks).
+  bool pending_in_blocks = false;
+  bool swap_mode() const {
+    return relabeled() && n == 1 && D == 1 && !hp() && !raw.host;
+  }
   cudaStream_t copy_stream = nullptr;
   gv::PoolState state = gv::PoolState::Idle;
   uint64_t pool_P = 0;        // samples of the prepared pool (this process)

@@ -884,7 +884,7 @@ __global__ void __launch_bounds__(kAugBlock) augment_kernel(WalkDev g, uint32_t 
       uint32_t slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, g.nv);
       uint2 pa = __ldg(g.dalias + slot);
       uint32_t x = alias_pick(pa.x, pa.y, slot, r.z);
-      my[0] = x;
+      my[0] = g.relabel ? __ldg(g.relabel + x) : x;
       for (uint32_t k = 1; k <= L; ++k) {
         const uint64_t o = __ldg(g.off + x);
         const uint32_t m = static_cast<uint32_t>(__ldg(g.off + x + 1) - o);
@@ -892,7 +892,7 @@ __global__ void __launch_bounds__(kAugBlock) augment_kernel(WalkDev g, uint32_t 
         slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, m);
         pa = __ldg(g.ealias + o + slot);
         x = __ldg(g.nbr + o + alias_pick(pa.x, pa.y, slot, r.z));
-        my[k] = x;
+        my[k] = g.relabel ? __ldg(g.relabel + x) : x;  // pairs in the pool's id space
       }
       // its pair count
       uint32_t c = 0;
@@ -937,15 +937,29 @@ __global__ void __launch_bounds__(kAugBlock) augment_kernel(WalkDev g, uint32_t 
 
 struct BinCtx {
   const uint32_t* packed;
+  const uint64_t* part_off;  // relabelled pool ids (IdMap)
   uint32_t nv, pbits, n;
 };
+
+// {part | local} of a node id: a gather of packed[] for ORIGINAL ids; for
+// RELABELLED ids the partition comes from the offsets (near-equal zig-zag
+// sizes: the proportional guess is off by at most one partition, corrected
+// against part_off) — no gather into a |V|-sized table.
+__device__ __forceinline__ uint32_t packed_of(const BinCtx& b, uint32_t id) {
+  if (b.part_off == nullptr) return __ldg(b.packed + id);
+  if (b.pbits == 0) return id;
+  uint32_t p = static_cast<uint32_t>(static_cast<uint64_t>(id) * b.n / b.nv);
+  while (p > 0 && id < __ldg(b.part_off + p)) --p;
+  while (p + 1 < b.n && id >= __ldg(b.part_off + p + 1)) ++p;
+  return (p << (32 - b.pbits)) | (id - static_cast<uint32_t>(__ldg(b.part_off + p)));
+}
 
 // bin of a sample and its local ids; out-of-range ids raise *err and map to bin 0.
 __device__ __forceinline__ uint32_t bin_of(const BinCtx& b, uint2 p, uint2& local,
                                            uint32_t* err) {
   // branch-free, so that a thread's several samples keep their gathers in flight
   const bool bad = p.x >= b.nv || p.y >= b.nv;
-  const uint32_t a = __ldg(b.packed + (bad ? 0u : p.x)), c = __ldg(b.packed + (bad ? 0u : p.y));
+  const uint32_t a = packed_of(b, bad ? 0u : p.x), c = packed_of(b, bad ? 0u : p.y);
   if (bad) *err = 1u;
   if (b.pbits == 0) {
     local = bad ? make_uint2(0, 0) : make_uint2(a, c);
@@ -987,7 +1001,7 @@ __device__ __forceinline__ uint32_t pass_bin(const BinCtx& b, uint2 p, uint2& va
     return p.x >> sh;
   }
   const bool bad = p.x >= b.nv || p.y >= b.nv;
-  const uint32_t a = __ldg(b.packed + (bad ? 0u : p.x)), c = __ldg(b.packed + (bad ? 0u : p.y));
+  const uint32_t a = packed_of(b, bad ? 0u : p.x), c = packed_of(b, bad ? 0u : p.y);
   if (bad) *err = 1u;
   val = bad ? make_uint2(0, 0) : make_uint2(a, c);
   return bad ? 0u : c >> sh;
@@ -1013,6 +1027,25 @@ __global__ void relabel_kernel(const uint2* __restrict__ in, uint64_t count, Bin
       if (i < count) __stcs(out + i, loc[j]);
     }
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    block_off[0] = 0;
+    block_off[1] = count;
+  }
+}
+
+// a3 for a pool already in relabelled ids at n = 1 (gv_options.pool_ids):
+// the pool is its own block, so only the range check remains — a streaming
+// read, no copy (the engine trains the pool where it lies).
+__global__ void validate_kernel(const uint2* __restrict__ in, uint64_t count, uint32_t nv,
+                                uint64_t* block_off, uint32_t* err) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint32_t mx = 0;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += stride) {
+    const uint2 p = __ldcs(in + i);
+    mx = max(mx, max(p.x, p.y));
+  }
+  if (mx >= nv) *err = 1u;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     block_off[0] = 0;
     block_off[1] = count;
@@ -1471,11 +1504,10 @@ BucketScratch scratch_parts(void* scratch, const BucketPlan& plan) {
 }
 }  // namespace
 
-cudaError_t launch_bucket_count(const uint2* in, uint64_t count, const uint32_t* packed,
-                                uint32_t nv, uint32_t pbits, const BucketPlan& plan,
-                                void* scratch, uint64_t* block_off, uint32_t* err, cudaStream_t s,
+cudaError_t launch_bucket_count(const uint2* in, uint64_t count, const IdMap& ids,
+                                const BucketPlan& plan, void* scratch, uint64_t* block_off, uint32_t* err, cudaStream_t s,
                                 int* launches) {
-  BinCtx b{packed, nv, pbits, plan.n};
+  BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, plan.n};
   const BucketScratch sc = scratch_parts(scratch, plan);
   if (plan.tiles == 0) {
     cudaMemsetAsync(block_off, 0, (plan.bins + 1) * sizeof(uint64_t), s);
@@ -1491,13 +1523,12 @@ cudaError_t launch_bucket_count(const uint2* in, uint64_t count, const uint32_t*
   return cudaGetLastError();
 }
 
-cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const uint32_t* packed,
-                                uint32_t nv, uint32_t pbits, const BucketPlan& plan,
-                                const void* scratch, const uint64_t* dst_off, uint2* const* outs,
+cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const IdMap& ids,
+                                const BucketPlan& plan, const void* scratch, const uint64_t* dst_off, uint2* const* outs,
                                 uint32_t bins_per_out, uint32_t* err, cudaStream_t s,
                                 int* launches) {
   if (plan.tiles == 0) return cudaSuccess;
-  BinCtx b{packed, nv, pbits, plan.n};
+  BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, plan.n};
   const BucketScratch sc = scratch_parts(const_cast<void*>(scratch), plan);
   const unsigned grid =
       static_cast<unsigned>(umin64(plan.tiles, static_cast<uint64_t>(num_sms()) * bucket_ctas()));
@@ -1548,10 +1579,10 @@ cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const uint32_t*
   return cudaErrorInvalidValue;  // unreachable: every grid is single-pass (<= 128 bins) or two-pass
 }
 
-cudaError_t launch_bucket(const uint2* in, uint64_t count, const uint32_t* packed, uint32_t nv,
-                          uint32_t pbits, const BucketPlan& plan, void* scratch, uint2* out,
+cudaError_t launch_bucket(const uint2* in, uint64_t count, const IdMap& ids,
+                          const BucketPlan& plan, void* scratch, uint2* out,
                           uint64_t* block_off, uint32_t* err, cudaStream_t s, int* launches) {
-  BinCtx b{packed, nv, pbits, plan.n};
+  BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, plan.n};
   const int sms = num_sms();
   if (plan.n == 1) {
     uint64_t grid = umin64((count + 255) / 256, static_cast<uint64_t>(sms) * 8);
@@ -1560,14 +1591,22 @@ cudaError_t launch_bucket(const uint2* in, uint64_t count, const uint32_t* packe
     if (launches) *launches += 1;
     return cudaGetLastError();
   }
-  cudaError_t e = launch_bucket_count(in, count, packed, nv, pbits, plan, scratch, block_off, err,
-                                      s, launches);
+  cudaError_t e = launch_bucket_count(in, count, ids, plan, scratch, block_off, err, s, launches);
   if (e != cudaSuccess || plan.tiles == 0) return e;
   uint2** outs = scratch_parts(scratch, plan).outs;  // the single output, one pointer
   e = cudaMemcpyAsync(outs, &out, sizeof(uint2*), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;
-  return launch_bucket_place(in, count, packed, nv, pbits, plan, scratch, block_off, outs,
+  return launch_bucket_place(in, count, ids, plan, scratch, block_off, outs,
                              plan.bins, err, s, launches);
+}
+
+cudaError_t launch_validate(const uint2* in, uint64_t count, uint32_t nv, uint64_t* block_off,
+                            uint32_t* err, cudaStream_t s, int* launches) {
+  uint64_t grid = umin64((count + 255) / 256, static_cast<uint64_t>(num_sms()) * 8);
+  if (grid == 0) grid = 1;
+  validate_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(in, count, nv, block_off, err);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_augment(const WalkDev& g, uint32_t walk_len, uint32_t s, uint32_t segments,

@@ -70,8 +70,9 @@ struct WalkDev {
   const uint2* ealias;   // per CSR entry {prob, alias}: neighbour tables
   const uint2* dalias;   // per node {prob, alias}: departure table (weight = degree)
   uint32_t nv;
+  const uint32_t* relabel;  // nullable: emit relabel[id] (perm: pool_ids = relabelled)
 };
-// Appends `count` pairs (ORIGINAL ids) to out: `segments` pool segments as in
+// Appends `count` pairs (ORIGINAL ids, or relabel[id] when g.relabel) to out: `segments` pool segments as in
 // gv_augment with threads = segments (reading R-AUG), one CTA per segment.
 // shuffle: 0 = pseudo shuffle, 1 = none (each segment in walk
 // order) — the ablation of tab:shuffle.
@@ -95,12 +96,23 @@ struct BucketPlan {
 BucketPlan make_bucket_plan(uint32_t n, uint64_t count);
 size_t bucket_scratch_bytes(const BucketPlan& p);  // tile counts + bin totals
 
+// How pool ids map to (partition, local id) in bucketing (a3):
+// part_off == nullptr: ORIGINAL ids, packed[orig] = (part << (32-pbits)) | local
+// (one gather per id); else RELABELLED ids (gv_options.pool_ids): the
+// partition p with part_off[p] <= id < part_off[p+1] (device, n + 1 words)
+// and local = id - part_off[p], with no gather.
+struct IdMap {
+  const uint32_t* packed;
+  const uint64_t* part_off;
+  uint32_t nv, pbits;
+};
+
 // Full pipeline: range check + relabel + histogram + scans + stable scatter.
-// in: (u, v) ORIGINAL ids; packed[orig] = (part << (32-pbits)) | local.
+// in: (u, v) ids as described by `ids`.
 // out: local ids in bin-major order; block_off_dev[bins+1] (uint64);
 // err_dev: set to 1 if an id >= nv is met (contents of out undefined then).
-cudaError_t launch_bucket(const uint2* in, uint64_t count, const uint32_t* packed,
-                          uint32_t nv, uint32_t pbits, const BucketPlan& plan, void* scratch,
+cudaError_t launch_bucket(const uint2* in, uint64_t count, const IdMap& ids,
+                          const BucketPlan& plan, void* scratch,
                           uint2* out, uint64_t* block_off_dev, uint32_t* err_dev,
                           cudaStream_t s, int* launches);
 
@@ -110,16 +122,18 @@ cudaError_t launch_bucket(const uint2* in, uint64_t count, const uint32_t* packe
 // NVLink, or plain stores for virtual ranks / the local row).
 // Count phase (n > 1): range check + histogram + scans; block_off_dev as
 // above; the per-tile offsets stay in scratch for the place phase.
-cudaError_t launch_bucket_count(const uint2* in, uint64_t count, const uint32_t* packed,
-                                uint32_t nv, uint32_t pbits, const BucketPlan& plan,
-                                void* scratch, uint64_t* block_off_dev, uint32_t* err_dev,
+cudaError_t launch_bucket_count(const uint2* in, uint64_t count, const IdMap& ids,
+                                const BucketPlan& plan, void* scratch, uint64_t* block_off_dev, uint32_t* err_dev,
                                 cudaStream_t s, int* launches);
+// a3 of a relabelled pool at n = 1: range check only (err_dev), block_off =
+// {0, count}; the pool is trained where it lies.
+cudaError_t launch_validate(const uint2* in, uint64_t count, uint32_t nv, uint64_t* block_off_dev,
+                            uint32_t* err_dev, cudaStream_t s, int* launches);
 // Place phase: sample of bin q (stable rank r within this pool's bin q) goes
 // to outs[q / bins_per_out][dst_off[q] + r]. outs (device array of device
 // pointers, peer-mapped allowed) and dst_off[bins] are in device memory.
-cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const uint32_t* packed,
-                                uint32_t nv, uint32_t pbits, const BucketPlan& plan,
-                                const void* scratch, const uint64_t* dst_off,
+cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const IdMap& ids,
+                                const BucketPlan& plan, const void* scratch, const uint64_t* dst_off,
                                 uint2* const* outs, uint32_t bins_per_out, uint32_t* err_dev,
                                 cudaStream_t s, int* launches);
 

@@ -22,6 +22,7 @@ GV_OK, GV_ERR_INVALID_ARG, GV_ERR_STATE, GV_ERR_OUT_OF_RANGE, GV_ERR_EMPTY, GV_E
     GV_ERR_NOMEM, GV_ERR_CUDA, GV_ERR_COMM = range(9)
 GV_LR_CONSTANT, GV_LR_LINEAR = 0, 1
 GV_SHUFFLE_PSEUDO, GV_SHUFFLE_NONE, GV_SHUFFLE_RANDOM = 0, 1, 2
+GV_IDS_ORIGINAL, GV_IDS_RELABELED = 0, 1
 
 
 class GVError(RuntimeError):
@@ -40,7 +41,7 @@ class gv_options(C.Structure):
                 ("device", C.c_int), ("rank", C.c_int), ("world_size", C.c_int),
                 ("virtual_ranks", C.c_int), ("ordered", C.c_int), ("compute_loss", C.c_int),
                 ("host_threads", C.c_int), ("max_pool_samples", C.c_uint64),
-                ("host_partitions", C.c_int), ("host_pool", C.c_int)]
+                ("host_partitions", C.c_int), ("host_pool", C.c_int), ("pool_ids", C.c_int)]
 
 
 class gv_episode_stats(C.Structure):

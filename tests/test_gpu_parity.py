@@ -679,3 +679,82 @@ def test_push_overlapping_training_single_raw_buffer(c1_graph, host_pool, vr):
     else:
         assert grown >= 16 * P, grown
     p.close()
+
+
+def _relabeled_pair(nv, src, dst, **kw):
+    """Two contexts over the same graph: ORIGINAL pool ids and RELABELED."""
+    out = []
+    for ids in (G.GV_IDS_ORIGINAL, G.GV_IDS_RELABELED):
+        g = G.GraphVite(nv, kw.get("d", 32), kw.get("n", 1), 1, 0.025,
+                        total_samples=kw.get("total", 0), ordered=kw.get("ordered", 1),
+                        virtual_ranks=kw.get("vr", 1), host_pool=kw.get("host_pool", 0),
+                        pool_ids=ids)
+        g.load_edges(src, dst)
+        out.append(g)
+    return out
+
+
+@pytest.mark.parametrize("n,vr,host_pool", [(1, 1, 0), (1, 1, 1), (4, 1, 0), (4, 2, 0),
+                                            (16, 1, 0), (16, 4, 0)])
+def test_relabeled_pool_ids_train_identically(c1_graph, n, vr, host_pool):
+    """gv_options.pool_ids = GV_IDS_RELABELED ("skipped
+    (identity) at n = 1 with relabeled input"): the same pools pushed as
+    perm[orig] train BIT-identically to the original-id pushes — same blocks
+    (bucketing without the relabel gather, partition found from the offsets),
+    same negatives, same updates — across several pools, including the n = 1
+    swap path (pool trained where it lies, raw and block buffers alternate),
+    a push overlapping training, and a replay."""
+    src, dst = c1_graph
+    P = 200_003
+    pools = [synth.edge_pool(src, dst, P, seed=60 + k) for k in range(3)]
+    a, b = _relabeled_pair(C1["nv"], src, dst, d=32, n=n, vr=vr, host_pool=host_pool, total=5 * P)
+    perm, _ = a.partition()
+    for g, pools_k in ((a, pools), (b, [perm[q] for q in pools])):
+        g.push(pools_k[0])
+        g.train_episode(stats=False)
+        g.push(pools_k[1])          # overlaps pool 0's training
+        st1 = g.train_episode()
+        g.replay()                  # pool 1 again, in place
+        g.train_episode(stats=False)
+        g.push(pools_k[2])
+        st3 = g.train_episode()
+        assert st1["samples_global"] == P and st3["pool_index"] == 3
+    assert np.array_equal(a.vertex(), b.vertex())
+    assert np.array_equal(a.context(), b.context())
+    o = O.Trainer(C1["nv"], 32, n, K=1, lr0=0.025, lr_kind=1, total_samples=5 * P)
+    o.load_edges(src, dst)
+    for q in (pools[0], pools[1], pools[1], pools[2]):
+        o.train_pool(q)
+    assert_matrix_parity(b.vertex(), o.get("vertex"), "vertex")
+    assert_matrix_parity(b.context(), o.get("context"), "context")
+    a.close()
+    b.close()
+
+
+@pytest.mark.parametrize("n", [1, 5])
+def test_relabeled_augmentation_and_range_check(c1_graph, n):
+    """Relabelled pools from the samplers are perm[] of the original-id pools,
+    byte for byte (host gv_augment and device gv_augment_device), and an id
+    >= num_nodes is still rejected before any update (GV_ERR_OUT_OF_RANGE)."""
+    src, dst = c1_graph
+    a, b = _relabeled_pair(C1["nv"], src, dst, d=16, n=n)
+    perm, _ = a.partition()
+    host_a = G.gv_augment(a.ctx, 40, 5, 7, 100_003, 11)
+    host_b = G.gv_augment(b.ctx, 40, 5, 7, 100_003, 11)
+    assert np.array_equal(perm[host_a], host_b)
+    a.augment_device(40, 5, 64, 50_001, 12)
+    b.augment_device(40, 5, 64, 50_001, 12)
+    da = G.gv_debug_get_pending(a.ctx)
+    db = G.gv_debug_get_pending(b.ctx)
+    assert np.array_equal(perm[da], db)
+    b.train_episode(stats=False)  # consume the device pool
+    V0 = b.vertex()
+    bad = perm[synth.edge_pool(src, dst, 1000, seed=3)]
+    bad[777, 1] = C1["nv"]
+    b.push(bad)
+    with pytest.raises(G.GVError) as e:
+        b.train_episode()
+    assert e.value.status == G.GV_ERR_OUT_OF_RANGE
+    assert np.array_equal(b.vertex(), V0)
+    a.close()
+    b.close()
