@@ -298,6 +298,11 @@ gv_status run_steps(gv_ctx* c) {
   // descriptors: D == 1 -> one launch per step over all n blocks;
   //              D > 1  -> one launch per block (g), so the first block of a
   //              step can release its context partition early.
+  // GV_BLOCK_LAUNCH=1 (measurement): one launch per block on one rank too —
+  // the kernel then sees one block's rows at a time, as a GPU of a D = n
+  // grid does (hot-row density n times that of n = 1)
+  static const bool per_block = getenv("GV_BLOCK_LAUNCH") && atoi(getenv("GV_BLOCK_LAUNCH")) != 0;
+  const bool step_launch = c->D == 1 && !c->hp() && !per_block;
   gv::HpPlan hp;  // out-of-core: residency order, slots, loads and write-backs
   if (c->hp()) gv::hp_plan(c, &hp);
   for (auto& r : c->ranks) {
@@ -314,7 +319,7 @@ gv_status run_steps(gv_ctx* c) {
         gv::BlockDesc& d = desc[t * m + g];
         d.sample_off = r.final_off[g * n + j];
         d.count_lo = static_cast<uint32_t>(r.final_off[g * n + j + 1] - r.final_off[g * n + j]);
-        d.prefix = (c->D == 1 && !c->hp()) ? prefix : 0;
+        d.prefix = step_launch ? prefix : 0;
         prefix += d.count_lo;
         d.vrow0 = static_cast<uint32_t>(c->part.off[i] - r.vrow_first);
         d.crow0 = static_cast<uint32_t>(c->D == 1 ? c->part.off[j]
@@ -340,7 +345,7 @@ gv_status run_steps(gv_ctx* c) {
                        cudaMemcpyHostToDevice, r.compute));
     // (pageable source: the copy is staged before cudaMemcpyAsync returns)
     if (c->opt.compute_loss) CK(cudaMemsetAsync(r.loss.p, 0, sizeof(double), r.compute));
-    const size_t need = static_cast<size_t>(2) * (c->D == 1 && !c->hp() ? n : n * m);
+    const size_t need = static_cast<size_t>(2) * (step_launch ? n : n * m);
     while (r.ev_sgd.size() < need) r.ev_sgd.push_back(new_event(true));
   }
   // enqueue the steps
@@ -390,7 +395,7 @@ gv_status run_steps(gv_ctx* c) {
       gv_step_plan plan;
       gv_plan_step(n, c->D, r.d, t, &plan);
       auto launch = [&](uint32_t g0, uint32_t cnt_blk) { return launch_blocks(r, t, g0, cnt_blk); };
-      if (c->D == 1) {
+      if (step_launch) {
         gv_status st = launch(0, m);
         if (st) return st;
         continue;
@@ -403,7 +408,7 @@ gv_status run_steps(gv_ctx* c) {
         }
         gv_status st = launch(g, 1);
         if (st) return st;
-        if (g == 0) {
+        if (g == 0 && c->D > 1) {
           CK(cudaEventRecord(r.ev_first_done[t], r.compute));
           if (gv_status st2 = c->tr->first_block_done(c, r, t)) return st2;
         }

@@ -436,13 +436,19 @@ constexpr int kRingLPS = GV_RING_LPS;  // lanes per sample: 16 (2 samples / warp
 // instead of LDGSTS: measured equal on C2 and C4 (profiles/README.md), and
 // compute-sanitizer racecheck cannot verify the async-proxy ordering, so the
 // default is LDGSTS; GV_RING_TMA=1 builds the TMA variant.
-constexpr bool kRingTma = GV_RING_TMA != 0;
+constexpr bool kRingTma = GV_RING_TMA == 1 || GV_RING_TMA == 2 || GV_RING_TMA == 4;
 // GV_RING_TMA=2: the deltas also leave through the TMA unit — each lane
 // writes its columns of err and g_t U over the stage it has consumed, and one
 // lane per group issues a bulk reduce-add (cp.reduce.async.bulk .add.f32, an
 // element-wise atomic add in L2) per row instead of red.global.add.v4 from
 // registers.
 constexpr bool kRingTmaRed = GV_RING_TMA == 2;
+// GV_RING_TMA=3 (LDGSTS loads) / 4 (TMA loads): only the VERTEX row's delta
+// leaves through the TMA unit (one bulk reduce-add per sample), the context
+// rows' deltas by red.global from registers — the two paths to L2 share the
+// delta traffic (the LSU's L1->XBAR request port bounds the default on C2).
+constexpr bool kRingTmaRedV = GV_RING_TMA == 3 || GV_RING_TMA == 4;
+constexpr bool kRingBulk = kRingTmaRed || kRingTmaRedV;
 
 template <int K, int LPS>
 struct RingCfg {
@@ -630,7 +636,7 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
 #if GV_SKIP_HOT_EXPERIMENT
       if ((hot >> r) & 1u) return;
 #endif
-      if (kRingTmaRed) {
+      if (kRingTmaRed || (kRingTmaRedV && r == 0)) {
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
           const int col = gl + LPS * q;
@@ -680,7 +686,7 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
       }
     }
     put_delta(0, u, 1.0f, err, (hot & 1u) ? pol_hot : pol_cold);
-    if (kRingTmaRed) {
+    if (kRingBulk) {
       // the group's generic writes of the deltas, then one lane hands the
       // rows to the TMA unit (async proxy)
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -688,7 +694,7 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
       if (gl == 0) {
         if (act) {
 #pragma unroll
-          for (int t = 0; t < T; ++t)
+          for (int t = 0; t < (kRingTmaRed ? T : 1); ++t)
             bulk_red_row((t == 0 ? vertex : context) +
                              static_cast<uint64_t>(t == 0 ? u : c[t - 1]) * stride,
                          stage + t * 32, static_cast<uint32_t>(dim4 * 16),
@@ -713,7 +719,7 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
     }
   }
   if (!kRingTma) cp_wait<0>();
-  if (kRingTmaRed && gl == 0) bulk_wait_all();
+  if (kRingBulk && gl == 0) bulk_wait_all();
   return loss;
 }
 
