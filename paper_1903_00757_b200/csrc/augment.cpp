@@ -88,6 +88,7 @@ void fill_segment(const WalkTables& t, uint32_t walk_len, uint32_t s, uint32_t t
       const uint32_t x = draw(t.departure.data(), g.nv, r);
       walks[i * W] = x;
       __builtin_prefetch(off + x);
+      if (relabel) __builtin_prefetch(relabel + x);
     }
     for (uint32_t k = 1; k <= walk_len; ++k) {
       for (uint32_t i = 0; i < kBatch; ++i) {
@@ -106,12 +107,11 @@ void fill_segment(const WalkTables& t, uint32_t walk_len, uint32_t s, uint32_t t
         const uint32_t x = nbr[o[i] + pick];
         walks[i * W + k] = x;
         __builtin_prefetch(off + x);
+        if (relabel) __builtin_prefetch(relabel + x);  // mapped after the batch, from cache
       }
     }
-    if (relabel) {  // pairs in the pool's id space (a bijection: w_a != w_b is unchanged)
-      for (uint32_t q = 0; q < kBatch * W; ++q) __builtin_prefetch(relabel + walks[q]);
+    if (relabel)  // pairs in the pool's id space (a bijection: w_a != w_b is unchanged)
       for (uint32_t q = 0; q < kBatch * W; ++q) walks[q] = relabel[walks[q]];
-    }
     // pairs within distance s, walk by walk, by increasing start then end position
     for (uint32_t i = 0; i < kBatch && filled < cap; ++i) {
       const uint32_t* walk = walks.data() + static_cast<size_t>(i) * W;
