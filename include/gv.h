@@ -334,6 +334,27 @@ gv_status gv_augment_device(gv_ctx* ctx, uint32_t walk_len, uint32_t s, uint32_t
 gv_status gv_augment_device_ex(gv_ctx* ctx, uint32_t walk_len, uint32_t s, uint32_t segments,
                                uint64_t count, uint64_t seed, int shuffle);
 
+/* NEXT-1 ("writing bucketed blocks directly"; Alg. 2
+ * P:176-196 with a3-a5): generate a WHOLE pool on the device and bucket it
+ * in the sampler — the walks write their pairs straight into the n x n
+ * blocks, with no raw pool and no separate bucketing pass. The blocks are
+ * exactly those gv_train_episode would build from the pool of
+ * gv_augment_device_ex(walk_len, s, segments, count, seed, shuffle) (a
+ * stable counting sort of that pool by block, reading R-BUCKET). The pool
+ * becomes the pending pool; it is generated on the copy stream, so it
+ * overlaps the training of the previous pool (two block buffers alternate).
+ * Device scratch: a walk cache of ~4 B per pair plus (segments * S * n^2)
+ * counters, S = s (pseudo shuffle) or 1. Not replayable (gv_replay_pool
+ * returns GV_ERR_STATE after it).
+ * Errors: GV_ERR_STATE (no graph; more than one rank; a pool pending),
+ * GV_ERR_INVALID_ARG (walk_len == 0 or > 1000, s == 0 or > walk_len,
+ * segments == 0, count == 0, shuffle not PSEUDO/NONE, or a shape the
+ * sampler cannot bucket: S > 32, count >= 2^32, S * n^2 counters beyond
+ * shared memory — use gv_augment_device then), GV_ERR_CAPACITY
+ * (max_pool_samples), GV_ERR_CUDA. */
+gv_status gv_augment_device_blocks(gv_ctx* ctx, uint32_t walk_len, uint32_t s, uint32_t segments,
+                                   uint64_t count, uint64_t seed, int shuffle);
+
 /* Copy the pending (not yet trained) pool to the host: out_pairs[2*cap],
  * *count = its size. Tests. */
 gv_status gv_debug_get_pending(gv_ctx* ctx, uint32_t* out_pairs, uint64_t cap, uint64_t* count);

@@ -141,12 +141,18 @@ gv_status place_fused(gv_ctx* c, const std::vector<std::vector<uint64_t>>& bc) {
 gv_status prepare(gv_ctx* c) {
   if (c->state == PoolState::Prepared) return GV_OK;
   NvtxRange nv_range("gv:prepare (bucket + exchange)");
+  const bool from_fused = c->fused_pending;  // NEXT-1: already bucketed on the device
   {
     std::lock_guard<std::mutex> lk(c->mu);
-    if (c->raw_count == 0) return fail(c, GV_ERR_EMPTY, "no pending samples");
-    c->pool_P = c->raw_count;
-    c->raw_count = 0;
-    c->raw_busy = true;  // pushes wait until raw_free is recorded below
+    if (from_fused) {
+      c->pool_P = c->fused_count;
+      c->fused_pending = false;
+    } else {
+      if (c->raw_count == 0) return fail(c, GV_ERR_EMPTY, "no pending samples");
+      c->pool_P = c->raw_count;
+      c->raw_count = 0;
+      c->raw_busy = true;  // pushes wait until raw_free is recorded below
+    }
     c->have_last = false;
   }
   // whatever way prepare ends, pushes must not wait forever
@@ -187,7 +193,17 @@ gv_status prepare(gv_ctx* c) {
     CK(r.scratch.ensure(gv::bucket_scratch_bytes(r.plan)));
     CK(cudaMemsetAsync(r.counts.p + bins + 1, 0, sizeof(uint64_t), r.compute));
     uint32_t* err = reinterpret_cast<uint32_t*>(r.counts.p + bins + 1);
-    if (swap) {
+    if (from_fused) {
+      // the device sampler wrote the blocks and their offsets: swap them in;
+      // the previous pool's SGD (enqueued before) is the last reader of the
+      // buffer that becomes blocks_alt
+      CK(cudaStreamWaitEvent(r.compute, c->fused_ready, 0));
+      CK(cudaMemcpyAsync(r.counts.p, c->fused_off.p, sizeof(uint64_t) * (bins + 2),
+                         cudaMemcpyDeviceToDevice, r.compute));
+      std::swap(r.blocks, r.blocks_alt);
+      CK(cudaEventRecord(c->alt_free, r.compute));
+      CK(cudaEventRecord(r.ev_bucket, r.compute));
+    } else if (swap) {
       // relabelled pool, n = 1: range check where the pool lies, then the
       // raw buffer becomes the block buffer (no copy); the old block buffer
       // becomes the raw buffer once the previous pool's SGD, enqueued before
@@ -219,7 +235,7 @@ gv_status prepare(gv_ctx* c) {
     c->raw_cv.notify_all();
     return GV_OK;
   };
-  if (!fused)
+  if (!fused && !from_fused)
     if (gv_status st = release_raw()) return st;
   // 2) counts of every rank to the host (a4)
   std::vector<std::vector<uint64_t>> cnt(c->D, std::vector<uint64_t>(bins + 2, 0));
@@ -503,6 +519,8 @@ gv_status setup_device(gv_ctx* c) {
   CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
   c->raw_ready = new_event(false);
   c->raw_free = new_event(false);
+  c->fused_ready = new_event(false);
+  c->alt_free = new_event(false);
   c->raw.host = c->opt.host_pool != 0;
   const uint32_t key0 = static_cast<uint32_t>(c->opt.init_seed);
   const uint32_t key1 = static_cast<uint32_t>(c->opt.init_seed >> 32);
@@ -960,16 +978,9 @@ gv_status gv_augment_device(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_t s
   return gv_augment_device_ex(c, walk_len, s, segments, count, seed, GV_SHUFFLE_PSEUDO);
 }
 
-gv_status gv_augment_device_ex(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_t segments,
-                               uint64_t count, uint64_t seed, int shuffle) {
-  if (gv_status st = check_ctx(c, true)) return st;
-  if (shuffle != GV_SHUFFLE_PSEUDO && shuffle != GV_SHUFFLE_NONE && shuffle != GV_SHUFFLE_RANDOM)
-    return fail(c, GV_ERR_INVALID_ARG, "shuffle must be GV_SHUFFLE_PSEUDO, _NONE or _RANDOM");
-  if (walk_len == 0 || walk_len > 1000 || s == 0 || s > walk_len || segments == 0)
-    return fail(c, GV_ERR_INVALID_ARG, "need 0 < walk_len <= 1000, 0 < s <= walk_len, segments > 0");
-  if (count == 0) return GV_OK;
-  if (count > (UINT64_MAX / segments)) return fail(c, GV_ERR_CAPACITY, "count * segments overflows");
-  CK(cudaSetDevice(c->opt.device));
+// The device copy of the samplers' tables (CSR, alias tables; perm for
+// relabelled pools), uploaded on first use.
+static gv_status walk_tables_on_device(gv_ctx* c, gv::WalkDev* wd) {
   if (!c->d_woff) {  // upload the CSR and the alias tables the host sampler uses
     const gv::HostGraph& g = c->graph;
     const size_t ne = g.nbr.size();
@@ -983,15 +994,73 @@ gv_status gv_augment_device_ex(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_
     CK(cudaMemcpy(c->d_dalias, c->walks.departure.data(), sizeof(uint2) * g.nv,
                   cudaMemcpyHostToDevice));
   }
-  std::unique_lock<std::mutex> lk(c->mu);
-  uint64_t have = 0;
-  if (gv_status st = reserve_raw(c, lk, count, &have)) return st;
   if (c->relabeled() && !c->d_perm) {
     CK(cudaMalloc(&c->d_perm, sizeof(uint32_t) * c->nv));
     CK(cudaMemcpy(c->d_perm, c->part.perm.data(), sizeof(uint32_t) * c->nv, cudaMemcpyHostToDevice));
   }
-  gv::WalkDev wd{c->d_woff, c->d_wnbr, c->d_walias, c->d_dalias, c->nv,
-                 c->relabeled() ? c->d_perm : nullptr};
+  *wd = gv::WalkDev{c->d_woff, c->d_wnbr, c->d_walias, c->d_dalias, c->nv,
+                    c->relabeled() ? c->d_perm : nullptr};
+  return GV_OK;
+}
+
+gv_status gv_augment_device_blocks(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_t segments,
+                                   uint64_t count, uint64_t seed, int shuffle) {
+  if (gv_status st = check_ctx(c, true)) return st;
+  if (shuffle != GV_SHUFFLE_PSEUDO && shuffle != GV_SHUFFLE_NONE)
+    return fail(c, GV_ERR_INVALID_ARG, "shuffle must be GV_SHUFFLE_PSEUDO or _NONE");
+  if (walk_len == 0 || walk_len > 1000 || s == 0 || s > walk_len || segments == 0 || count == 0)
+    return fail(c, GV_ERR_INVALID_ARG, "need 0 < walk_len <= 1000, 0 < s <= walk_len, segments, count > 0");
+  if (c->D != 1) return fail(c, GV_ERR_STATE, "gv_augment_device_blocks needs one rank");
+  const size_t scratch = gv::augment_blocks_scratch_bytes(
+      walk_len, s, shuffle == GV_SHUFFLE_NONE ? 1 : 0, c->n, segments, count);
+  if (scratch == 0)
+    return fail(c, GV_ERR_INVALID_ARG, "shape not eligible for bucketing in the sampler "
+                                       "(s > 32, count >= 2^32 or n^2 * s too large)");
+  if (c->opt.max_pool_samples && count > c->opt.max_pool_samples)
+    return fail(c, GV_ERR_CAPACITY, "pool would exceed max_pool_samples");
+  CK(cudaSetDevice(c->opt.device));
+  gv::WalkDev wd;
+  if (gv_status st = walk_tables_on_device(c, &wd)) return st;
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (c->raw_count != 0 || c->fused_pending || c->pending_in_blocks || c->state == PoolState::Prepared)
+    return fail(c, GV_ERR_STATE, "a pool is pending: train it first");
+  Rank& r = c->ranks[0];
+  const uint32_t bins = c->n * c->n;
+  CK(c->aug_scratch.ensure(scratch));
+  CK(c->fused_off.ensure(bins + 2));
+  CK(cudaStreamWaitEvent(c->copy_stream, c->alt_free, 0));  // the previous reader of blocks_alt
+  if (count > r.blocks_alt.cap) {
+    CK(cudaStreamSynchronize(c->copy_stream));  // the old buffer is no longer read
+    CK(r.blocks_alt.ensure(count));
+  }
+  CK(cudaMemsetAsync(c->fused_off.p + bins + 1, 0, sizeof(uint64_t), c->copy_stream));
+  const gv::IdMap ids{c->d_packed, c->relabeled() ? c->d_part_off : nullptr, c->nv, c->part.pbits};
+  CK(gv::launch_augment_blocks(wd, walk_len, s, segments, count, seed,
+                               shuffle == GV_SHUFFLE_NONE ? 1 : 0, ids, c->n, c->aug_scratch.p,
+                               c->fused_off.p, reinterpret_cast<uint32_t*>(c->fused_off.p + bins + 1),
+                               r.blocks_alt.p, c->copy_stream, nullptr));
+  CK(cudaEventRecord(c->fused_ready, c->copy_stream));
+  c->fused_pending = true;
+  c->fused_count = count;
+  c->have_last = false;
+  return GV_OK;
+}
+
+gv_status gv_augment_device_ex(gv_ctx* c, uint32_t walk_len, uint32_t s, uint32_t segments,
+                               uint64_t count, uint64_t seed, int shuffle) {
+  if (gv_status st = check_ctx(c, true)) return st;
+  if (shuffle != GV_SHUFFLE_PSEUDO && shuffle != GV_SHUFFLE_NONE && shuffle != GV_SHUFFLE_RANDOM)
+    return fail(c, GV_ERR_INVALID_ARG, "shuffle must be GV_SHUFFLE_PSEUDO, _NONE or _RANDOM");
+  if (walk_len == 0 || walk_len > 1000 || s == 0 || s > walk_len || segments == 0)
+    return fail(c, GV_ERR_INVALID_ARG, "need 0 < walk_len <= 1000, 0 < s <= walk_len, segments > 0");
+  if (count == 0) return GV_OK;
+  if (count > (UINT64_MAX / segments)) return fail(c, GV_ERR_CAPACITY, "count * segments overflows");
+  CK(cudaSetDevice(c->opt.device));
+  gv::WalkDev wd;
+  if (gv_status st = walk_tables_on_device(c, &wd)) return st;
+  std::unique_lock<std::mutex> lk(c->mu);
+  uint64_t have = 0;
+  if (gv_status st = reserve_raw(c, lk, count, &have)) return st;
   if (shuffle == GV_SHUFFLE_RANDOM) {  // walk order into scratch, then a keyed permutation
     CK(c->shuf_tmp.ensure(count));
     CK(gv::launch_augment(wd, walk_len, s, segments, count, seed, 1, c->shuf_tmp.p,
@@ -1156,8 +1225,8 @@ gv_status gv_device_bytes(gv_ctx* c, uint64_t* bytes) {
   if (!c->raw.host) b += c->raw.bytes_total();
   for (auto& r : c->ranks) {
     b += (r.vrows + r.crows) * c->stride * 4;
-    b += r.blocks.bytes_total() +
-         r.scratch.bytes_total();
+    b += r.blocks.bytes_total() + r.blocks_alt.bytes_total() + r.scratch.bytes_total();
+  b += c->aug_scratch.bytes_total();
   }
   *bytes = b;
   return GV_OK;
@@ -1175,7 +1244,7 @@ void gv_destroy(gv_ctx* c) {
   for (auto& r : c->ranks) {
     cudaFree(r.vertex);
     cudaFree(r.context);
-    r.blocks.release(); r.scratch.release();
+    r.blocks.release(); r.blocks_alt.release(); r.scratch.release();
     r.counts.release(); r.desc.release(); r.loss.release();
     if (r.counts_host) cudaFreeHost(r.counts_host);
     for (cudaEvent_t e : {r.ev_start, r.ev_bucket, r.ev_exch, r.ev_end,
@@ -1188,6 +1257,10 @@ void gv_destroy(gv_ctx* c) {
   }
   c->raw.release();
   if (c->raw_ready) cudaEventDestroy(c->raw_ready);
+  if (c->fused_ready) cudaEventDestroy(c->fused_ready);
+  if (c->alt_free) cudaEventDestroy(c->alt_free);
+  c->fused_off.release();
+  c->aug_scratch.release();
   if (c->raw_free) cudaEventDestroy(c->raw_free);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   gv::hp_destroy(c);

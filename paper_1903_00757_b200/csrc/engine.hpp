@@ -72,6 +72,7 @@ struct Rank {
   std::vector<int> slot_of;  // partition -> context slot (D > 1)
   int free_slot = -1;
   DevBuf<uint2> blocks;
+  DevBuf<uint2> blocks_alt;  // NEXT-1: the next pool, bucketed by the device sampler
   DevBuf<uint8_t> scratch;
   DevBuf<uint64_t> counts;      // [0, bins]: block_off; [bins+1]: error flag
   DevBuf<BlockDesc> desc;
@@ -165,6 +166,15 @@ struct gv_ctx {
   // raw and block buffers instead of copying, so the last pool lives in the
   // block buffer and a replay re-arms it there (pending_in_blocks).
   bool pending_in_blocks = false;
+  // NEXT-1 (gv_augment_device_blocks): the pending pool was generated and
+  // bucketed on the device, into ranks[0].blocks_alt with its block offsets
+  // and error flag in fused_off; prepare swaps it in without a bucket pass.
+  bool fused_pending = false;
+  uint64_t fused_count = 0;
+  gv::DevBuf<uint64_t> fused_off;  // bins + 1 offsets, [bins + 1] = error flag
+  gv::DevBuf<uint8_t> aug_scratch;  // walk cache + counts of the fused sampler
+  cudaEvent_t fused_ready = nullptr;  // copy stream: the fused pool is complete
+  cudaEvent_t alt_free = nullptr;     // compute stream: blocks_alt no longer read
   bool swap_mode() const {
     return relabeled() && n == 1 && D == 1 && !hp() && !raw.host;
   }

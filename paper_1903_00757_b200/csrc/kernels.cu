@@ -858,6 +858,60 @@ __global__ void init_vertex_kernel(float* __restrict__ vertex, uint32_t stride, 
 // segment holds cap pairs, the last walk truncated as on the host.
 constexpr int kAugBlock = 128;
 
+// Walk w of segment t into my[0..L] (R-AUG): departure ∝ degree, then L
+// steps ∝ edge weight, Philox counter {w, step, t, 'WALK'}. Nodes are stored
+// in the pool's id space (g.relabel), the walk itself moves on original ids.
+__device__ __forceinline__ void walk_into(const WalkDev& g, uint32_t w, uint32_t t, uint32_t L,
+                                          uint32_t key0, uint32_t key1, uint32_t* my) {
+  u32x4 r = philox4x32_10(u32x4{w, 0u, t, kTagWalk}, key0, key1);
+  uint32_t slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, g.nv);
+  uint2 pa = __ldg(g.dalias + slot);
+  uint32_t x = alias_pick(pa.x, pa.y, slot, r.z);
+  my[0] = g.relabel ? __ldg(g.relabel + x) : x;
+  for (uint32_t k = 1; k <= L; ++k) {
+    const uint64_t o = __ldg(g.off + x);
+    const uint32_t m = static_cast<uint32_t>(__ldg(g.off + x + 1) - o);
+    r = philox4x32_10(u32x4{w, k, t, kTagWalk}, key0, key1);
+    slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, m);
+    pa = __ldg(g.ealias + o + slot);
+    x = __ldg(g.nbr + o + alias_pick(pa.x, pa.y, slot, r.z));
+    my[k] = g.relabel ? __ldg(g.relabel + x) : x;  // pairs in the pool's id space
+  }
+}
+
+// Pairs of a walk: (w_a, w_b), 0 < b - a <= s, w_a != w_b, by a then b.
+__device__ __forceinline__ uint32_t walk_pairs(const uint32_t* my, uint32_t L, uint32_t s) {
+  uint32_t c = 0;
+  for (uint32_t a = 0; a < L; ++a) {
+    const uint32_t xa = my[a], last = min(a + s, L);
+    for (uint32_t bb = a + 1; bb <= last; ++bb) c += (my[bb] != xa);
+  }
+  return c;
+}
+
+// Block-wide exclusive scan of c over the kAugBlock threads (walks of a
+// batch, in walk order): returns the walk's first pair index within the
+// batch; *total = the batch's pairs. warp_tot: kAugBlock / 32 words of smem.
+__device__ __forceinline__ uint32_t batch_scan(uint32_t c, uint32_t* warp_tot, uint32_t* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_tot[wid] = incl;
+  __syncthreads();
+  uint32_t before = 0, tot = 0;
+#pragma unroll
+  for (int q = 0; q < kAugBlock / 32; ++q) {
+    if (q < wid) before += warp_tot[q];
+    tot += warp_tot[q];
+  }
+  *total = tot;
+  return before + (incl - c);
+}
+
 __global__ void __launch_bounds__(kAugBlock) augment_kernel(WalkDev g, uint32_t L, uint32_t s,
                                                             uint32_t T, uint64_t count,
                                                             uint32_t key0, uint32_t key1,
@@ -868,7 +922,7 @@ __global__ void __launch_bounds__(kAugBlock) augment_kernel(WalkDev g, uint32_t 
   uint64_t* sub_start =  // [s], 8-byte aligned after the walks
       reinterpret_cast<uint64_t*>(sh + ((kAugBlock * (L + 1) + 1) & ~1u));
   __shared__ uint32_t warp_tot[kAugBlock / 32];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tid = threadIdx.x;
   const uint32_t W = L + 1;
   uint32_t* my = walks + tid * W;  // stride L+1 (odd when L is even: few bank conflicts)
   for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
@@ -884,44 +938,10 @@ __global__ void __launch_bounds__(kAugBlock) augment_kernel(WalkDev g, uint32_t 
     __syncthreads();
     uint64_t filled = 0;
     for (uint32_t base = 0; filled < cap; base += kAugBlock) {
-      const uint32_t w = base + tid;
-      // the walk (departure + L steps)
-      u32x4 r = philox4x32_10(u32x4{w, 0u, t, kTagWalk}, key0, key1);
-      uint32_t slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, g.nv);
-      uint2 pa = __ldg(g.dalias + slot);
-      uint32_t x = alias_pick(pa.x, pa.y, slot, r.z);
-      my[0] = g.relabel ? __ldg(g.relabel + x) : x;
-      for (uint32_t k = 1; k <= L; ++k) {
-        const uint64_t o = __ldg(g.off + x);
-        const uint32_t m = static_cast<uint32_t>(__ldg(g.off + x + 1) - o);
-        r = philox4x32_10(u32x4{w, k, t, kTagWalk}, key0, key1);
-        slot = slot_of((static_cast<uint64_t>(r.x) << 32) | r.y, m);
-        pa = __ldg(g.ealias + o + slot);
-        x = __ldg(g.nbr + o + alias_pick(pa.x, pa.y, slot, r.z));
-        my[k] = g.relabel ? __ldg(g.relabel + x) : x;  // pairs in the pool's id space
-      }
-      // its pair count
-      uint32_t c = 0;
-      for (uint32_t a = 0; a < L; ++a) {
-        const uint32_t xa = my[a], last = min(a + s, L);
-        for (uint32_t bb = a + 1; bb <= last; ++bb) c += (my[bb] != xa);
-      }
-      // block exclusive scan of the counts
-      uint32_t incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (lane == 31) warp_tot[wid] = incl;
-      __syncthreads();
-      uint32_t before = 0, total = 0;
-#pragma unroll
-      for (int q = 0; q < kAugBlock / 32; ++q) {
-        if (q < wid) before += warp_tot[q];
-        total += warp_tot[q];
-      }
-      uint64_t k = filled + before + (incl - c);
+      walk_into(g, base + tid, t, L, key0, key1, my);
+      const uint32_t c = walk_pairs(my, L, s);
+      uint32_t total;
+      uint64_t k = filled + batch_scan(c, warp_tot, &total);
       // write this walk's pairs at their pseudo-shuffled positions
       for (uint32_t a = 0; a < L && k < cap; ++a) {
         const uint32_t xa = my[a], last = min(a + s, L);
@@ -1307,6 +1327,171 @@ __global__ void bucket_adjust_kernel(const uint64_t* __restrict__ dst_off,
   }
 }
 
+// ------------------------------- augmentation straight into blocks (NEXT-1)
+// The device sampler's pool bucketed without ever being written as a raw
+// pool (Alg. 2 P:176-196 + a3-a5). The result is the
+// stable counting sort of the pool augment_kernel would write — block (i, j)
+// = its samples in pool order — so it equals or_bucket(or_augment(...)).
+// Pool order within segment t is (sub-block j = k mod S, then k), S = s
+// (pseudo shuffle) or 1 (no shuffle), k = the pair's index in the
+// segment in walk order. Hence a pair's slot in its block is
+//   block_off[bin] + (pairs of bin in segments < t, and in sub-blocks < j of
+//   segment t) + (pairs of bin in sub-block j of segment t before k).
+// Pass 1 (augment_count_kernel): the walks as augment_kernel draws them; the
+// walk nodes and each walk's (truncated) pair count go to a walk cache
+// (~ 4 B per pair: a walk of L + 1 nodes yields >= L pairs, since self-loops
+// are dropped at ingest), and cnt[bin][t S + j] counts pairs per (segment,
+// sub-block, bin). The bucket scans turn cnt into offsets.
+// Pass 2 (augment_place_kernel): one warp per (segment, sub-block j) replays
+// the cached walks in order, keeps the pairs with k mod S = j, ranks them per
+// bin in k order (ballot + match_any within 32 pairs, running counters in
+// shared memory) and stores the local ids at their slots.
+struct WalkCache {
+  uint32_t* nodes;   // [T][wmax][L + 1]
+  uint32_t* pairs;   // [T][wmax]: pairs of each walk after truncation at cap
+  uint32_t* nwalks;  // [T]
+  uint32_t wmax;
+};
+
+__device__ __forceinline__ uint32_t pair_bin(const BinCtx& b, uint32_t x, uint32_t y, uint2& local) {
+  const uint32_t a = packed_of(b, x), c = packed_of(b, y);
+  if (b.pbits == 0) {
+    local = make_uint2(a, c);
+    return 0;
+  }
+  const uint32_t sh = 32 - b.pbits, mask = (1u << sh) - 1u;
+  local = make_uint2(a & mask, c & mask);
+  return (a >> sh) * b.n + (c >> sh);
+}
+
+__global__ void __launch_bounds__(kAugBlock) augment_count_kernel(
+    WalkDev g, uint32_t L, uint32_t s, uint32_t S, uint32_t T, uint64_t count, uint32_t key0,
+    uint32_t key1, BinCtx b, uint32_t bins, WalkCache wc, uint32_t* __restrict__ cnt,
+    uint32_t* err) {
+  extern __shared__ uint32_t sh[];
+  uint32_t* hist = sh;                   // [S][bins]
+  uint32_t* walks = sh + S * bins;       // [kAugBlock][L+1]
+  __shared__ uint32_t warp_tot[kAugBlock / 32];
+  __shared__ uint32_t used;              // walks of the segment that hold pairs
+  const int tid = threadIdx.x;
+  const uint32_t W = L + 1;
+  uint32_t* my = walks + tid * W;
+  for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
+    const uint64_t cap = count * (t + 1) / T - count * t / T;
+    for (uint32_t q = tid; q < S * bins; q += kAugBlock) hist[q] = 0;
+    if (tid == 0) used = 0;
+    __syncthreads();
+    uint64_t filled = 0;
+    for (uint32_t base = 0; filled < cap; base += kAugBlock) {
+      const uint32_t w = base + tid;
+      walk_into(g, w, t, L, key0, key1, my);
+      const uint32_t c = walk_pairs(my, L, s);
+      uint32_t total;
+      const uint64_t k0 = filled + batch_scan(c, warp_tot, &total);
+      const uint32_t cw = k0 >= cap ? 0u : static_cast<uint32_t>(umin64(c, cap - k0));
+      if (cw > 0) {
+        if (w >= wc.wmax) {
+          *err = 2u;  // internal: walk cache bound violated
+        } else {
+          uint32_t* dst = wc.nodes + (static_cast<uint64_t>(t) * wc.wmax + w) * W;
+          for (uint32_t q = 0; q <= L; ++q) dst[q] = my[q];
+          wc.pairs[static_cast<uint64_t>(t) * wc.wmax + w] = cw;
+          atomicMax(&used, w + 1);
+        }
+        uint64_t k = k0;
+        for (uint32_t a = 0; a < L && k < k0 + cw; ++a) {
+          const uint32_t xa = my[a], last = min(a + s, L);
+          for (uint32_t bb = a + 1; bb <= last && k < k0 + cw; ++bb) {
+            const uint32_t xb = my[bb];
+            if (xb == xa) continue;
+            uint2 loc;
+            const uint32_t bin = pair_bin(b, xa, xb, loc);
+            atomicAdd(&hist[static_cast<uint32_t>(k % S) * bins + bin], 1u);
+            ++k;
+          }
+        }
+      }
+      filled += total;
+      __syncthreads();  // warp_tot reuse
+    }
+    for (uint32_t q = tid; q < S * bins; q += kAugBlock) {
+      const uint32_t j = q / bins, bin = q - j * bins;
+      cnt[static_cast<uint64_t>(bin) * T * S + static_cast<uint64_t>(t) * S + j] = hist[q];
+    }
+    if (tid == 0) wc.nwalks[t] = used;
+    __syncthreads();
+  }
+}
+
+// blockDim = 32 S: warp j places sub-block j of each segment of the CTA.
+__global__ void augment_place_kernel(uint32_t L, uint32_t s, uint32_t S, uint32_t T, BinCtx b,
+                                     uint32_t bins, WalkCache wc, const uint32_t* __restrict__ cnt,
+                                     const uint64_t* __restrict__ block_off,
+                                     uint2* __restrict__ out) {
+  extern __shared__ uint32_t sh[];
+  const uint32_t lane = threadIdx.x & 31, j = threadIdx.x >> 5;
+  const uint32_t W = L + 1;
+  uint32_t* run = sh + j * (bins + W);  // per-bin running ranks of this warp's sub-block
+  uint32_t* walk = run + bins;
+  const uint32_t lt = (1u << lane) - 1u;
+  // candidates (a, a + d), d = 1..s, by a then d: the full part a <= L - s
+  // has s each; the tail a > L - s has L - a each
+  const uint32_t full_a = L >= s ? L - s + 1 : 0, full = full_a * s;
+  const uint32_t ncand = full + (L >= s ? s * (s - 1) / 2 : L * (L + 1) / 2);
+  for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
+    for (uint32_t q = lane; q < bins; q += 32) run[q] = 0;
+    __syncwarp();
+    const uint64_t tS = static_cast<uint64_t>(t) * S + j;
+    const uint32_t nw = wc.nwalks[t];
+    uint64_t k0 = 0;
+    for (uint32_t w = 0; w < nw; ++w) {
+      const uint64_t widx = static_cast<uint64_t>(t) * wc.wmax + w;
+      const uint32_t* src = wc.nodes + widx * W;
+      for (uint32_t q = lane; q < W; q += 32) walk[q] = src[q];
+      const uint32_t cw = wc.pairs[widx];
+      __syncwarp();
+      uint32_t qbase = 0;  // valid pairs of the walk before this round
+      for (uint32_t c0 = 0; c0 < ncand && qbase < cw; c0 += 32) {
+        const uint32_t ci = c0 + lane;
+        uint32_t a = 0, d = 1;
+        bool valid = false;
+        if (ci < ncand) {
+          if (ci < full) {
+            a = ci / s;
+            d = ci - a * s + 1;
+          } else {  // tail: a = full_a + r, with L - a candidates each
+            uint32_t u = ci - full;
+            a = full_a;
+            while (u >= L - a) {
+              u -= L - a;
+              ++a;
+            }
+            d = u + 1;
+          }
+          valid = walk[a] != walk[a + d];
+        }
+        const uint32_t vmask = __ballot_sync(kFull, valid);
+        const uint32_t q = qbase + __popc(vmask & lt);
+        const bool mine = valid && q < cw && ((k0 + q) % S) == j;
+        uint2 loc = make_uint2(0, 0);
+        const uint32_t bin = mine ? pair_bin(b, walk[a], walk[a + d], loc) : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(kFull, bin);
+        if (mine) {
+          const uint32_t rank = run[bin] + __popc(peers & lt);
+          const uint64_t slot = block_off[bin] + cnt[static_cast<uint64_t>(bin) * T * S + tS] + rank;
+          out[slot] = loc;
+        }
+        __syncwarp();
+        if (mine && (peers >> lane) == 1u) run[bin] += __popc(peers);  // highest peer lane
+        __syncwarp();
+        qbase += __popc(vmask);
+      }
+      k0 += cw;
+    }
+    __syncwarp();
+  }
+}
+
 // Per-device launch caches: a process may drive contexts on several devices
 // (gv_options.device), and function attributes / occupancy are per device.
 constexpr int kMaxDev = 64;
@@ -1632,6 +1817,82 @@ cudaError_t launch_augment(const WalkDev& g, uint32_t walk_len, uint32_t s, uint
                                                 static_cast<uint32_t>(seed),
                                                 static_cast<uint32_t>(seed >> 32),
                                                 shuffle == 1 ? 1u : 0u, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------- augmentation straight into blocks (host)
+namespace {
+struct AugBlocksLayout {
+  uint32_t S, bins, wmax, T;
+  size_t nodes, pairs, nwalks, cnt, tot, end;
+  AugBlocksLayout(uint32_t L, uint32_t s, uint32_t shuffle, uint32_t n, uint32_t segments,
+                  uint64_t count) {
+    S = shuffle == 1 ? 1 : s;
+    bins = n * n;
+    T = segments;
+    const uint64_t cap_max = (count + segments - 1) / segments;
+    wmax = static_cast<uint32_t>(cap_max / std::max<uint32_t>(L, 1) + 2);
+    const uint64_t walks = static_cast<uint64_t>(T) * wmax;
+    nodes = 0;
+    pairs = align256(walks * (L + 1) * 4);
+    nwalks = pairs + align256(walks * 4);
+    cnt = nwalks + align256(static_cast<size_t>(T) * 4);
+    tot = cnt + align256(static_cast<size_t>(bins) * T * S * 4);
+    end = tot + align256(static_cast<size_t>(bins) * 8);
+  }
+  size_t smem_count(uint32_t L) const { return (static_cast<size_t>(S) * bins + kAugBlock * (L + 1)) * 4; }
+  size_t smem_place(uint32_t L) const { return static_cast<size_t>(S) * (bins + L + 1) * 4; }
+};
+constexpr size_t kAugSmemMax = 200 * 1024;
+}  // namespace
+
+size_t augment_blocks_scratch_bytes(uint32_t walk_len, uint32_t s, uint32_t shuffle, uint32_t n,
+                                    uint32_t segments, uint64_t count) {
+  const AugBlocksLayout Lo(walk_len, s, shuffle, n, segments, count);
+  if (shuffle > 1 || Lo.S > 32 || count > 0xFFFFFFFFull || segments == 0 ||
+      Lo.smem_count(walk_len) > kAugSmemMax || Lo.smem_place(walk_len) > kAugSmemMax)
+    return 0;  // not eligible: the caller augments into a raw pool and buckets it
+  return Lo.end;
+}
+
+cudaError_t launch_augment_blocks(const WalkDev& g, uint32_t walk_len, uint32_t s,
+                                  uint32_t segments, uint64_t count, uint64_t seed,
+                                  uint32_t shuffle, const IdMap& ids, uint32_t n, void* scratch,
+                                  uint64_t* block_off, uint32_t* err, uint2* out, cudaStream_t st,
+                                  int* launches) {
+  if (augment_blocks_scratch_bytes(walk_len, s, shuffle, n, segments, count) == 0)
+    return cudaErrorInvalidValue;
+  const AugBlocksLayout Lo(walk_len, s, shuffle, n, segments, count);
+  char* base = static_cast<char*>(scratch);
+  WalkCache wc{reinterpret_cast<uint32_t*>(base + Lo.nodes), reinterpret_cast<uint32_t*>(base + Lo.pairs),
+               reinterpret_cast<uint32_t*>(base + Lo.nwalks), Lo.wmax};
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(base + Lo.cnt);
+  uint64_t* tot = reinterpret_cast<uint64_t*>(base + Lo.tot);
+  BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, n};
+  const size_t sm1 = Lo.smem_count(walk_len), sm2 = Lo.smem_place(walk_len);
+  static size_t set1[kMaxDev] = {}, set2[kMaxDev] = {};
+  size_t& d1 = set1[cur_dev()];
+  size_t& d2 = set2[cur_dev()];
+  if (sm1 > 48 * 1024 && sm1 > d1) {
+    cudaFuncSetAttribute(augment_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sm1));
+    d1 = sm1;
+  }
+  if (sm2 > 48 * 1024 && sm2 > d2) {
+    cudaFuncSetAttribute(augment_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sm2));
+    d2 = sm2;
+  }
+  const unsigned grid = std::min<uint32_t>(segments, static_cast<uint32_t>(num_sms()) * 16);
+  augment_count_kernel<<<grid, kAugBlock, sm1, st>>>(g, walk_len, s, Lo.S, segments, count,
+                                                     static_cast<uint32_t>(seed),
+                                                     static_cast<uint32_t>(seed >> 32), b, Lo.bins,
+                                                     wc, cnt, err);
+  bucket_scan_bins_kernel<<<Lo.bins, 1024, 0, st>>>(cnt, static_cast<uint64_t>(segments) * Lo.S, tot);
+  bucket_scan_totals_kernel<<<1, 1024, 0, st>>>(tot, Lo.bins, block_off);
+  augment_place_kernel<<<grid, 32 * Lo.S, sm2, st>>>(walk_len, s, Lo.S, segments, b, Lo.bins, wc,
+                                                      cnt, block_off, out);
+  if (launches) *launches += 4;
   return cudaGetLastError();
 }
 

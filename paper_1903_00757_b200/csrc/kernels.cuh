@@ -125,6 +125,22 @@ cudaError_t launch_bucket(const uint2* in, uint64_t count, const IdMap& ids,
 cudaError_t launch_bucket_count(const uint2* in, uint64_t count, const IdMap& ids,
                                 const BucketPlan& plan, void* scratch, uint64_t* block_off_dev, uint32_t* err_dev,
                                 cudaStream_t s, int* launches);
+// NEXT-1: device augmentation straight into the n x n blocks (no raw pool):
+// the blocks and block_off (bins + 1) that launch_bucket would produce from
+// launch_augment's pool with the same arguments. Scratch: a walk cache
+// (~4 B per pair) and the per-(segment, sub-block, bin) counts.
+// augment_blocks_scratch_bytes returns 0 when the shape is not eligible
+// (shuffle = random, s > 32 with the pseudo shuffle, count >= 2^32, or the
+// per-CTA tables exceed shared memory); callers then use launch_augment +
+// launch_bucket. err: 2 if the walk cache bound is violated (internal).
+size_t augment_blocks_scratch_bytes(uint32_t walk_len, uint32_t s, uint32_t shuffle, uint32_t n,
+                                    uint32_t segments, uint64_t count);
+cudaError_t launch_augment_blocks(const WalkDev& g, uint32_t walk_len, uint32_t s,
+                                  uint32_t segments, uint64_t count, uint64_t seed,
+                                  uint32_t shuffle, const IdMap& ids, uint32_t n, void* scratch,
+                                  uint64_t* block_off_dev, uint32_t* err_dev, uint2* out,
+                                  cudaStream_t st, int* launches);
+
 // a3 of a relabelled pool at n = 1: range check only (err_dev), block_off =
 // {0, count}; the pool is trained where it lies.
 cudaError_t launch_validate(const uint2* in, uint64_t count, uint32_t nv, uint64_t* block_off_dev,

@@ -6,6 +6,7 @@
 
 #include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -43,12 +44,23 @@ extern "C" gv_status gv_run(gv_ctx* c, const gv_augment_cfg* cfg, uint64_t total
   if (cfg->device) {
     // GPU-resident pipeline (NEXT-1): pool k+1 is generated on the copy
     // stream while pool k trains on the compute stream.
-    status = gv_augment_device(c, cfg->walk_len, cfg->s, cfg->threads, pool_count(0), cfg->seed);
+    // Pools are bucketed inside the sampler (gv_augment_device_blocks) when
+    // the shape allows it, else generated raw and bucketed by the trainer.
+    // (GV_AUG_BLOCKS=0: always raw pools, for A/B measurements)
+    const char* env = getenv("GV_AUG_BLOCKS");
+    const bool blocks = !(env && atoi(env) == 0) &&
+                        gv_augment_device_blocks(c, cfg->walk_len, cfg->s, cfg->threads,
+                                                 pool_count(0), cfg->seed, GV_SHUFFLE_PSEUDO) == GV_OK;
+    auto produce = [&](uint64_t k) {
+      return blocks ? gv_augment_device_blocks(c, cfg->walk_len, cfg->s, cfg->threads,
+                                               pool_count(k), cfg->seed + k, GV_SHUFFLE_PSEUDO)
+                    : gv_augment_device(c, cfg->walk_len, cfg->s, cfg->threads, pool_count(k),
+                                        cfg->seed + k);
+    };
+    if (!blocks) status = produce(0);
     for (uint64_t k = 0; k < npools && status == GV_OK; ++k) {
       status = gv_train_episode(c, nullptr);
-      if (status == GV_OK && k + 1 < npools)
-        status = gv_augment_device(c, cfg->walk_len, cfg->s, cfg->threads, pool_count(k + 1),
-                                   cfg->seed + k + 1);
+      if (status == GV_OK && k + 1 < npools) status = produce(k + 1);
       if (status == GV_OK && !cfg->collaborate) status = gv_synchronize(c);
     }
     if (status == GV_OK) status = gv_synchronize(c);

@@ -117,6 +117,8 @@ SIGNATURES = {
     "gv_augment_device": (st, [ctx_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64]),
     "gv_augment_device_ex": (st, [ctx_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
                                   C.c_int]),
+    "gv_augment_device_blocks": (st, [ctx_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                      C.c_uint64, C.c_int]),
     "gv_debug_get_pending": (st, [ctx_p, u32p, C.c_uint64, u64p]),
     "gv_get_partition": (st, [ctx_p, u32p, u64p]),
     "gv_get_alias": (st, [ctx_p, C.c_uint32, u32p, u32p, C.c_uint64]),
@@ -295,6 +297,10 @@ def gv_augment_device_ex(ctx, walk_len, s, segments, count, seed, shuffle):
     _ck(lib.gv_augment_device_ex(ctx, walk_len, s, segments, count, seed, shuffle), ctx)
 
 
+def gv_augment_device_blocks(ctx, walk_len, s, segments, count, seed, shuffle=GV_SHUFFLE_PSEUDO):
+    _ck(lib.gv_augment_device_blocks(ctx, walk_len, s, segments, count, seed, shuffle), ctx)
+
+
 def gv_debug_get_pending(ctx):
     n = C.c_uint64(0)
     _ck(lib.gv_debug_get_pending(ctx, None, 0, C.byref(n)), ctx)
@@ -440,6 +446,9 @@ class GraphVite:
 
     def augment_device(self, walk_len, s, segments, count, seed, shuffle=GV_SHUFFLE_PSEUDO):
         gv_augment_device_ex(self.ctx, walk_len, s, segments, count, seed, shuffle)
+
+    def augment_device_blocks(self, walk_len, s, segments, count, seed, shuffle=GV_SHUFFLE_PSEUDO):
+        gv_augment_device_blocks(self.ctx, walk_len, s, segments, count, seed, shuffle)
 
     def partition(self):
         return gv_get_partition(self.ctx, self.nv, self.n)

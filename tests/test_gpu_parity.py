@@ -758,3 +758,63 @@ def test_relabeled_augmentation_and_range_check(c1_graph, n):
     assert np.array_equal(b.vertex(), V0)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("n,ids,segments,s,count", [
+    (1, G.GV_IDS_ORIGINAL, 7, 2, 100_003), (4, G.GV_IDS_ORIGINAL, 1184, 5, 2_000_000),
+    (4, G.GV_IDS_RELABELED, 64, 3, 250_001), (16, G.GV_IDS_RELABELED, 96, 2, 300_000),
+    (16, G.GV_IDS_ORIGINAL, 3, 5, 17), (8, G.GV_IDS_RELABELED, 1184, 5, 1_000_003),
+    (32, G.GV_IDS_ORIGINAL, 200, 1, 400_000)])
+def test_device_blocks_bitexact(c1_graph, n, ids, segments, s, count):
+    """NEXT-1, "writing bucketed blocks directly" (gv_augment_device_blocks):
+    the walks write their pairs straight into the n x n blocks — no raw pool,
+    no bucketing launch in the pool's training — and the blocks equal
+    or_bucket(or_augment(...)) byte for byte: the oracle's augmentation
+    (threads = segments) stable-sorted by block, ragged segments and the
+    truncated last walk of each segment included."""
+    src, dst = c1_graph
+    p = G.GraphVite(C1["nv"], 8, n, 1, 0.025, pool_ids=ids)
+    p.load_edges(src, dst)
+    p.augment_device_blocks(40, s, segments, count, 4242)
+    assert len(G.gv_debug_get_pending(p.ctx)) == 0  # nothing went through a raw pool
+    G.gv_prepare_episode(p.ctx)
+    got, boff = G.gv_debug_get_buckets(p.ctx, n, count)
+    ref = O.Sampler(O.Graph(C1["nv"], src, dst)).augment(40, s, segments, count, 4242)
+    o = O.Trainer(C1["nv"], 8, n)
+    o.load_edges(src, dst)
+    perm, off = o.partition()
+    exp, eoff = O.bucket(ref, C1["nv"], perm, off, n)
+    assert np.array_equal(boff, eoff)
+    assert np.array_equal(got, exp)
+    st = p.train_episode()
+    assert st["kernel_launches"] == st["sgd_launches"]  # the pool's training launched no bucketing
+    with pytest.raises(G.GVError):
+        p.replay()
+    p.close()
+
+
+@pytest.mark.parametrize("n,ids", [(4, G.GV_IDS_ORIGINAL), (8, G.GV_IDS_RELABELED)])
+def test_device_blocks_pools_train_like_oracle(c1_graph, n, ids):
+    """Pools bucketed in the sampler, pool k+1 generated on the copy stream
+    while pool k trains (the two block buffers alternate), ordered kernel:
+    equals the oracle trained on its own augmentation of the same seeds; a
+    second sampler call while a pool is pending is refused."""
+    src, dst = c1_graph
+    P, pools, segs = 250_000, 3, 96
+    g = G.GraphVite(C1["nv"], 64, n, 1, 0.025, total_samples=P * pools, ordered=1, pool_ids=ids)
+    g.load_edges(src, dst)
+    g.augment_device_blocks(40, 2, segs, P, 500)
+    with pytest.raises(G.GVError):
+        g.augment_device_blocks(40, 2, segs, P, 501)
+    for k in range(pools):
+        g.train_episode(stats=False)
+        if k + 1 < pools:
+            g.augment_device_blocks(40, 2, segs, P, 501 + k)
+    o = O.Trainer(C1["nv"], 64, n, K=1, lr0=0.025, lr_kind=1, total_samples=P * pools)
+    o.load_edges(src, dst)
+    sampler = O.Sampler(O.Graph(C1["nv"], src, dst))
+    for k in range(pools):
+        o.train_pool(sampler.augment(40, 2, segs, P, 500 + k))
+    assert_matrix_parity(g.vertex(), o.get("vertex"), "vertex")
+    assert_matrix_parity(g.context(), o.get("context"), "context")
+    g.close()
