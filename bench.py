@@ -332,7 +332,7 @@ def measure(args, world, rank, dev, n, *, steps, warmup, e2e=True, pipeline=True
         src, dst = make_graph()
     t_gen = time.perf_counter() - t0
     P = CFG["pool"]
-    total_samples = P * n * (warmup + steps + (steps if e2e else 0) + 1)
+    total_samples = P * world * args.vranks * (warmup + steps + (steps if e2e else 0) + 1)
     g = G.GraphVite(CFG["nv"], CFG["d"], n, CFG["K"], CFG["lr"], total_samples=total_samples,
                     neg_weight=CFG["neg_weight"], seed=CFG["seed"],
                     device=dev, rank=rank, world_size=world, ordered=1 if args.ordered else 0,

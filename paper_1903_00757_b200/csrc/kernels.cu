@@ -1334,23 +1334,27 @@ __global__ void bucket_adjust_kernel(const uint64_t* __restrict__ dst_off,
 // = its samples in pool order — so it equals or_bucket(or_augment(...)).
 // Pool order within segment t is (sub-block j = k mod S, then k), S = s
 // (pseudo shuffle) or 1 (no shuffle), k = the pair's index in the
-// segment in walk order. Hence a pair's slot in its block is
-//   block_off[bin] + (pairs of bin in segments < t, and in sub-blocks < j of
-//   segment t) + (pairs of bin in sub-block j of segment t before k).
+// segment in walk order. Walks come in batches of kAugBlock, and batch b of
+// segment t holds a contiguous k range, so a pair's slot in its block is
+//   block_off[bin] + (pairs of bin in tiles before (t, j, b), tiles ordered
+//   by segment, then sub-block, then batch) + (its rank among the pairs of
+//   bin in tile (t, j, b), in k order).
 // Pass 1 (augment_count_kernel): the walks as augment_kernel draws them; the
-// walk nodes and each walk's (truncated) pair count go to a walk cache
-// (~ 4 B per pair: a walk of L + 1 nodes yields >= L pairs, since self-loops
-// are dropped at ingest), and cnt[bin][t S + j] counts pairs per (segment,
-// sub-block, bin). The bucket scans turn cnt into offsets.
-// Pass 2 (augment_place_kernel): one warp per (segment, sub-block j) replays
-// the cached walks in order, keeps the pairs with k mod S = j, ranks them per
-// bin in k order (ballot + match_any within 32 pairs, running counters in
-// shared memory) and stores the local ids at their slots.
+// walk nodes and each walk's (truncated) pair count go to a walk cache (<= 4 B
+// per pair: a walk of L + 1 nodes yields >= L pairs, since self-loops are
+// dropped at ingest), each batch's first k to bk0, and cnt[bin][tile] counts
+// pairs per tile. The bucket scans turn cnt into offsets.
+// Pass 2 (augment_place_kernel): one warp per (segment, batch) replays the
+// batch's cached walks in order, enumerates each walk's candidate pairs 32 at
+// a time (ballot of the valid ones gives each pair's k), ranks them per
+// (sub-block, bin) with __match_any_sync against running counters in shared
+// memory and stores the local ids at their slots.
 struct WalkCache {
   uint32_t* nodes;   // [T][wmax][L + 1]
   uint32_t* pairs;   // [T][wmax]: pairs of each walk after truncation at cap
   uint32_t* nwalks;  // [T]
-  uint32_t wmax;
+  uint64_t* bk0;     // [T][nb]: k of the first pair of batch b
+  uint32_t wmax, nb;
 };
 
 __device__ __forceinline__ uint32_t pair_bin(const BinCtx& b, uint32_t x, uint32_t y, uint2& local) {
@@ -1364,31 +1368,39 @@ __device__ __forceinline__ uint32_t pair_bin(const BinCtx& b, uint32_t x, uint32
   return (a >> sh) * b.n + (c >> sh);
 }
 
+// tile (t, j, batch) of the scan; cnt is bin-major: cnt[bin * tiles + tile]
+__device__ __forceinline__ uint64_t aug_tile(uint32_t t, uint32_t j, uint32_t batch, uint32_t S,
+                                             uint32_t nb) {
+  return (static_cast<uint64_t>(t) * S + j) * nb + batch;
+}
+
 __global__ void __launch_bounds__(kAugBlock) augment_count_kernel(
     WalkDev g, uint32_t L, uint32_t s, uint32_t S, uint32_t T, uint64_t count, uint32_t key0,
     uint32_t key1, BinCtx b, uint32_t bins, WalkCache wc, uint32_t* __restrict__ cnt,
     uint32_t* err) {
   extern __shared__ uint32_t sh[];
-  uint32_t* hist = sh;                   // [S][bins]
+  uint32_t* hist = sh;                   // [S][bins] of the current batch
   uint32_t* walks = sh + S * bins;       // [kAugBlock][L+1]
   __shared__ uint32_t warp_tot[kAugBlock / 32];
   __shared__ uint32_t used;              // walks of the segment that hold pairs
   const int tid = threadIdx.x;
   const uint32_t W = L + 1;
+  const uint64_t tiles = static_cast<uint64_t>(T) * S * wc.nb;
   uint32_t* my = walks + tid * W;
+  for (uint32_t q = tid; q < S * bins; q += kAugBlock) hist[q] = 0;
   for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
     const uint64_t cap = count * (t + 1) / T - count * t / T;
-    for (uint32_t q = tid; q < S * bins; q += kAugBlock) hist[q] = 0;
     if (tid == 0) used = 0;
     __syncthreads();
     uint64_t filled = 0;
-    for (uint32_t base = 0; filled < cap; base += kAugBlock) {
+    for (uint32_t base = 0, batch = 0; filled < cap; base += kAugBlock, ++batch) {
       const uint32_t w = base + tid;
       walk_into(g, w, t, L, key0, key1, my);
       const uint32_t c = walk_pairs(my, L, s);
       uint32_t total;
       const uint64_t k0 = filled + batch_scan(c, warp_tot, &total);
       const uint32_t cw = k0 >= cap ? 0u : static_cast<uint32_t>(umin64(c, cap - k0));
+      if (tid == 0 && batch < wc.nb) wc.bk0[static_cast<uint64_t>(t) * wc.nb + batch] = filled;
       if (cw > 0) {
         if (w >= wc.wmax) {
           *err = 2u;  // internal: walk cache bound violated
@@ -1412,41 +1424,49 @@ __global__ void __launch_bounds__(kAugBlock) augment_count_kernel(
         }
       }
       filled += total;
-      __syncthreads();  // warp_tot reuse
-    }
-    for (uint32_t q = tid; q < S * bins; q += kAugBlock) {
-      const uint32_t j = q / bins, bin = q - j * bins;
-      cnt[static_cast<uint64_t>(bin) * T * S + static_cast<uint64_t>(t) * S + j] = hist[q];
+      __syncthreads();  // hist complete, warp_tot reusable
+      if (batch < wc.nb)
+        for (uint32_t q = tid; q < S * bins; q += kAugBlock) {
+          const uint32_t j = q / bins, bin = q - j * bins;
+          cnt[static_cast<uint64_t>(bin) * tiles + aug_tile(t, j, batch, S, wc.nb)] = hist[q];
+          hist[q] = 0;
+        }
+      __syncthreads();
     }
     if (tid == 0) wc.nwalks[t] = used;
-    __syncthreads();
   }
 }
 
-// blockDim = 32 S: warp j places sub-block j of each segment of the CTA.
-__global__ void augment_place_kernel(uint32_t L, uint32_t s, uint32_t S, uint32_t T, BinCtx b,
-                                     uint32_t bins, WalkCache wc, const uint32_t* __restrict__ cnt,
-                                     const uint64_t* __restrict__ block_off,
-                                     uint2* __restrict__ out) {
+// 4 warps per CTA; warp q of CTA c places tile (segment, batch) = 4 c + q
+// (grid-stride): all sub-blocks of that batch.
+constexpr int kPlaceWarps = 4;
+__global__ void __launch_bounds__(32 * kPlaceWarps) augment_place_kernel(
+    uint32_t L, uint32_t s, uint32_t S, uint32_t T, BinCtx b, uint32_t bins, WalkCache wc,
+    const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ block_off,
+    uint2* __restrict__ out) {
   extern __shared__ uint32_t sh[];
-  const uint32_t lane = threadIdx.x & 31, j = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
   const uint32_t W = L + 1;
-  uint32_t* run = sh + j * (bins + W);  // per-bin running ranks of this warp's sub-block
-  uint32_t* walk = run + bins;
+  uint32_t* run = sh + wq * (S * bins + W);  // running ranks per (sub-block, bin) of this tile
+  uint32_t* walk = run + S * bins;
   const uint32_t lt = (1u << lane) - 1u;
+  const uint64_t tiles = static_cast<uint64_t>(T) * S * wc.nb;
   // candidates (a, a + d), d = 1..s, by a then d: the full part a <= L - s
   // has s each; the tail a > L - s has L - a each
   const uint32_t full_a = L >= s ? L - s + 1 : 0, full = full_a * s;
   const uint32_t ncand = full + (L >= s ? s * (s - 1) / 2 : L * (L + 1) / 2);
-  for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
-    for (uint32_t q = lane; q < bins; q += 32) run[q] = 0;
-    __syncwarp();
-    const uint64_t tS = static_cast<uint64_t>(t) * S + j;
-    const uint32_t nw = wc.nwalks[t];
-    uint64_t k0 = 0;
-    for (uint32_t w = 0; w < nw; ++w) {
+  const uint64_t ntile = static_cast<uint64_t>(T) * wc.nb;
+  for (uint64_t tb = static_cast<uint64_t>(blockIdx.x) * kPlaceWarps + wq; tb < ntile;
+       tb += static_cast<uint64_t>(gridDim.x) * kPlaceWarps) {
+    const uint32_t t = static_cast<uint32_t>(tb / wc.nb), batch = static_cast<uint32_t>(tb % wc.nb);
+    const uint32_t w0 = batch * kAugBlock, nw = min(wc.nwalks[t], w0 + kAugBlock);
+    if (w0 >= nw) continue;  // warp-uniform
+    for (uint32_t q = lane; q < S * bins; q += 32) run[q] = 0;
+    uint64_t k0 = wc.bk0[static_cast<uint64_t>(t) * wc.nb + batch];
+    for (uint32_t w = w0; w < nw; ++w) {
       const uint64_t widx = static_cast<uint64_t>(t) * wc.wmax + w;
       const uint32_t* src = wc.nodes + widx * W;
+      __syncwarp();
       for (uint32_t q = lane; q < W; q += 32) walk[q] = src[q];
       const uint32_t cw = wc.pairs[widx];
       __syncwarp();
@@ -1472,23 +1492,26 @@ __global__ void augment_place_kernel(uint32_t L, uint32_t s, uint32_t S, uint32_
         }
         const uint32_t vmask = __ballot_sync(kFull, valid);
         const uint32_t q = qbase + __popc(vmask & lt);
-        const bool mine = valid && q < cw && ((k0 + q) % S) == j;
+        const bool mine = valid && q < cw;
         uint2 loc = make_uint2(0, 0);
-        const uint32_t bin = mine ? pair_bin(b, walk[a], walk[a + d], loc) : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(kFull, bin);
+        const uint32_t j = static_cast<uint32_t>((k0 + q) % S);
+        const uint32_t bin = mine ? pair_bin(b, walk[a], walk[a + d], loc) : 0;
+        const uint32_t key = mine ? j * bins + bin : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(kFull, key);
         if (mine) {
-          const uint32_t rank = run[bin] + __popc(peers & lt);
-          const uint64_t slot = block_off[bin] + cnt[static_cast<uint64_t>(bin) * T * S + tS] + rank;
+          const uint32_t rank = run[key] + __popc(peers & lt);
+          const uint64_t slot = block_off[bin] +
+                                cnt[static_cast<uint64_t>(bin) * tiles + aug_tile(t, j, batch, S, wc.nb)] +
+                                rank;
           out[slot] = loc;
         }
         __syncwarp();
-        if (mine && (peers >> lane) == 1u) run[bin] += __popc(peers);  // highest peer lane
+        if (mine && (peers >> lane) == 1u) run[key] += __popc(peers);  // highest peer lane
         __syncwarp();
         qbase += __popc(vmask);
       }
       k0 += cw;
     }
-    __syncwarp();
   }
 }
 
@@ -1823,8 +1846,9 @@ cudaError_t launch_augment(const WalkDev& g, uint32_t walk_len, uint32_t s, uint
 // ------------------------------- augmentation straight into blocks (host)
 namespace {
 struct AugBlocksLayout {
-  uint32_t S, bins, wmax, T;
-  size_t nodes, pairs, nwalks, cnt, tot, end;
+  uint32_t S, bins, wmax, T, nb;
+  size_t nodes, pairs, nwalks, bk0, cnt, tot, end;
+  uint64_t tiles;
   AugBlocksLayout(uint32_t L, uint32_t s, uint32_t shuffle, uint32_t n, uint32_t segments,
                   uint64_t count) {
     S = shuffle == 1 ? 1 : s;
@@ -1832,16 +1856,21 @@ struct AugBlocksLayout {
     T = segments;
     const uint64_t cap_max = (count + segments - 1) / segments;
     wmax = static_cast<uint32_t>(cap_max / std::max<uint32_t>(L, 1) + 2);
+    nb = (wmax + kAugBlock - 1) / kAugBlock;
+    tiles = static_cast<uint64_t>(T) * S * nb;
     const uint64_t walks = static_cast<uint64_t>(T) * wmax;
     nodes = 0;
     pairs = align256(walks * (L + 1) * 4);
     nwalks = pairs + align256(walks * 4);
-    cnt = nwalks + align256(static_cast<size_t>(T) * 4);
-    tot = cnt + align256(static_cast<size_t>(bins) * T * S * 4);
+    bk0 = nwalks + align256(static_cast<size_t>(T) * 4);
+    cnt = bk0 + align256(static_cast<size_t>(T) * nb * 8);
+    tot = cnt + align256(static_cast<size_t>(bins) * tiles * 4);
     end = tot + align256(static_cast<size_t>(bins) * 8);
   }
   size_t smem_count(uint32_t L) const { return (static_cast<size_t>(S) * bins + kAugBlock * (L + 1)) * 4; }
-  size_t smem_place(uint32_t L) const { return static_cast<size_t>(S) * (bins + L + 1) * 4; }
+  size_t smem_place(uint32_t L) const {
+    return static_cast<size_t>(kPlaceWarps) * (static_cast<size_t>(S) * bins + L + 1) * 4;
+  }
 };
 constexpr size_t kAugSmemMax = 200 * 1024;
 }  // namespace
@@ -1849,7 +1878,7 @@ constexpr size_t kAugSmemMax = 200 * 1024;
 size_t augment_blocks_scratch_bytes(uint32_t walk_len, uint32_t s, uint32_t shuffle, uint32_t n,
                                     uint32_t segments, uint64_t count) {
   const AugBlocksLayout Lo(walk_len, s, shuffle, n, segments, count);
-  if (shuffle > 1 || Lo.S > 32 || count > 0xFFFFFFFFull || segments == 0 ||
+  if (shuffle > 1 || count > 0xFFFFFFFFull || segments == 0 || Lo.tiles > (1ull << 31) ||
       Lo.smem_count(walk_len) > kAugSmemMax || Lo.smem_place(walk_len) > kAugSmemMax)
     return 0;  // not eligible: the caller augments into a raw pool and buckets it
   return Lo.end;
@@ -1865,7 +1894,8 @@ cudaError_t launch_augment_blocks(const WalkDev& g, uint32_t walk_len, uint32_t 
   const AugBlocksLayout Lo(walk_len, s, shuffle, n, segments, count);
   char* base = static_cast<char*>(scratch);
   WalkCache wc{reinterpret_cast<uint32_t*>(base + Lo.nodes), reinterpret_cast<uint32_t*>(base + Lo.pairs),
-               reinterpret_cast<uint32_t*>(base + Lo.nwalks), Lo.wmax};
+               reinterpret_cast<uint32_t*>(base + Lo.nwalks), reinterpret_cast<uint64_t*>(base + Lo.bk0),
+               Lo.wmax, Lo.nb};
   uint32_t* cnt = reinterpret_cast<uint32_t*>(base + Lo.cnt);
   uint64_t* tot = reinterpret_cast<uint64_t*>(base + Lo.tot);
   BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, n};
@@ -1884,17 +1914,23 @@ cudaError_t launch_augment_blocks(const WalkDev& g, uint32_t walk_len, uint32_t 
     d2 = sm2;
   }
   const unsigned grid = std::min<uint32_t>(segments, static_cast<uint32_t>(num_sms()) * 16);
+  // tiles past a segment's last batch are never written by the count pass
+  cudaError_t e = cudaMemsetAsync(cnt, 0, static_cast<size_t>(Lo.bins) * Lo.tiles * 4, st);
+  if (e != cudaSuccess) return e;
   augment_count_kernel<<<grid, kAugBlock, sm1, st>>>(g, walk_len, s, Lo.S, segments, count,
                                                      static_cast<uint32_t>(seed),
                                                      static_cast<uint32_t>(seed >> 32), b, Lo.bins,
                                                      wc, cnt, err);
-  bucket_scan_bins_kernel<<<Lo.bins, 1024, 0, st>>>(cnt, static_cast<uint64_t>(segments) * Lo.S, tot);
+  bucket_scan_bins_kernel<<<Lo.bins, 1024, 0, st>>>(cnt, Lo.tiles, tot);
   bucket_scan_totals_kernel<<<1, 1024, 0, st>>>(tot, Lo.bins, block_off);
-  augment_place_kernel<<<grid, 32 * Lo.S, sm2, st>>>(walk_len, s, Lo.S, segments, b, Lo.bins, wc,
-                                                      cnt, block_off, out);
+  const uint64_t ntile = static_cast<uint64_t>(segments) * Lo.nb;
+  const unsigned grid2 = static_cast<unsigned>(
+      umin64((ntile + kPlaceWarps - 1) / kPlaceWarps, static_cast<uint64_t>(num_sms()) * 32));
+  augment_place_kernel<<<grid2, 32 * kPlaceWarps, sm2, st>>>(walk_len, s, Lo.S, segments, b,
+                                                             Lo.bins, wc, cnt, block_off, out);
   if (launches) *launches += 4;
   return cudaGetLastError();
-}
+}  // launch_augment_blocks
 
 // ------------------------------------------------ random shuffle (ablation)
 // A keyed bijection of [0, 2^(2h)) by a 4-round Feistel network on h-bit

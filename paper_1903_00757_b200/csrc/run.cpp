@@ -12,7 +12,7 @@
 #include <string>
 #include <thread>
 
-#include "../../include/gv.h"
+#include "engine.hpp"
 
 namespace {
 
@@ -31,8 +31,10 @@ struct HostPool {
 
 extern "C" gv_status gv_run(gv_ctx* c, const gv_augment_cfg* cfg, uint64_t total_samples,
                             gv_run_report* report) {
-  if (!c || !cfg) return GV_ERR_INVALID_ARG;
-  if (cfg->pool_samples == 0 || cfg->threads == 0) return GV_ERR_INVALID_ARG;
+  if (!c || !cfg) return gv::fail(c, GV_ERR_INVALID_ARG, "null context or config");
+  if (!c->loaded) return gv::fail(c, GV_ERR_STATE, "gv_load_edges has not been called");
+  if (cfg->pool_samples == 0 || cfg->threads == 0)
+    return gv::fail(c, GV_ERR_INVALID_ARG, "pool_samples and threads must be > 0");
   const uint64_t P = cfg->pool_samples;
   const uint64_t npools = (total_samples + P - 1) / P;
   gv_run_report rep;
@@ -61,6 +63,8 @@ extern "C" gv_status gv_run(gv_ctx* c, const gv_augment_cfg* cfg, uint64_t total
     for (uint64_t k = 0; k < npools && status == GV_OK; ++k) {
       status = gv_train_episode(c, nullptr);
       if (status == GV_OK && k + 1 < npools) status = produce(k + 1);
+      if (status == GV_OK) status = gv_read_stats(c, &st);  // pool k (pool k+1 already generating)
+      if (status == GV_OK) rep.loss_sum += st.loss_sum;
       if (status == GV_OK && !cfg->collaborate) status = gv_synchronize(c);
     }
     if (status == GV_OK) status = gv_synchronize(c);
@@ -134,6 +138,12 @@ extern "C" gv_status gv_run(gv_ctx* c, const gv_augment_cfg* cfg, uint64_t total
         hp.ready = false;
         cv.notify_all();
       }
+      // pool k-1's loss, read once pool k is staged (the GPU idles only for
+      // the few microseconds between this sync and the next enqueue)
+      if (status == GV_OK && k > 0) {
+        status = gv_read_stats(c, &st);
+        if (status == GV_OK) rep.loss_sum += st.loss_sum;
+      }
       if (status == GV_OK) status = gv_train_episode(c, nullptr);
       if (status != GV_OK) {
         std::lock_guard<std::mutex> lk(mu);
@@ -144,7 +154,8 @@ extern "C" gv_status gv_run(gv_ctx* c, const gv_augment_cfg* cfg, uint64_t total
     }
     producer.join();
     if (status == GV_OK) status = prod_status;
-    if (status == GV_OK) status = gv_synchronize(c);
+    if (status == GV_OK) status = gv_read_stats(c, &st);  // the last pool (synchronizes)
+    if (status == GV_OK) rep.loss_sum += st.loss_sum;
   }
   rep.pools = npools;
   rep.samples = total_samples;

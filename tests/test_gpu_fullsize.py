@@ -94,20 +94,24 @@ def test_collaboration_pipeline_matches_oracle():
     sequential (collaborate = 0) run gives the same bytes."""
     src, dst = synth.chung_lu(5000, 25_000, gamma=2.1, wmax=400.0, seed=7)
     P, pools = 200_000, 3
-    out = {}
+    out, loss = {}, {}
     for collab in (1, 0):
         g = G.GraphVite(5000, 32, 2, 1, 0.025, total_samples=P * pools, ordered=1)
         g.load_edges(src, dst)
         rep = G.gv_run(g.ctx, 40, 2, 4, P, 77, P * pools, collaborate=bool(collab))
         assert rep["pools"] == pools and rep["samples"] == P * pools
         out[collab] = (g.vertex(), g.context())
+        loss[collab] = rep["loss_sum"]
         g.close()
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
     o = O.Trainer(5000, 32, 2, K=1, lr0=0.025, lr_kind=1, total_samples=P * pools)
     o.load_edges(src, dst)
     sampler = O.Sampler(O.Graph(5000, src, dst))
+    lo = 0.0
     for k in range(pools):
-        o.train_pool(sampler.augment(40, 2, 4, P, 77 + k))
+        lo += o.train_pool(sampler.augment(40, 2, 4, P, 77 + k))
+    for collab in (1, 0):  # the run's loss: every pool's, in both modes (SURVEY §8(a) a9)
+        assert abs(loss[collab] - lo) <= 1e-4 * abs(lo), (collab, loss[collab], lo)
     assert_matrix_parity(out[1][0], o.get("vertex"), "vertex")
     assert_matrix_parity(out[1][1], o.get("context"), "context")
 

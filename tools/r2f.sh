@@ -1,0 +1,10 @@
+# round 2, GPU pass f: NEXT-1 sampler-to-blocks v2 (tiles per batch, one warp per segment batch) — parity, pipeline A/B on C2 at n = 1/4/16
+set -x
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q -k "device_blocks or device_pipeline or device_augmentation or collaboration" > gpurun_out/r2f_blocks.log 2>&1; echo blocks=$?
+for pp in 1 4 16; do
+  timeout 600 python bench.py --config C2 --parts-per-rank $pp --steps 5 --warmup 3 --no-extra --no-cpu-baseline --no-e2e > gpurun_out/r2f_c2_n${pp}_blocks.json 2> gpurun_out/r2f_c2_n${pp}_blocks.err; echo c2_${pp}_blocks=$?
+done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/r2f_c2_n4_launches.csv python bench.py --config C2 --parts-per-rank 4 --steps 2 --warmup 1 --no-extra --no-cpu-baseline --no-e2e > gpurun_out/r2f_launches.log 2>&1; echo launches=$?
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r2f_gputest.log 2>&1; echo gputest=$?
+tail -3 gpurun_out/r2f_gputest.log
