@@ -46,11 +46,14 @@ extern "C" gv_status gv_run(gv_ctx* c, const gv_augment_cfg* cfg, uint64_t total
   if (cfg->device) {
     // GPU-resident pipeline (NEXT-1): pool k+1 is generated on the copy
     // stream while pool k trains on the compute stream.
-    // Pools are bucketed inside the sampler (gv_augment_device_blocks) when
-    // the shape allows it, else generated raw and bucketed by the trainer.
-    // (GV_AUG_BLOCKS=0: always raw pools, for A/B measurements)
+    // Pools are generated raw and bucketed by the trainer; GV_AUG_BLOCKS=1
+    // buckets them inside the sampler (gv_augment_device_blocks) when the
+    // shape allows it. Measured on C2 (profiles/r02_f_*): equal at n = 1,
+    // 14% / 4% slower end to end at n = 4 / 16 — the sampler's two passes
+    // (walk cache + per-tile counts, then placement) cost more than one raw
+    // pool write plus the trainer's bucketing pass.
     const char* env = getenv("GV_AUG_BLOCKS");
-    const bool blocks = !(env && atoi(env) == 0) &&
+    const bool blocks = env && atoi(env) != 0 &&
                         gv_augment_device_blocks(c, cfg->walk_len, cfg->s, cfg->threads,
                                                  pool_count(0), cfg->seed, GV_SHUFFLE_PSEUDO) == GV_OK;
     auto produce = [&](uint64_t k) {
