@@ -965,7 +965,11 @@ struct BinCtx {
   const uint32_t* packed;
   const uint64_t* part_off;  // relabelled pool ids (IdMap)
   uint32_t nv, pbits, n;
+  uint32_t pmul;  // floor(n 2^32 / nv): the proportional partition guess by a multiply-high
 };
+__host__ __device__ inline uint32_t part_guess_mul(uint32_t n, uint32_t nv) {
+  return n >= nv ? 0xFFFFFFFFu : static_cast<uint32_t>((static_cast<uint64_t>(n) << 32) / nv);
+}
 
 // {part | local} of a node id: a gather of packed[] for ORIGINAL ids; for
 // RELABELLED ids the partition comes from the offsets (near-equal zig-zag
@@ -974,7 +978,7 @@ struct BinCtx {
 __device__ __forceinline__ uint32_t packed_of(const BinCtx& b, uint32_t id) {
   if (b.part_off == nullptr) return __ldg(b.packed + id);
   if (b.pbits == 0) return id;
-  uint32_t p = static_cast<uint32_t>(static_cast<uint64_t>(id) * b.n / b.nv);
+  uint32_t p = min(__umulhi(id, b.pmul), b.n - 1);  // within one partition of the answer
   while (p > 0 && id < __ldg(b.part_off + p)) --p;
   while (p + 1 < b.n && id >= __ldg(b.part_off + p + 1)) ++p;
   return (p << (32 - b.pbits)) | (id - static_cast<uint32_t>(__ldg(b.part_off + p)));
@@ -1721,7 +1725,7 @@ BucketScratch scratch_parts(void* scratch, const BucketPlan& plan) {
 cudaError_t launch_bucket_count(const uint2* in, uint64_t count, const IdMap& ids,
                                 const BucketPlan& plan, void* scratch, uint64_t* block_off, uint32_t* err, cudaStream_t s,
                                 int* launches) {
-  BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, plan.n};
+  BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, plan.n, part_guess_mul(plan.n, ids.nv)};
   const BucketScratch sc = scratch_parts(scratch, plan);
   if (plan.tiles == 0) {
     cudaMemsetAsync(block_off, 0, (plan.bins + 1) * sizeof(uint64_t), s);
@@ -1742,7 +1746,7 @@ cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const IdMap& id
                                 uint32_t bins_per_out, uint32_t* err, cudaStream_t s,
                                 int* launches) {
   if (plan.tiles == 0) return cudaSuccess;
-  BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, plan.n};
+  BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, plan.n, part_guess_mul(plan.n, ids.nv)};
   const BucketScratch sc = scratch_parts(const_cast<void*>(scratch), plan);
   const unsigned grid =
       static_cast<unsigned>(umin64(plan.tiles, static_cast<uint64_t>(num_sms()) * bucket_ctas()));
@@ -1796,7 +1800,7 @@ cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const IdMap& id
 cudaError_t launch_bucket(const uint2* in, uint64_t count, const IdMap& ids,
                           const BucketPlan& plan, void* scratch, uint2* out,
                           uint64_t* block_off, uint32_t* err, cudaStream_t s, int* launches) {
-  BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, plan.n};
+  BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, plan.n, part_guess_mul(plan.n, ids.nv)};
   const int sms = num_sms();
   if (plan.n == 1) {
     uint64_t grid = umin64((count + 255) / 256, static_cast<uint64_t>(sms) * 8);
@@ -1898,7 +1902,7 @@ cudaError_t launch_augment_blocks(const WalkDev& g, uint32_t walk_len, uint32_t 
                Lo.wmax, Lo.nb};
   uint32_t* cnt = reinterpret_cast<uint32_t*>(base + Lo.cnt);
   uint64_t* tot = reinterpret_cast<uint64_t*>(base + Lo.tot);
-  BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, n};
+  BinCtx b{ids.packed, ids.part_off, ids.nv, ids.pbits, n, part_guess_mul(n, ids.nv)};
   const size_t sm1 = Lo.smem_count(walk_len), sm2 = Lo.smem_place(walk_len);
   static size_t set1[kMaxDev] = {}, set2[kMaxDev] = {};
   size_t& d1 = set1[cur_dev()];

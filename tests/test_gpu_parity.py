@@ -818,3 +818,29 @@ def test_device_blocks_pools_train_like_oracle(c1_graph, n, ids):
     assert_matrix_parity(g.vertex(), o.get("vertex"), "vertex")
     assert_matrix_parity(g.context(), o.get("context"), "context")
     g.close()
+
+
+@pytest.mark.parametrize("n,vr", [(2, 1), (3, 1), (12, 1), (37, 1), (64, 1), (16, 4), (24, 8)])
+def test_relabeled_bucketing_bitexact(n, vr):
+    """a3 on relabelled ids finds each node's partition from the n + 1
+    offsets (a multiply-high guess corrected against them) instead of the
+    gather: the blocks equal the oracle's stable counting sort of the
+    original-id pool, byte for byte, for uneven partition sizes (n not
+    dividing |V|) up to n = 64, with the fused multi-rank exchange."""
+    src, dst = _graph()
+    nv, count = 2000, 150_001
+    pool = synth.edge_pool(src, dst, count, seed=n + 500)
+    g = G.GraphVite(nv, 8, n, 1, 0.025, virtual_ranks=vr, pool_ids=G.GV_IDS_RELABELED)
+    g.load_edges(src, dst)
+    perm, _ = g.partition()
+    g.push(perm[pool])
+    G.gv_prepare_episode(g.ctx)
+    got, boff = G.gv_debug_get_buckets(g.ctx, n, count)
+    o = O.Trainer(nv, 8, n)
+    o.load_edges(src, dst)
+    operm, off = o.partition()
+    exp, eoff = O.bucket(pool, nv, operm, off, n)
+    assert np.array_equal(boff, eoff)
+    assert np.array_equal(got, exp)
+    g.train_episode(stats=False)
+    g.close()
