@@ -1194,7 +1194,7 @@ __global__ void __launch_bounds__(1024) bucket_scan_totals_kernel(const uint64_t
   if (threadIdx.x == blockDim.x - 1) block_off[bins] = run;
 }
 
-// Stable scatter of tiles of kFastTile samples over at most 128 bins. A
+// Stable scatter of tiles of kFastTile samples over at most kOnePassBins bins. A
 // sample's slot = dst_off[bin] + (the tile's offset in the bin, from the
 // scanned per-tile counts) + (count of the same bin in earlier warps of the
 // tile) + (count in earlier chunks of this warp) + (rank among lower lanes of
@@ -1207,8 +1207,9 @@ __global__ void __launch_bounds__(1024) bucket_scan_totals_kernel(const uint64_t
 // possibly a peer GPU's memory mapped over NVLink.
 constexpr uint32_t kFastTile = 2048;
 constexpr int kFastChunks = kFastTile / 256;  // chunks of 32 per warp (8 warps)
+constexpr uint32_t kOnePassBins = 256;        // n <= 16: one pass (bins > 256: two passes)
 
-// MODE 0: one pass over the n x n bins (n <= 11). MODE 1 / 2 are the two passes of a large grid (n >= 12, see pass_bin): the
+// MODE 0: one pass over the n x n bins (n <= 16). MODE 1 / 2 are the two passes of a large grid (n >= 17, see pass_bin): the
 // bins are the n column / row partitions. In MODE 2 the input is sorted by
 // column, so a sample's rank r among this segment's samples of row i is
 // (its row's samples in earlier columns) + (its rank in block (i, j)), and
@@ -1266,11 +1267,12 @@ __global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
       base[q] = (MODE == 2 ? 0ull : dst_off[q]) + cnt[q * tiles + t];
     }
     __syncthreads();
-    if (w == 0) {  // exclusive scan of the tile counts over bins (bins <= 128)
-      uint32_t v[4], sum = 0;
+    if (w == 0) {  // exclusive scan of the tile counts over bins (bins <= kOnePassBins)
+      constexpr int PER = kOnePassBins / 32;
+      uint32_t v[PER], sum = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t q = lane * 4 + k;
+      for (int k = 0; k < PER; ++k) {
+        const uint32_t q = lane * PER + k;
         v[k] = q < bins ? tstart[q] : 0u;
         sum += v[k];
       }
@@ -1282,8 +1284,8 @@ __global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
       }
       uint32_t run = incl - sum;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t q = lane * 4 + k;
+      for (int k = 0; k < PER; ++k) {
+        const uint32_t q = lane * PER + k;
         if (q < bins) tstart[q] = run;
         run += v[k];
       }
@@ -1667,11 +1669,19 @@ BucketPlan make_bucket_plan(uint32_t n, uint64_t count) {
   BucketPlan p;
   p.n = n;
   p.bins = n * n;
-  uint32_t tile = std::max<uint32_t>(2048, 16 * p.bins);
+  // one pass up to GV_BUCKET_ONE_PASS_BINS bins (default and maximum
+  // kOnePassBins; 128 restores the round-1 split, two passes from n = 12)
+  static const uint32_t one_pass = [] {
+    const char* e = getenv("GV_BUCKET_ONE_PASS_BINS");
+    const int v = e ? atoi(e) : static_cast<int>(kOnePassBins);
+    return static_cast<uint32_t>(std::min<int>(std::max<int>(v, 1), static_cast<int>(kOnePassBins)));
+  }();
+  p.two_pass = p.bins > one_pass;
+  // the count phase's tiles are the single pass's tiles (kFastTile)
+  uint32_t tile = p.two_pass ? std::max<uint32_t>(2048, 16 * p.bins) : kFastTile;
   tile = (tile + 255) / 256 * 256;
   p.tile = tile;
   p.tiles = (count + tile - 1) / tile;
-  p.two_pass = p.bins > 128;
   p.tiles2 = (count + kFastTile - 1) / kFastTile;
   return p;
 }
@@ -1759,7 +1769,7 @@ cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const IdMap& id
     kern<<<g, 256, smem, s>>>(src, count, b, bins, tiles, cnt, off, o, per_out, err);
     if (launches) *launches += 1;
   };
-  if (plan.tile == kFastTile && plan.bins <= 128) {
+  if (!plan.two_pass) {
     fast(bucket_scatter_fast_kernel<0>, in, plan.bins, plan.tiles, sc.cnt, dst_off, outs,
          bins_per_out);
     return cudaGetLastError();

@@ -90,7 +90,7 @@ struct BucketPlan {
   uint32_t bins;      // n*n
   uint32_t tile;      // samples per tile
   uint64_t tiles;     // ceil(P / tile)
-  bool two_pass;      // n*n > 128: place by column, then by row (LSD radix, bucket_place)
+  bool two_pass;      // n*n > 256: place by column, then by row (LSD radix, bucket_place)
   uint64_t tiles2;    // ceil(P / 2048): tiles of the two placement passes
 };
 BucketPlan make_bucket_plan(uint32_t n, uint64_t count);
