@@ -432,6 +432,16 @@ constexpr int kRingLPS = GV_RING_LPS;  // lanes per sample: 16 (2 samples / warp
 #ifndef GV_SKIP_HOT_EXPERIMENT
 #define GV_SKIP_HOT_EXPERIMENT 0
 #endif
+// GV_RING_PF=D > 0: one lane per group also issues TMA bulk L2 prefetches
+// (cp.async.bulk.prefetch.L2, one per row) for the sample D iterations past
+// the ring's P: more DRAM reads in flight without more shared memory (the
+// ring's stages bound the samples in flight per SM).
+#ifndef GV_RING_PF
+#define GV_RING_PF 0
+#endif
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(gmem), "r"(bytes) : "memory");
+}
 // Rows staged by TMA bulk copies (cp.async.bulk + one mbarrier per stage)
 // instead of LDGSTS: measured equal on C2 and C4 (profiles/README.md), and
 // compute-sanitizer racecheck cannot verify the async-proxy ordering, so the
@@ -708,6 +718,22 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
     }
     if (i + P < iters) issue(i + P, st_in, chunk);
     if (!kRingTma) cp_commit();
+#if GV_RING_PF > 0
+    {
+      const uint32_t jp = i + P + GV_RING_PF;
+      if (jp < iters && jp / ITER_PER_CHUNK <= chunk + 1) {  // ids loaded (warp-uniform)
+        uint32_t pu, pc[K + 1], phot;
+        ids_of(jp, chunk, pu, pc, phot);
+        if (gl == 0 && G * jp + h < sq.L) {
+          bulk_prefetch_l2(vertex + static_cast<uint64_t>(pu) * stride, static_cast<uint32_t>(dim4 * 16));
+#pragma unroll
+          for (int t = 0; t <= K; ++t)
+            bulk_prefetch_l2(context + static_cast<uint64_t>(pc[t]) * stride,
+                             static_cast<uint32_t>(dim4 * 16));
+        }
+      }
+    }
+#endif
     st = (st + 1 == R) ? 0 : st + 1;
     st_in = (st_in + 1 == R) ? 0 : st_in + 1;
     if ((i % ITER_PER_CHUNK) == ITER_PER_CHUNK - 1) {  // all groups finished the chunk
