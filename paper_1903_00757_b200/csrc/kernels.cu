@@ -432,10 +432,11 @@ constexpr int kRingLPS = GV_RING_LPS;  // lanes per sample: 16 (2 samples / warp
 #ifndef GV_SKIP_HOT_EXPERIMENT
 #define GV_SKIP_HOT_EXPERIMENT 0
 #endif
-// GV_RING_PF=D > 0: one lane per group also issues TMA bulk L2 prefetches
-// (cp.async.bulk.prefetch.L2, one per row) for the sample D iterations past
-// the ring's P: more DRAM reads in flight without more shared memory (the
-// ring's stages bound the samples in flight per SM).
+// GV_RING_PF=D > 0 (build option, measured slower): one lane per group also
+// issues TMA bulk L2 prefetches (cp.async.bulk.prefetch.L2, one per row) for
+// the sample D iterations past the ring's P — more DRAM reads in flight
+// without more shared memory. C5: 1.63 / 1.47 / 1.42e9 at D = 2 / 4 / 5 vs
+// 1.74e9 (profiles/r02_l_*): off.
 #ifndef GV_RING_PF
 #define GV_RING_PF 0
 #endif
@@ -1108,6 +1109,11 @@ __global__ void validate_kernel(const uint2* __restrict__ in, uint64_t count, ui
   }
 }
 
+#ifndef GV_HIST_AGG_MAX_BINS
+#define GV_HIST_AGG_MAX_BINS 32
+#endif
+constexpr uint32_t kHistAggregateMaxBins = GV_HIST_AGG_MAX_BINS;  // warp-aggregated up to here
+
 template <int MODE>
 __global__ void bucket_hist_kernel(const uint2* __restrict__ in, uint64_t count, BinCtx b,
                                    uint32_t bins, uint32_t tile, uint64_t tiles,
@@ -1136,11 +1142,20 @@ __global__ void bucket_hist_kernel(const uint2* __restrict__ in, uint64_t count,
         const uint32_t x = pass_bin<MODE>(b, p[j], loc, err);
         bn[j] = i < end ? x : 0xFFFFFFFFu;
       }
+      if (bins > kHistAggregateMaxBins) {
+        // many bins: lanes rarely share one, so a plain shared atomic per
+        // sample costs fewer instructions than the ballot multisplit (the
+        // kernel is issue-bound, profiles/r02_k_bucket_n16_ncu_summary.txt)
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const uint32_t mask = peer_mask(bn[j], nbits);
-        if (bn[j] != 0xFFFFFFFFu && (__ffs(mask) - 1) == static_cast<int>(threadIdx.x & 31))
-          atomicAdd(&hist[bn[j]], static_cast<uint32_t>(__popc(mask)));
+        for (int j = 0; j < U; ++j)
+          if (bn[j] != 0xFFFFFFFFu) atomicAdd(&hist[bn[j]], 1u);
+      } else {
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const uint32_t mask = peer_mask(bn[j], nbits);
+          if (bn[j] != 0xFFFFFFFFu && (__ffs(mask) - 1) == static_cast<int>(threadIdx.x & 31))
+            atomicAdd(&hist[bn[j]], static_cast<uint32_t>(__popc(mask)));
+        }
       }
     }
     __syncthreads();
