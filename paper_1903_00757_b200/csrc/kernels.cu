@@ -1289,10 +1289,11 @@ __global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
       bn[ch] = k < valid ? x : 0xFFFFFFFFu;
     }
     __syncthreads();
+    uint32_t pm[kFastChunks];  // each chunk's multisplit, kept for the ranking below
 #pragma unroll
     for (int ch = 0; ch < kFastChunks; ++ch) {  // per-warp bin counts
-      const uint32_t mask = peer_mask(bn[ch], nbits);
-      if (bn[ch] != 0xFFFFFFFFu && (__ffs(mask) - 1) == lane) wcnt[w * bins + bn[ch]] += __popc(mask);
+      pm[ch] = peer_mask(bn[ch], nbits);
+      if (bn[ch] != 0xFFFFFFFFu && (__ffs(pm[ch]) - 1) == lane) wcnt[w * bins + bn[ch]] += __popc(pm[ch]);
       __syncwarp();
     }
     __syncthreads();
@@ -1334,7 +1335,7 @@ __global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
     __syncthreads();
 #pragma unroll
     for (int ch = 0; ch < kFastChunks; ++ch) {  // sort the tile by bin (stable)
-      const uint32_t mask = peer_mask(bn[ch], nbits);
+      const uint32_t mask = pm[ch];
       if (bn[ch] != 0xFFFFFFFFu) {
         const uint32_t pos = tstart[bn[ch]] + wcnt[w * bins + bn[ch]] + __popc(mask & lt_mask);
         staged[pos] = lc[ch];
