@@ -1345,6 +1345,14 @@ __global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
       if (bn[ch] != 0xFFFFFFFFu && (__ffs(mask) - 1) == lane) wcnt[w * bins + bn[ch]] += __popc(mask);
       __syncwarp();
     }
+    if (MODE != 2) {
+      // per bin, the address of staged position 0's slot: staged[k] of bin q
+      // goes to dest[q] + 8 k (unsigned wrap-around arithmetic), so the
+      // store loop below does no division and one shared load
+      __syncthreads();
+      for (uint32_t q = threadIdx.x; q < bins; q += blockDim.x)
+        base[q] = reinterpret_cast<uint64_t>(outs[q / bins_per_out]) + (base[q] - tstart[q]) * 8u;
+    }
     __syncthreads();
     for (uint32_t k = threadIdx.x; k < valid; k += blockDim.x) {  // coalesced per bin
       const uint32_t q = sbin[k];
@@ -1354,7 +1362,7 @@ __global__ void __launch_bounds__(256) bucket_scatter_fast_kernel(
         const uint64_t slot = dst_off[q * b.n + (v.y >> sh)] + base[q] + (k - tstart[q]);
         outs[q / bins_per_out][slot] = make_uint2(v.x & mask, v.y & mask);
       } else {
-        outs[q / bins_per_out][base[q] + (k - tstart[q])] = staged[k];
+        *reinterpret_cast<uint2*>(base[q] + 8ull * k) = staged[k];
       }
     }
     __syncthreads();

@@ -23,16 +23,18 @@ def graph(kind, nv, ne):
 
 
 def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000, grow=0, aug=0,
-         kind=0):
+         kind=0, relabeled=0):
     import synth
     from paper_1903_00757_b200 import gv as G
     d = 32 if kind == 0 else 128
     src, dst = graph(kind, nv, ne)
     sizes = [count * (4 ** e if grow else 1) for e in range(pools)]  # grow: receive buffers realloc
     g = G.GraphVite(nv, d, n, 1, 0.025, total_samples=sum(sizes), rank=rank, world_size=world,
-                    ordered=ordered)
+                    ordered=ordered,
+                    pool_ids=G.GV_IDS_RELABELED if relabeled else G.GV_IDS_ORIGINAL)
     G.gv_comm_init(g.ctx, bytes.fromhex(uid_hex))
     g.load_edges(src, dst)
+    perm, _ = g.partition()
     losses = []
     for e in range(pools):
         cnt = sizes[e]
@@ -41,7 +43,8 @@ def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000
             g.augment_device(40, 2, 16, seg, 500 + 1000 * e + rank)
         else:
             pool = synth.edge_pool(src, dst, cnt, seed=(900 if kind == 0 else 200) + e)
-            g.push(pool[cnt * rank // world: cnt * (rank + 1) // world])
+            seg = pool[cnt * rank // world: cnt * (rank + 1) // world]
+            g.push(perm[seg] if relabeled else seg)
         st = g.train_episode()
         losses.append(st["loss_sum"])
         assert st["samples_global"] == cnt, st
@@ -56,4 +59,4 @@ def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000
 if __name__ == "__main__":
     a = sys.argv[1:]
     main(int(a[0]), int(a[1]), a[2], int(a[3]), int(a[4]), int(a[5]), int(a[6]), a[7],
-         *(int(x) for x in a[8:13]))
+         *(int(x) for x in a[8:14]))

@@ -23,14 +23,15 @@ from paper_1903_00757_b200 import gv as G  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(tmp_path, world, n, pools, count, ordered, nv=4000, ne=20_000, grow=0, aug=0, kind=0):
+def _run(tmp_path, world, n, pools, count, ordered, nv=4000, ne=20_000, grow=0, aug=0, kind=0,
+         relabeled=0):
     uid = G.gv_comm_unique_id().hex()
     worker = os.path.join(ROOT, "tests", "_mp_worker.py")
     outs = [str(tmp_path / f"r{r}.npz") for r in range(world)]
     env = dict(os.environ, GV_IPC_TIMEOUT="120")
     procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), uid, str(n), str(pools),
                                str(count), str(ordered), outs[r], str(nv), str(ne), str(grow),
-                               str(aug), str(kind)],
+                               str(aug), str(kind), str(relabeled)],
                               env=env)
              for r in range(world)]
     codes = [p.wait(timeout=600) for p in procs]
@@ -71,6 +72,20 @@ def test_processes_ordered_match_oracle(tmp_path, world, n):
     np.testing.assert_allclose(loss, lo, rtol=1e-4)
 
 
+@pytest.mark.parametrize("world,n", [(2, 4), (4, 16)])
+def test_processes_relabeled_pools_match_oracle(tmp_path, world, n):
+    """gv_options.pool_ids = GV_IDS_RELABELED over the CUDA-IPC transport:
+    each process pushes perm[] of its pool segment; bucketing finds the
+    partitions from the offsets and the fused exchange places the samples —
+    ordered mode equals the serial oracle fed the original-id pools."""
+    pools, count = 2, 200_001
+    V, C, loss = _run(tmp_path, world, n, pools, count, ordered=1, relabeled=1)
+    Vo, Co, lo = _oracle(n, pools, count)
+    assert_matrix_parity(V, Vo, "vertex")
+    assert_matrix_parity(C, Co, "context")
+    np.testing.assert_allclose(loss, lo, rtol=1e-4)
+
+
 def test_processes_growing_pools_match_oracle(tmp_path):
     """Pools of 5e4, 2e5, 8e5 samples: every rank's receive buffer (which its
     peers map and store into) is replaced twice; the retired buffers are
@@ -84,14 +99,15 @@ def test_processes_growing_pools_match_oracle(tmp_path):
     np.testing.assert_allclose(loss, lo, rtol=1e-4)
 
 
-def test_processes_device_augmentation_match_oracle(tmp_path):
+@pytest.mark.parametrize("relabeled", [0, 1])
+def test_processes_device_augmentation_match_oracle(tmp_path, relabeled):
     """Each process augments its own pool segment on its GPU
     (gv_augment_device, walk 40, s = 2, 16 segments, seed per rank and
-    pool); the pool is the concatenation of the ranks' segments in rank
-    order. Ordered mode equals the oracle trained on the oracle's
-    augmentation of the same segments."""
+    pool; original or relabelled ids); the pool is the concatenation of the
+    ranks' segments in rank order. Ordered mode equals the oracle trained on
+    the oracle's augmentation of the same segments."""
     world, n, pools, count = 2, 2, 2, 200_000
-    V, C, loss = _run(tmp_path, world, n, pools, count, ordered=1, aug=1)
+    V, C, loss = _run(tmp_path, world, n, pools, count, ordered=1, aug=1, relabeled=relabeled)
     nv, ne = 4000, 20_000
     src, dst = synth.chung_lu(nv, ne, gamma=2.1, wmax=400.0, seed=11)
     o = O.Trainer(nv, 32, n, K=1, lr0=0.025, lr_kind=1, total_samples=pools * count)
