@@ -1500,11 +1500,12 @@ __global__ void __launch_bounds__(32 * kPlaceWarps) augment_place_kernel(
     uint32_t L, uint32_t s, uint32_t S, uint32_t T, BinCtx b, uint32_t bins, WalkCache wc,
     const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ block_off,
     uint2* __restrict__ out) {
-  extern __shared__ uint32_t sh[];
+  extern __shared__ uint64_t sh64[];
   const uint32_t lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
   const uint32_t W = L + 1;
-  uint32_t* run = sh + wq * (S * bins + W);  // running ranks per (sub-block, bin) of this tile
-  uint32_t* walk = run + S * bins;
+  // per (sub-block, bin) of this warp's tile: the slot of its next pair
+  uint64_t* dst = sh64 + wq * (S * bins + (W + 1) / 2);
+  uint32_t* walk = reinterpret_cast<uint32_t*>(dst + S * bins);
   const uint32_t lt = (1u << lane) - 1u;
   const uint64_t tiles = static_cast<uint64_t>(T) * S * wc.nb;
   // candidates (a, a + d), d = 1..s, by a then d: the full part a <= L - s
@@ -1517,15 +1518,30 @@ __global__ void __launch_bounds__(32 * kPlaceWarps) augment_place_kernel(
     const uint32_t t = static_cast<uint32_t>(tb / wc.nb), batch = static_cast<uint32_t>(tb % wc.nb);
     const uint32_t w0 = batch * kAugBlock, nw = min(wc.nwalks[t], w0 + kAugBlock);
     if (w0 >= nw) continue;  // warp-uniform
-    for (uint32_t q = lane; q < S * bins; q += 32) run[q] = 0;
+    __syncwarp();
+    for (uint32_t q = lane; q < S * bins; q += 32) {
+      const uint32_t j = q / bins, bin = q - j * bins;
+      dst[q] = block_off[bin] + cnt[static_cast<uint64_t>(bin) * tiles + aug_tile(t, j, batch, S, wc.nb)];
+    }
     uint64_t k0 = wc.bk0[static_cast<uint64_t>(t) * wc.nb + batch];
+    // the next walk's nodes and pair count are loaded while this one is placed
+    const uint32_t* src = wc.nodes + (static_cast<uint64_t>(t) * wc.wmax + w0) * W;
+    uint32_t n0 = lane < W ? src[lane] : 0u, n1 = lane + 32 < W ? src[lane + 32] : 0u;
+    uint32_t cw_next = wc.pairs[static_cast<uint64_t>(t) * wc.wmax + w0];
     for (uint32_t w = w0; w < nw; ++w) {
-      const uint64_t widx = static_cast<uint64_t>(t) * wc.wmax + w;
-      const uint32_t* src = wc.nodes + widx * W;
       __syncwarp();
-      for (uint32_t q = lane; q < W; q += 32) walk[q] = src[q];
-      const uint32_t cw = wc.pairs[widx];
+      if (lane < W) walk[lane] = n0;
+      if (lane + 32 < W) walk[lane + 32] = n1;
+      for (uint32_t q = lane + 64; q < W; q += 32) walk[q] = src[q];  // walks longer than 64
+      const uint32_t cw = cw_next;
+      if (w + 1 < nw) {
+        src += W;
+        n0 = lane < W ? src[lane] : 0u;
+        n1 = lane + 32 < W ? src[lane + 32] : 0u;
+        cw_next = wc.pairs[static_cast<uint64_t>(t) * wc.wmax + w + 1];
+      }
       __syncwarp();
+      const uint32_t kmod = static_cast<uint32_t>(k0 % S);
       uint32_t qbase = 0;  // valid pairs of the walk before this round
       for (uint32_t c0 = 0; c0 < ncand && qbase < cw; c0 += 32) {
         const uint32_t ci = c0 + lane;
@@ -1550,19 +1566,13 @@ __global__ void __launch_bounds__(32 * kPlaceWarps) augment_place_kernel(
         const uint32_t q = qbase + __popc(vmask & lt);
         const bool mine = valid && q < cw;
         uint2 loc = make_uint2(0, 0);
-        const uint32_t j = static_cast<uint32_t>((k0 + q) % S);
+        const uint32_t j = (kmod + q) % S;
         const uint32_t bin = mine ? pair_bin(b, walk[a], walk[a + d], loc) : 0;
         const uint32_t key = mine ? j * bins + bin : 0xFFFFFFFFu;
         const uint32_t peers = __match_any_sync(kFull, key);
-        if (mine) {
-          const uint32_t rank = run[key] + __popc(peers & lt);
-          const uint64_t slot = block_off[bin] +
-                                cnt[static_cast<uint64_t>(bin) * tiles + aug_tile(t, j, batch, S, wc.nb)] +
-                                rank;
-          out[slot] = loc;
-        }
+        if (mine) out[dst[key] + __popc(peers & lt)] = loc;
         __syncwarp();
-        if (mine && (peers >> lane) == 1u) run[key] += __popc(peers);  // highest peer lane
+        if (mine && (peers >> lane) == 1u) dst[key] += __popc(peers);  // highest peer lane
         __syncwarp();
         qbase += __popc(vmask);
       }
@@ -1933,7 +1943,7 @@ struct AugBlocksLayout {
   }
   size_t smem_count(uint32_t L) const { return (static_cast<size_t>(S) * bins + kAugBlock * (L + 1)) * 4; }
   size_t smem_place(uint32_t L) const {
-    return static_cast<size_t>(kPlaceWarps) * (static_cast<size_t>(S) * bins + L + 1) * 4;
+    return static_cast<size_t>(kPlaceWarps) * (static_cast<size_t>(S) * bins + (L + 2) / 2) * 8;
   }
 };
 constexpr size_t kAugSmemMax = 200 * 1024;
