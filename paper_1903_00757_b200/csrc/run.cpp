@@ -48,10 +48,10 @@ extern "C" gv_status gv_run(gv_ctx* c, const gv_augment_cfg* cfg, uint64_t total
     // stream while pool k trains on the compute stream.
     // Pools are generated raw and bucketed by the trainer; GV_AUG_BLOCKS=1
     // buckets them inside the sampler (gv_augment_device_blocks) when the
-    // shape allows it. Measured on C2 (profiles/r02_f_*): equal at n = 1,
-    // 14% / 4% slower end to end at n = 4 / 16 — the sampler's two passes
-    // (walk cache + per-tile counts, then placement) cost more than one raw
-    // pool write plus the trainer's bucketing pass.
+    // shape allows it. Measured on C2 (profiles/r02_q_*): 2.52 / 2.13 /
+    // 1.78e9 vs 2.61 / 2.11 / 1.92e9 at n = 1 / 4 / 16 — the sampler's two
+    // passes (walk cache + per-tile counts, then placement) cost about as
+    // much as one raw pool write plus the trainer's bucketing pass.
     const char* env = getenv("GV_AUG_BLOCKS");
     const bool blocks = env && atoi(env) != 0 &&
                         gv_augment_device_blocks(c, cfg->walk_len, cfg->s, cfg->threads,
