@@ -644,8 +644,10 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
     // delta of row r (0 = vertex, 1 + t = target t): red from registers, or
     // (kRingTmaRed) written over the consumed stage row for the bulk reduce
     auto put_delta = [&](int r, uint32_t row, float g, const Row<CPL>& x, uint64_t pol) {
-#if GV_SKIP_HOT_EXPERIMENT
+#if GV_SKIP_HOT_EXPERIMENT == 1
       if ((hot >> r) & 1u) return;
+#elif GV_SKIP_HOT_EXPERIMENT == 2
+      if (((hot >> r) & 1u) && h == 0) return;  // a quarter of the hot rows' deltas (lane group 0)
 #endif
       if (kRingTmaRed || (kRingTmaRedV && r == 0)) {
 #pragma unroll
