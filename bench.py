@@ -68,7 +68,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS),
                     help="C5 (default, Friendster-shaped), C4, C2 (Youtube-shaped)")
-    ap.add_argument("--pool", type=int, default=0, help="samples per rank per pool (0 = config)")
+    ap.add_argument("--pool", "--episode-size", dest="pool", type=int, default=0,
+                    help="samples per rank per pool (0 = config; SPEC's --episode-size)")
     ap.add_argument("--threads", type=int, default=0, help="sampler threads (0 = all cores)")
     ap.add_argument("--cpu-sample", type=int, default=0,
                     help="samples of the bounded oracle run (cpu_baseline; 0 = config)")
@@ -85,6 +86,8 @@ def parse():
                          "pool is trained where it lies) or the caller's original ids")
     ap.add_argument("--host-pool", action="store_true",
                     help="raw pool in pinned host memory (P:284), read over PCIe by bucketing")
+    ap.add_argument("--partitions", type=int, default=0,
+                    help="n, the grid size (SPEC's --partitions): parts_per_rank = n / ranks")
     ap.add_argument("--parts-per-rank", type=int, default=0,
                     help="m = n / ranks partitions per rank (0 = automatic: 1 on one GPU; with "
                          "N > 1 the smallest m whose rotation hides behind m - 1 blocks)")
@@ -531,6 +534,11 @@ def run_ours(args):
         CFG.clear()
         CFG.update(saved)
         gc.collect()
+    if args.partitions:
+        if args.partitions % (world * args.vranks):
+            raise SystemExit(f"--partitions {args.partitions} is not a multiple of the "
+                             f"{world * args.vranks} ranks")
+        args.parts_per_rank = args.partitions // (world * args.vranks)
     m = args.parts_per_rank or auto_parts_per_rank(world, CFG["nv"], CFG["d"])
     n = world * args.vranks * m
     if args.host_partitions:

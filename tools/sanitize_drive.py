@@ -42,4 +42,29 @@ for mode in (G.GV_SHUFFLE_NONE, G.GV_SHUFFLE_RANDOM):
     g.train_episode()
 G.gv_train_explicit(g.ctx, [0, 1], [2, 3], [[4, 5, 6], [7, 7, 2]], 0.1)
 g.close()
+# round 2: relabelled pools (n = 1: range check only, raw and block buffers
+# swap; n = 4 / 16: partition from the offsets), and the sampler writing
+# blocks directly (count pass, tile scans, placement)
+for n, vr in [(1, 1), (4, 1), (16, 4)]:
+    g = G.GraphVite(3000, 128, n, 1, 0.025, total_samples=200_000, virtual_ranks=vr,
+                    pool_ids=G.GV_IDS_RELABELED)
+    g.load_edges(src, dst)
+    perm, _ = g.partition()
+    g.push(perm[pool])
+    g.train_episode()
+    g.push(perm[pool])  # overlaps the first pool's training
+    g.train_episode()
+    g.replay()
+    g.train_episode()
+    assert np.isfinite(g.vertex()).all()
+    g.close()
+for n, ids in [(1, G.GV_IDS_ORIGINAL), (4, G.GV_IDS_RELABELED), (16, G.GV_IDS_ORIGINAL)]:
+    g = G.GraphVite(3000, 64, n, 1, 0.025, pool_ids=ids)
+    g.load_edges(src, dst)
+    g.augment_device_blocks(10, 3, 37, 20_011, 7)
+    g.train_episode()
+    g.augment_device_blocks(10, 3, 37, 20_011, 8, shuffle=G.GV_SHUFFLE_NONE)
+    g.train_episode()
+    assert np.isfinite(g.vertex()).all()
+    g.close()
 print("sanitize drive ok")
