@@ -24,9 +24,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3,-Wall",
           "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
-SOURCES = ["kernels.cu", "engine.cpp", "transport_local.cpp", "transport_ipc.cpp", "outofcore.cpp",
+SOURCES = ["sgd.cu", "bucket.cu", "sampler.cu", "engine.cpp", "transport_local.cpp", "transport_ipc.cpp", "outofcore.cpp",
            "host_graph.cpp", "augment.cpp", "run.cpp", "ipc.cpp", "graph_share.cpp"]
-HEADERS = ["kernels.cuh", "philox.cuh", "host_graph.hpp", "augment.hpp", "ipc.hpp",
+HEADERS = ["kernels.cuh", "device_common.cuh", "bucket_common.cuh", "philox.cuh", "host_graph.hpp", "augment.hpp", "ipc.hpp",
            "graph_share.hpp", "engine.hpp", "transport.hpp"]
 
 
