@@ -379,6 +379,7 @@ gv_status run_steps(gv_ctx* c) {
     a.key1 = key1;
     a.loss_acc = c->opt.compute_loss ? r.loss.p : nullptr;
     a.hot_rows = c->hot_rows;
+    a.chunk_ctr = c->ring_dynamic ? r.chunk_ctr.p : nullptr;
     gv_step_plan plan;
     gv_plan_step(n, c->D, r.d, t, &plan);
     a.desc = r.desc.p + t * m + g0;
@@ -562,6 +563,7 @@ gv_status setup_device(gv_ctx* c) {
     }  // !hp
     CK(r.counts.ensure(n * n + 2));
     CK(r.loss.ensure(1));
+    CK(r.chunk_ctr.ensure(1));
     CK(cudaMallocHost(&r.counts_host, sizeof(uint64_t) * (n * n + 2) * c->D));
     r.ev_start = new_event(true);
     r.ev_bucket = new_event(true);
@@ -706,6 +708,7 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
   // red.global.add write-back (DRAM reads +29%, -19% samples/s; profiles/).
   // GV_HOT_ROWS=<local-id threshold> enables them for experiments.
   if (const char* e = getenv("GV_HOT_ROWS")) c->hot_rows = static_cast<uint32_t>(atol(e));
+  if (const char* e = getenv("GV_RING_DYN")) c->ring_dynamic = atoi(e) != 0;
   c->ranks.resize(c->local);
   for (int v = 0; v < c->local; ++v) c->ranks[v].d = (o.world_size > 1) ? o.rank : v;
   if (o.world_size == 1) c->tr = gv::make_local_transport();  // processes: gv_comm_init
@@ -1245,7 +1248,7 @@ void gv_destroy(gv_ctx* c) {
     cudaFree(r.vertex);
     cudaFree(r.context);
     r.blocks.release(); r.blocks_alt.release(); r.scratch.release();
-    r.counts.release(); r.desc.release(); r.loss.release();
+    r.counts.release(); r.desc.release(); r.loss.release(); r.chunk_ctr.release();
     if (r.counts_host) cudaFreeHost(r.counts_host);
     for (cudaEvent_t e : {r.ev_start, r.ev_bucket, r.ev_exch, r.ev_end,
                           r.ev_exch_sent, r.ev_last_recv})

@@ -79,6 +79,7 @@ struct Rank {
   DevBuf<uint64_t> place_args;  // fused exchange: dst_off[bins] | outs[D] (device pointers)
   BucketPlan plan{};
   DevBuf<double> loss;
+  DevBuf<unsigned long long> chunk_ctr;  // dynamic chunk schedule of the ring kernel
   uint64_t* counts_host = nullptr;  // pinned
   std::vector<uint64_t> local_off;  // this rank's local block_off (bins + 1)
   std::vector<uint64_t> final_off;  // m*n + 1: layout of blocks (g, j) in `blocks`
@@ -125,6 +126,7 @@ struct gv_ctx {
   uint32_t stride = 0;
   int threads = 1;
   int sms = 148;
+  int ring_dynamic = 1;  // GV_RING_DYN: warps claim chunks from a counter (0: static)
   uint32_t hot_rows = 0;  // L2 retention: local ids below this are evict_last
   std::string err;
   std::mutex err_mu;  // push may fail on a producer thread while the trainer runs

@@ -33,6 +33,9 @@ struct SgdArgs {
   double* loss_acc;       // nullable
   uint32_t hot_rows;      // local ids < hot_rows are L2 evict_last, others evict_first
                           // (0 = no cache hints)
+  unsigned long long* chunk_ctr;  // nullable: ring kernel warps claim 32-sample chunks
+                                  // from this counter (zeroed by the launcher) instead
+                                  // of the static chunk w, w + W, ... schedule
 };
 
 struct ExplicitArgs {

@@ -488,23 +488,38 @@ struct RingCfg {
   static constexpr size_t warp_bytes() { return static_cast<size_t>(WARP_ALL) * 16; }
 };
 
-// Sequence of samples processed by one warp: sample p is stream index
-// start + (p >> 5) * stride + (p & 31), p < L.
-struct WarpSeq {
-  uint64_t start, stride;
-  uint32_t L;
+// Chunks of 32 consecutive stream samples handed to the warps of the ring
+// kernel. Static (ctr == nullptr): warp w takes chunks w, w + W, w + 2W, ...
+// Dynamic (a.chunk_ctr): a warp claims its next chunk from a global counter
+// one chunk ahead of use, so the warps' positions in the stream stay within
+// a few chunks of each other however their speeds differ — the samples in
+// flight are a narrow window of the stream, and what the stream's order puts
+// close together (a vertex tile of the pool, gv_options.vertex_tile) is
+// close together in time too, i.e. in L2.
+struct ChunkSrc {
+  uint64_t warp, nw, nchunks, total;
+  unsigned long long* ctr;
+  // global index of this warp's k-th chunk (warp-uniform; lane 0 claims)
+  __device__ __forceinline__ uint64_t claim(uint32_t k, int lane) const {
+    if (ctr == nullptr) return warp + static_cast<uint64_t>(k) * nw;
+    unsigned long long g = 0;
+    if (lane == 0) g = atomicAdd(ctr, 1ull);
+    return __shfl_sync(kFull, g, 0);
+  }
+  // samples of chunk g (0 past the end)
+  __device__ __forceinline__ uint32_t valid(uint64_t g) const {
+    return g < nchunks ? static_cast<uint32_t>(umin64(32, total - (g << 5))) : 0u;
+  }
 };
 
 template <int K>
-__device__ __forceinline__ void seq_chunk_ids(const SgdArgs& a, const WarpSeq& sq, uint32_t chunk,
-                                              int lane, uint32_t& u, uint32_t* c, uint32_t& hot) {
-  const uint32_t p = (chunk << 5) + lane;
+__device__ __forceinline__ void chunk_ids(const SgdArgs& a, const ChunkSrc& cs, uint64_t g,
+                                          int lane, uint32_t& u, uint32_t* c, uint32_t& hot) {
   u = 0;
   hot = 0;
 #pragma unroll
   for (int t = 0; t <= K; ++t) c[t] = 0;
-  if (p < sq.L)
-    sample_ids<K>(a, sq.start + static_cast<uint64_t>(chunk) * sq.stride + lane, u, c, &hot);
+  if (static_cast<uint32_t>(lane) < cs.valid(g)) sample_ids<K>(a, (g << 5) + lane, u, c, &hot);
 }
 
 // sums over the LPS lanes of each group
@@ -545,7 +560,7 @@ __device__ __forceinline__ void red_rowg(float* base, uint32_t row, uint32_t str
 // processes samples g, g+G, g+2G, ... of the warp's sequence; lane gl of a
 // group owns float4 columns gl, gl+LPS, ... of every row.
 template <int K, int LPS>
-__device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, float4* ring,
+__device__ __forceinline__ float run_ring(const SgdArgs& a, const ChunkSrc& cs, float4* ring,
                                           int dim4, int lane, bool want_loss) {
   using RC = RingCfg<K, LPS>;
   constexpr int P = kRingP, R = RC::R, T = RC::T, G = RC::G, CPL = 32 / LPS;
@@ -564,12 +579,20 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
   float* const context = a.context;
   const uint32_t stride = a.stride;
   float loss = 0.f;
-  if (sq.L == 0) return loss;
-  const uint32_t iters = (sq.L + G - 1) / G;  // iteration i: group h runs sample G i + h
-  uint32_t cu, cc[K + 1], nu, nc[K + 1];      // ids of the current / next 32-sample chunk
+  // iteration i runs sample G (i mod ITER_PER_CHUNK) + h of the warp's chunk
+  // i / ITER_PER_CHUNK; the ids of the current and the next chunk are loaded
+  uint32_t cu, cc[K + 1], nu, nc[K + 1];  // ids of the current / next 32-sample chunk
   uint32_t ch_hot, nh_hot;
-  seq_chunk_ids<K>(a, sq, 0, lane, cu, cc, ch_hot);
-  seq_chunk_ids<K>(a, sq, 1, lane, nu, nc, nh_hot);
+  const uint64_t g0 = cs.claim(0, lane), g1 = cs.claim(1, lane);
+  uint32_t vcur = cs.valid(g0), vnxt = cs.valid(g1);  // samples of the current / next chunk
+  if (vcur == 0) return loss;
+  chunk_ids<K>(a, cs, g0, lane, cu, cc, ch_hot);
+  chunk_ids<K>(a, cs, g1, lane, nu, nc, nh_hot);
+  // group h's sample of iteration j (in the current or the next chunk) exists
+  auto valid_it = [&](uint32_t j, uint32_t cur_chunk) {
+    const uint32_t v = (j / ITER_PER_CHUNK) == cur_chunk ? vcur : vnxt;
+    return G * (j % ITER_PER_CHUNK) + h < v;
+  };
 #if GV_SKIP_HOT_EXPERIMENT
   // measurement-only build: the deltas of rows with local id < hot_rows are
   // dropped (wrong training) to measure what hot-row write contention costs
@@ -597,7 +620,7 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
       __syncwarp();
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     }
-    if (G * j + h < sq.L) {
+    if (valid_it(j, cur_chunk)) {
       float4* stage = my + st * RC::STAGE;
       if (kRingTma) {  // one lane per group: expect the bytes, then one bulk copy per row
         if (gl == 0) {
@@ -626,15 +649,16 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
     }
   };
 #pragma unroll
-  for (int j = 0; j < P; ++j) {
-    if (static_cast<uint32_t>(j) < iters) issue(j, j, 0);
+  for (int j = 0; j < P; ++j) {  // P < ITER_PER_CHUNK: all in chunk 0
+    issue(j, j, 0);
     if (!kRingTma) cp_commit();
   }
   int st = 0;     // stage of iteration i
   int st_in = P;  // stage the prefetch of iteration i + P goes to
-  for (uint32_t i = 0; i < iters; ++i) {
+  for (uint32_t i = 0;; ++i) {
     const uint32_t chunk = i / ITER_PER_CHUNK;
-    const bool act = G * i + h < sq.L;
+    if (vcur == 0) break;  // the warp's chunks ran past the end of the stream
+    const bool act = valid_it(i, chunk);
     if (kRingTma) {
       if (act) mbar_wait(bars + st, (phases >> st) & 1u);
       phases ^= 1u << st;
@@ -733,15 +757,15 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
       }
       __syncwarp();
     }
-    if (i + P < iters) issue(i + P, st_in, chunk);
+    issue(i + P, st_in, chunk);  // P < ITER_PER_CHUNK: in this chunk or the next
     if (!kRingTma) cp_commit();
 #if GV_RING_PF > 0
     {
       const uint32_t jp = i + P + GV_RING_PF;
-      if (jp < iters && jp / ITER_PER_CHUNK <= chunk + 1) {  // ids loaded (warp-uniform)
+      if (jp / ITER_PER_CHUNK <= chunk + 1) {  // ids loaded (warp-uniform)
         uint32_t pu, pc[K + 1], phot;
         ids_of(jp, chunk, pu, pc, phot);
-        if (gl == 0 && G * jp + h < sq.L) {
+        if (gl == 0 && valid_it(jp, chunk)) {
           bulk_prefetch_l2(vertex + static_cast<uint64_t>(pu) * stride, static_cast<uint32_t>(dim4 * 16));
 #pragma unroll
           for (int t = 0; t <= K; ++t)
@@ -756,9 +780,12 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const WarpSeq& sq, f
     if ((i % ITER_PER_CHUNK) == ITER_PER_CHUNK - 1) {  // all groups finished the chunk
       cu = nu;
       ch_hot = nh_hot;
+      vcur = vnxt;
 #pragma unroll
       for (int t = 0; t <= K; ++t) cc[t] = nc[t];
-      seq_chunk_ids<K>(a, sq, chunk + 2, lane, nu, nc, nh_hot);
+      const uint64_t g = cs.claim(chunk + 2, lane);
+      vnxt = cs.valid(g);
+      chunk_ids<K>(a, cs, g, lane, nu, nc, nh_hot);
     }
   }
   if (!kRingTma) cp_wait<0>();
@@ -772,16 +799,9 @@ __global__ void __launch_bounds__(256) sgd_ring_kernel(const SgdArgs a, int dim4
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  const uint64_t nchunks = (a.total + 31) >> 5;
-  WarpSeq sq{warp << 5, nw << 5, 0};
-  if (warp < nchunks) {
-    const uint64_t mine = (nchunks - 1 - warp) / nw + 1;
-    uint64_t L = mine << 5;
-    if (warp + (mine - 1) * nw == nchunks - 1) L -= (nchunks << 5) - a.total;
-    sq.L = static_cast<uint32_t>(L);
-  }
+  const ChunkSrc cs{warp, nw, (a.total + 31) >> 5, a.total, a.chunk_ctr};
   float4* ring = smem_f4 + (threadIdx.x >> 5) * RingCfg<K, kRingLPS>::WARP_ALL;
-  const float loss = run_ring<K, kRingLPS>(a, sq, ring, dim4, lane, a.loss_acc != nullptr);
+  const float loss = run_ring<K, kRingLPS>(a, cs, ring, dim4, lane, a.loss_acc != nullptr);
   if (a.loss_acc != nullptr && (lane % kRingLPS) == 0)
     atomicAdd(a.loss_acc, static_cast<double>(loss));
 }
@@ -956,6 +976,10 @@ cudaError_t launch_sgd_hogwild(const SgdArgs& a, int dim, int K, int sms, cudaSt
     const uint64_t chunks = (a.total + 31) / 32;
     uint64_t grid = static_cast<uint64_t>(sms > 0 ? sms : num_sms()) * o;
     grid = std::min<uint64_t>(grid, (chunks + warps - 1) / warps);
+    if (a.chunk_ctr) {
+      const cudaError_t e = cudaMemsetAsync(a.chunk_ctr, 0, sizeof(unsigned long long), s);
+      if (e != cudaSuccess) return e;
+    }
     f<<<static_cast<unsigned>(grid), 32 * warps, smem, s>>>(a, dim / 4);
     return cudaGetLastError();
   }
