@@ -12,7 +12,8 @@
  *
  * Pins (tests/test_oracle_*.py): Philox KATs; exact alias mass identity and
  * chi-square; zig-zag worked example; stable-sort and conservation
- * of bucketing vs numpy; the hand-derived 4-node SGD example and finite
+ * of bucketing vs numpy (and of the vertex-tile order, R-VTILE, vs numpy's
+ * stable sort per block); the hand-derived 4-node SGD example and finite
  * differences of the objective; schedule coverage; AUC vs sklearn.
  * Parity unpinned against the paper itself: the paper prints no intermediate
  * values (SURVEY §8(c) "Against the paper").
@@ -353,6 +354,38 @@ int or_bucket(const uint32_t* pairs, uint64_t count, uint32_t nv,
   return OR_OK;
 }
 
+/* Reading R-VTILE: within each block (i, j) of or_bucket's
+ * output, a stable counting sort by the sample's vertex tile
+ * floor(u_local / 2^tile_bits) — pool order inside a tile.               */
+int or_bucket_tiled(const uint32_t* pairs, uint64_t count, uint32_t nv,
+                    const uint32_t* perm, const uint64_t* part_off, uint32_t n,
+                    uint32_t tile_bits, uint32_t* out, uint64_t* block_off) {
+  if (tile_bits > 31) return OR_ERR_INVALID_ARG;
+  if (tile_bits == 0) return or_bucket(pairs, count, nv, perm, part_off, n, out, block_off);
+  uint32_t* lp = (uint32_t*)malloc((count ? count : 1) * 8);
+  if (!lp) return OR_ERR_NOMEM;
+  int rc = or_bucket(pairs, count, nv, perm, part_off, n, lp, block_off);
+  if (rc) { free(lp); return rc; }
+  for (uint64_t b = 0; b < (uint64_t)n * n; b++) {
+    uint64_t beg = block_off[b], end = block_off[b + 1];
+    uint32_t i = (uint32_t)(b / n);
+    uint64_t rows = part_off[i + 1] - part_off[i];
+    uint64_t tiles = (rows >> tile_bits) + 1;
+    uint64_t* start = (uint64_t*)calloc(tiles + 1, sizeof(uint64_t));
+    if (!start) { free(lp); return OR_ERR_NOMEM; }
+    for (uint64_t q = beg; q < end; q++) start[(lp[2 * q] >> tile_bits) + 1]++;
+    for (uint64_t t = 0; t < tiles; t++) start[t + 1] += start[t];
+    for (uint64_t q = beg; q < end; q++) {
+      uint64_t pos = beg + start[lp[2 * q] >> tile_bits]++;
+      out[2 * pos] = lp[2 * q];
+      out[2 * pos + 1] = lp[2 * q + 1];
+    }
+    free(start);
+  }
+  free(lp);
+  return OR_OK;
+}
+
 /* Alg. 3: cid <- (i + offset) mod num_GPU. */
 uint32_t or_schedule_cid(uint32_t n, uint32_t t, uint32_t i) { return (i + t) % n; }
 
@@ -400,7 +433,14 @@ struct or_trainer {
   float* context;
   uint64_t samples_done;
   uint32_t pool_index;
+  uint32_t vtile_bits;  /* R-VTILE: 0 = blocks in pool order (or_bucket) */
 };
+
+int or_trainer_set_vertex_tile(or_trainer* t, uint32_t tile_bits) {
+  if (tile_bits > 31) return OR_ERR_INVALID_ARG;
+  t->vtile_bits = tile_bits;
+  return OR_OK;
+}
 
 int or_trainer_create(uint32_t nv, uint32_t d, uint32_t n, uint32_t K, float lr0,
                       int lr_kind, double floor_ratio, uint64_t total_samples,
@@ -497,7 +537,7 @@ int or_trainer_train_pool(or_trainer* t, const uint32_t* pairs, uint64_t count,
   uint64_t* block_off = (uint64_t*)malloc(((size_t)n * n + 1) * 8);
   uint32_t* lp = (uint32_t*)malloc((count ? count : 1) * 8);
   if (!block_off || !lp) { free(block_off); free(lp); return OR_ERR_NOMEM; }
-  int rc = or_bucket(pairs, count, t->nv, t->perm, t->part_off, n, lp, block_off);
+  int rc = or_bucket_tiled(pairs, count, t->nv, t->perm, t->part_off, n, t->vtile_bits, lp, block_off);
   if (rc) { free(block_off); free(lp); return rc; }
   uint32_t e = t->pool_index;
   double loss = 0.0;
@@ -531,7 +571,7 @@ int or_trainer_train_pool_hogwild(or_trainer* t, const uint32_t* pairs, uint64_t
   uint64_t* block_off = (uint64_t*)malloc(((size_t)n * n + 1) * 8);
   uint32_t* lp = (uint32_t*)malloc((count ? count : 1) * 8);
   if (!block_off || !lp) { free(block_off); free(lp); return OR_ERR_NOMEM; }
-  int rc = or_bucket(pairs, count, t->nv, t->perm, t->part_off, n, lp, block_off);
+  int rc = or_bucket_tiled(pairs, count, t->nv, t->perm, t->part_off, n, t->vtile_bits, lp, block_off);
   if (rc) { free(block_off); free(lp); return rc; }
   uint32_t e = t->pool_index, d = t->d;
   double loss = 0.0;

@@ -59,6 +59,15 @@ int or_bucket(const uint32_t* pairs, uint64_t count, uint32_t nv,
               const uint32_t* perm, const uint64_t* part_off, uint32_t n,
               uint32_t* out_local_pairs, uint64_t* block_off);
 
+/* or_bucket, then inside each block (i, j) a stable sort of its samples by
+ * vertex tile floor(u_local / 2^tile_bits) (reading R-VTILE: the block's
+ * vertex partition i split into sub-partitions of 2^tile_bits rows, trained
+ * one after the other — P:233's partitions-beyond-GPUs along the vertex
+ * side only). tile_bits = 0: no tile order, identical to or_bucket. */
+int or_bucket_tiled(const uint32_t* pairs, uint64_t count, uint32_t nv,
+                    const uint32_t* perm, const uint64_t* part_off, uint32_t n,
+                    uint32_t tile_bits, uint32_t* out_local_pairs, uint64_t* block_off);
+
 /* Offset schedule of Alg. 3: context partition of vertex partition i
  * at offset step t. */
 uint32_t or_schedule_cid(uint32_t n, uint32_t t, uint32_t i);
@@ -77,6 +86,9 @@ int or_trainer_train_pool(or_trainer* t, const uint32_t* pairs, uint64_t count,
  * each block's samples over `threads` OpenMP threads, lock-free. */
 int or_trainer_train_pool_hogwild(or_trainer* t, const uint32_t* pairs, uint64_t count,
                                   int threads, double* loss_out);
+/* R-VTILE for train_pool / train_pool_hogwild: bucket with or_bucket_tiled
+ * (tile_bits = 0, the default, is or_bucket). */
+int or_trainer_set_vertex_tile(or_trainer* t, uint32_t tile_bits);
 /* Train one block (i,j) given its local pairs, pool index e and lr. */
 int or_trainer_train_block(or_trainer* t, const uint32_t* local_pairs, uint64_t count,
                            uint32_t i, uint32_t j, uint32_t e, float lr, double* loss_out);

@@ -67,7 +67,10 @@ def _declare(L):
         "or_lr": (C.c_float, [C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_uint64]),
         "or_sgd_sample": (C.c_double, [f32p, C.POINTER(f32p), C.c_uint32, C.c_uint32, C.c_float, C.c_float]),
         "or_bucket": (C.c_int, [u32p, C.c_uint64, C.c_uint32, u32p, u64p, C.c_uint32, u32p, u64p]),
+        "or_bucket_tiled": (C.c_int, [u32p, C.c_uint64, C.c_uint32, u32p, u64p, C.c_uint32,
+                                      C.c_uint32, u32p, u64p]),
         "or_schedule_cid": (C.c_uint32, [C.c_uint32, C.c_uint32, C.c_uint32]),
+        "or_trainer_set_vertex_tile": (C.c_int, [vp, C.c_uint32]),
         "or_trainer_create": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float,
                                         C.c_int, C.c_double, C.c_uint64, C.c_uint64, C.c_uint64,
                                         C.c_float, C.POINTER(vp)]),
@@ -179,6 +182,19 @@ def bucket(pairs, nv, perm, part_off, n):
     return out[:2 * cnt].reshape(-1, 2), boff
 
 
+def bucket_tiled(pairs, nv, perm, part_off, n, tile_bits):
+    """or_bucket_tiled: bucketing, then each block in vertex-tile order (R-VTILE)."""
+    pairs = _u32(pairs).reshape(-1)
+    cnt = len(pairs) // 2
+    out = np.zeros(max(2 * cnt, 2), np.uint32)
+    boff = np.zeros(n * n + 1, np.uint64)
+    perm = _u32(perm)
+    part_off = np.ascontiguousarray(part_off, dtype=np.uint64)
+    _check(lib().or_bucket_tiled(_p(pairs, u32p), cnt, nv, _p(perm, u32p), _p(part_off, u64p), n,
+                                 tile_bits, _p(out, u32p), _p(boff, u64p)), "bucket_tiled")
+    return out[:2 * cnt].reshape(-1, 2), boff
+
+
 def schedule_cid(n, t, i):
     return int(lib().or_schedule_cid(n, t, i))
 
@@ -285,12 +301,14 @@ class Trainer:
     """Serial oracle trainer."""
 
     def __init__(self, nv, d, n, K=1, lr0=0.025, lr_kind=1, floor_ratio=1e-4, total_samples=0,
-                 seed=5, init_seed=4, neg_weight=5.0):
+                 seed=5, init_seed=4, neg_weight=5.0, vertex_tile=0):
         self.nv, self.d, self.n, self.K = nv, d, n, K
         h = vp()
         _check(lib().or_trainer_create(nv, d, n, K, lr0, lr_kind, floor_ratio, total_samples, seed,
                                        init_seed, neg_weight, C.byref(h)), "trainer_create")
         self.h = h
+        if vertex_tile:  # R-VTILE: blocks in vertex-tile order (or_bucket_tiled)
+            _check(lib().or_trainer_set_vertex_tile(h, vertex_tile), "set_vertex_tile")
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:

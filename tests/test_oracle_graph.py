@@ -163,3 +163,55 @@ def test_sampler_over_trainer_graph_equals_fresh_graph():
     a = t.sampler().augment(40, 3, 5, 20_000, 11)
     b = O.Sampler(O.Graph(2000, src, dst)).augment(40, 3, 5, 20_000, 11)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("n,count,bits", [(1, 0, 3), (1, 5000, 1), (1, 5000, 4), (2, 4999, 2),
+                                          (3, 12345, 5), (4, 20000, 3), (8, 20000, 9)])
+def test_bucket_tiled_is_stable_sort_by_block_then_tile(n, count, bits):
+    """R-VTILE pinned to a library routine: or_bucket_tiled == numpy's stable
+    lexsort of the relabelled pool by (block = part(u) n + part(v), vertex
+    tile = local(u) >> bits) — pool order inside a (block, tile) — with the
+    block offsets of plain bucketing; each block's multiset is unchanged."""
+    rng = np.random.default_rng(n * 7919 + count + bits)
+    nv = 1000
+    deg = rng.integers(1, 50, nv).astype(np.float64)
+    perm, inv, off = O.zigzag(deg, n)
+    pool = synth.uniform_pool(nv, count, seed=count + 1)
+    out, boff = O.bucket_tiled(pool, nv, perm, off, n, bits)
+    plain, boff0 = O.bucket(pool, nv, perm, off, n)
+    assert np.array_equal(boff, boff0)
+    new = perm[pool] if count else np.zeros((0, 2), np.uint32)
+    part = np.searchsorted(off[1:], new, side="right")
+    local = new - off[part].astype(np.uint32)
+    bins = part[:, 0] * n + part[:, 1]
+    order = np.lexsort((local[:, 0] >> bits, bins))  # last key primary; stable
+    assert np.array_equal(out, local[order])
+    for b in range(n * n):
+        blk, ref = out[boff[b]:boff[b + 1]], plain[boff0[b]:boff0[b + 1]]
+        assert np.all(np.diff(blk[:, 0] >> bits) >= 0)  # tiles ascending inside a block
+        assert sorted(map(tuple, blk)) == sorted(map(tuple, ref))
+
+
+def test_bucket_tiled_special_cases():
+    """tile_bits = 0 is plain bucketing; tiles at least as large as every
+    partition leave each block in pool order (again plain bucketing); one-row
+    tiles sort each block by local vertex id, stably; bits > 31 is rejected."""
+    nv, n = 700, 3
+    rng = np.random.default_rng(5)
+    perm, inv, off = O.zigzag(rng.integers(1, 30, nv).astype(np.float64), n)
+    pool = synth.uniform_pool(nv, 9000, seed=11)
+    plain, b0 = O.bucket(pool, nv, perm, off, n)
+    for bits in (0, 9, 31):  # 2^9 = 512 >= every partition (~234 rows)
+        out, b = O.bucket_tiled(pool, nv, perm, off, n, bits)
+        assert np.array_equal(out, plain) and np.array_equal(b, b0)
+    out, b = O.bucket_tiled(pool, nv, perm, off, n, 1)
+    for q in range(n * n):
+        blk = out[b[q]:b[q + 1]]
+        assert np.all(np.diff(blk[:, 0] >> 1) >= 0)
+    # worked example: one partition, tiles of 2 rows, pool (3,0) (0,1) (2,2) (1,3) (0,0)
+    perm1, _, off1 = O.zigzag([4.0, 3.0, 2.0, 1.0], 1)  # degree-descending: identity order
+    assert list(perm1) == [0, 1, 2, 3]
+    out, b = O.bucket_tiled([[3, 0], [0, 1], [2, 2], [1, 3], [0, 0]], 4, perm1, off1, 1, 1)
+    assert out.tolist() == [[0, 1], [1, 3], [0, 0], [3, 0], [2, 2]]
+    with pytest.raises(O.OracleError):
+        O.bucket_tiled(pool, nv, perm, off, n, 32)

@@ -298,3 +298,35 @@ def test_train_pool_applies_lr_per_offset_step(n):
     assert np.array_equal(ref.get("vertex"), hand.get("vertex"))
     assert np.array_equal(ref.get("context"), hand.get("context"))
     assert not np.array_equal(ref.get("vertex"), per_pool.get("vertex"))
+
+
+@pytest.mark.parametrize("n,bits", [(1, 4), (3, 3)])
+def test_train_pool_vertex_tile_is_tiled_bucketing_then_alg3(n, bits):
+    """R-VTILE in the trainer: train_pool with vertex_tile = bits equals Alg. 3
+    driven by hand over the blocks of O.bucket_tiled (pinned above against
+    numpy's stable sort), bit for bit; and it differs from the untiled
+    trainer (the sample order inside a block matters, so the pin is not
+    vacuous)."""
+    nv = 600
+    src, dst = synth.chung_lu(nv, 3000, gamma=2.1, wmax=60.0, seed=1)
+    pool = synth.edge_pool(src, dst, 20_000, seed=77)
+    mk = lambda vt: O.Trainer(nv, 16, n, K=1, lr0=0.05, lr_kind=1, total_samples=30_000,  # noqa: E731
+                              vertex_tile=vt)
+    tiled, hand, plain = mk(bits), mk(0), mk(0)
+    for t in (tiled, hand, plain):
+        t.load_edges(src, dst)
+    tiled.train_pool(pool)
+    plain.train_pool(pool)
+    perm, off = hand.partition()
+    lp, boff = O.bucket_tiled(pool, nv, perm, off, n, bits)
+    s_before = 0
+    for step in range(n):
+        lr_t = O.lr(1, 0.05, 1e-4, s_before, 30_000)
+        for i in range(n):
+            j = (i + step) % n
+            b = i * n + j
+            hand.train_block(lp[int(boff[b]):int(boff[b + 1])], i, j, 0, lr_t)
+            s_before += int(boff[b + 1] - boff[b])
+    assert np.array_equal(tiled.get("vertex"), hand.get("vertex"))
+    assert np.array_equal(tiled.get("context"), hand.get("context"))
+    assert not np.array_equal(tiled.get("vertex"), plain.get("vertex"))
