@@ -86,6 +86,9 @@ def parse():
                          "pool is trained where it lies) or the caller's original ids")
     ap.add_argument("--host-pool", action="store_true",
                     help="raw pool in pinned host memory (P:284), read over PCIe by bucketing")
+    ap.add_argument("--vertex-tile", type=int, default=14,
+                    help="gv_options.vertex_tile b (reading R-VTILE): blocks in vertex-tile order, "
+                         "tiles of 2^b rows reused from L2 (0 = pool order)")
     ap.add_argument("--partitions", type=int, default=0,
                     help="n, the grid size (SPEC's --partitions): parts_per_rank = n / ranks")
     ap.add_argument("--parts-per-rank", type=int, default=0,
@@ -341,7 +344,8 @@ def measure(args, world, rank, dev, n, *, steps, warmup, e2e=True, pipeline=True
                     device=dev, rank=rank, world_size=world, ordered=1 if args.ordered else 0,
                     virtual_ranks=args.vranks, host_partitions=1 if args.host_partitions else 0,
                     host_pool=1 if args.host_pool else 0,
-                    pool_ids=G.GV_IDS_RELABELED if args.pool_ids == "relabeled" else G.GV_IDS_ORIGINAL)
+                    pool_ids=G.GV_IDS_RELABELED if args.pool_ids == "relabeled" else G.GV_IDS_ORIGINAL,
+                    vertex_tile=args.vertex_tile)
     if world > 1:
         uid = [G.gv_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -354,6 +358,16 @@ def measure(args, world, rank, dev, n, *, steps, warmup, e2e=True, pipeline=True
     t0 = time.perf_counter()
     g.augment(CFG["walk"], CFG["s"], threads, P * args.vranks, 1000 + rank, out=host_pool)
     t_aug = time.perf_counter() - t0
+    # compulsory row traffic of the schedule: with blocks in
+    # vertex-tile order (R-VTILE) at n = 1 a vertex row is read and written
+    # once per pool (its tile's rows stay in L2 while the tile's samples run);
+    # context rows (positive and negatives) are random, once per sample
+    distinct_u = None
+    if args.vertex_tile > 0 and n == 1 and args.pool_ids == "relabeled":
+        seen = np.zeros(CFG["nv"], dtype=np.bool_)
+        seen[host_pool[:, 0].numpy()] = True
+        distinct_u = int(seen.sum())
+        del seen
     g.push(host_pool)
     stream = torch.cuda.ExternalStream(g.stream())
 
@@ -399,6 +413,10 @@ def measure(args, world, rank, dev, n, *, steps, warmup, e2e=True, pipeline=True
     value = samples / (ms / 1e3)
     # roofline of the dominant kernel (block-SGD): algorithmic bytes per launch / launch time
     bps = BYTES_PER_SAMPLE(CFG["d"], CFG["K"])
+    bps_untiled = bps
+    if distinct_u is not None:  # context rows per sample + each vertex row once per pool
+        row = CFG["d"] * 4
+        bps = 2 * (1 + CFG["K"]) * row + 2 * row * distinct_u / (P * args.vranks)
     local_samples = samples // world  # all virtual ranks of this process
     avg_launch_ms = sgd_ms / max(sgd_launches / args.vranks, 1)  # ms_sgd: max over v-ranks
     per_launch_samples = local_samples / max(sgd_launches, 1)
@@ -409,7 +427,8 @@ def measure(args, world, rank, dev, n, *, steps, warmup, e2e=True, pipeline=True
         with open(os.path.join(ROOT, "profiles", "sgd_traffic.json")) as f:
             tr = json.load(f)[CFG["key"]]  # captured for this config (n = 1)
         default_shape = CFG["d"] == CONFIGS[CFG["key"]]["d"] and CFG["K"] == CONFIGS[CFG["key"]]["K"]
-        if n == 1 and world == 1 and default_shape:
+        same_order = tr.get("vertex_tile", 0) == args.vertex_tile  # captured on this order
+        if n == 1 and world == 1 and default_shape and same_order:
             traffic = tr["dram_bytes_per_sample"] * per_launch_samples
     except Exception:
         tr = None
@@ -422,6 +441,12 @@ def measure(args, world, rank, dev, n, *, steps, warmup, e2e=True, pipeline=True
                               "of the shipped kernel, per sample x samples per launch)",
             "kernel": kernel, "peak_source": peak_kind, "sgd_share_of_step": sgd_ms / tot_ms,
             "bytes_per_sample": bps, "launch_ms": avg_launch_ms,
+            "bytes_per_sample_model": ("compulsory rows of the vertex-tile schedule: 2(1+K)d4 "
+                                       "(context rows) + 2d4 x distinct vertex rows / samples "
+                                       f"({distinct_u:,} / {P * args.vranks:,})"
+                                       if distinct_u is not None else
+                                       "2(2+K)d4: every row of a sample read and written once"),
+            "alg_untiled_gbs": per_launch_samples * bps_untiled / (avg_launch_ms / 1e3) / 1e9,
             "samples_per_launch": per_launch_samples}
     if traffic is not None:
         roof["ncu_dram_bytes_per_sample"] = tr["dram_bytes_per_sample"]
@@ -564,6 +589,7 @@ def run_ours(args):
                                   "seed": CFG["seed"], "lr_schedule": "linear, floor 1e-4"},
                        "host_partitions": bool(args.host_partitions),
                        "host_pool": bool(args.host_pool), "pool_ids": args.pool_ids,
+                       "vertex_tile": args.vertex_tile,
                        "mode": "ordered" if args.ordered else "hogwild"},
             "roofline": r["roofline"], "cpu_baseline": cpu, "cpu_hogwild": cpu_hog,
             "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "clocks": r["clocks"],

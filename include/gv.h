@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define GV_ABI_VERSION 3
+#define GV_ABI_VERSION 4
 
 typedef struct gv_ctx gv_ctx; /* opaque; owned by the library */
 
@@ -124,6 +124,19 @@ typedef struct {
                              swap roles ("skipped (identity) at
                              n = 1 with relabeled input"). Same samples, same
                              training; only the ids' encoding differs. */
+  int vertex_tile;        /* b in [0, 31]: sample order inside a block (reading
+                             R-VTILE). 0 (default) = pool order
+                             (R-BUCKET). b > 0: within block (i, j) the samples
+                             are stably sorted by vertex tile u_local >> b — the
+                             block's vertex partition split into sub-partitions
+                             of 2^b relabelled rows trained one after another
+                             (P:233's partitions beyond the GPUs, along the
+                             vertex side), so a tile's vertex rows are reused
+                             from L2 ("leverage the on-chip memory"). The
+                             sort runs after bucketing / the exchange, on the
+                             device, into a second buffer of the rank's block
+                             size (8 B per sample); its time counts in ms_bucket
+                             (one rank) or ms_exchange (D > 1). */
 } gv_options;
 
 #define GV_IDS_ORIGINAL 0

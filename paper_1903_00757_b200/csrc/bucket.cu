@@ -2,6 +2,8 @@
 // histogram + bin-major scans + stable scatter of a pool into the n x n grid
 // (Alg. 3 "Redistribute"; reading R-BUCKET), with the scatter
 // able to store into the owners' receive buffers (a6 fused, peer memory).
+#include <vector>
+
 #include "bucket_common.cuh"
 
 namespace gv {
@@ -125,6 +127,10 @@ __device__ __forceinline__ int bin_bits(uint32_t bins) { return bins <= 1 ? 0 : 
 template <int MODE>
 __device__ __forceinline__ uint32_t pass_bin(const BinCtx& b, uint2 p, uint2& val, uint32_t* err) {
   if (MODE == 0) return bin_of(b, p, val, err);
+  if (MODE == 3) {  // a digit of the vertex tile of a local pair (R-VTILE), value unchanged
+    val = p;
+    return (p.x >> b.tshift) & b.tmask;
+  }
   const uint32_t sh = 32 - b.pbits;
   if (MODE == 2) {
     val = p;
@@ -558,6 +564,93 @@ cudaError_t launch_bucket(const uint2* in, uint64_t count, const IdMap& ids,
   if (e != cudaSuccess) return e;
   return launch_bucket_place(in, count, ids, plan, scratch, block_off, outs,
                              plan.bins, err, s, launches);
+}
+
+// ------------------------------------------------------------ vertex tiles
+namespace {
+int tile_digit_passes(uint64_t rows, uint32_t tile_bits, int* tb_out) {
+  const uint64_t tiles = rows == 0 ? 1 : ((rows - 1) >> tile_bits) + 1;
+  int tb = 0;
+  while ((1ull << tb) < tiles) ++tb;
+  *tb_out = tb;
+  return (tb + 7) / 8;
+}
+struct TileLayout {
+  size_t slots, cnt, tot, off, err, end;
+  TileLayout(uint64_t max_count, uint32_t nseg) {
+    const uint64_t tiles = std::max<uint64_t>((max_count + kFastTile - 1) / kFastTile, 1);
+    slots = 0;
+    cnt = align256(static_cast<size_t>(nseg) * 3 * 8);
+    tot = cnt + align256(static_cast<size_t>(256) * tiles * 4);
+    off = tot + align256(256 * 8);
+    err = off + align256(257 * 8);
+    end = err + 256;
+  }
+};
+}  // namespace
+
+size_t tile_sort_scratch_bytes(uint64_t max_seg_count, uint32_t nseg) {
+  return TileLayout(max_seg_count, nseg).end;
+}
+
+cudaError_t launch_tile_sort(uint2* buf, uint2* tmp, const uint64_t* seg_off,
+                             const uint64_t* seg_rows, uint32_t nseg, uint32_t tile_bits,
+                             void* scratch, cudaStream_t s, int* launches) {
+  if (tile_bits == 0 || nseg == 0) return cudaSuccess;
+  uint64_t max_count = 0;
+  for (uint32_t k = 0; k < nseg; ++k) max_count = std::max(max_count, seg_off[k + 1] - seg_off[k]);
+  const TileLayout L(max_count, nseg);
+  char* base = static_cast<char*>(scratch);
+  uint2** slots = reinterpret_cast<uint2**>(base + L.slots);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(base + L.cnt);
+  uint64_t* tot = reinterpret_cast<uint64_t*>(base + L.tot);
+  uint64_t* off = reinterpret_cast<uint64_t*>(base + L.off);
+  uint32_t* err = reinterpret_cast<uint32_t*>(base + L.err);  // never written by the tile digit
+  // output pointer of every (segment, pass): one host-to-device copy
+  std::vector<uint2*> ptr(static_cast<size_t>(nseg) * 3, nullptr);
+  for (uint32_t k = 0; k < nseg; ++k) {
+    int tb = 0;
+    const int np = tile_digit_passes(seg_rows[k], tile_bits, &tb);
+    for (int q = 0; q < np; ++q) ptr[k * 3 + q] = ((q & 1) ? buf : tmp) + seg_off[k];
+  }
+  cudaError_t e = cudaMemcpyAsync(slots, ptr.data(), ptr.size() * sizeof(uint2*),
+                                  cudaMemcpyHostToDevice, s);  // pageable: staged before return
+  if (e != cudaSuccess) return e;
+  const uint64_t cap = static_cast<uint64_t>(num_sms()) * bucket_ctas();
+  for (uint32_t k = 0; k < nseg; ++k) {
+    const uint64_t count = seg_off[k + 1] - seg_off[k];
+    int tb = 0;
+    const int np = tile_digit_passes(seg_rows[k], tile_bits, &tb);
+    if (count < 2 || tb == 0) continue;  // one tile: the block is already in tile order
+    const uint64_t tiles = (count + kFastTile - 1) / kFastTile;
+    const unsigned grid = static_cast<unsigned>(umin64(tiles, cap));
+    uint32_t shift = tile_bits;
+    for (int q = 0; q < np; ++q) {
+      const int w = (tb - static_cast<int>(shift - tile_bits) + (np - q) - 1) / (np - q);  // balanced
+      const uint32_t bins = 1u << w;
+      BinCtx b{};
+      b.tshift = shift;
+      b.tmask = bins - 1;
+      const uint2* src = ((q & 1) ? tmp : buf) + seg_off[k];
+      bucket_hist_kernel<3><<<grid, 256, bins * 4, s>>>(src, count, b, bins, kFastTile, tiles, cnt,
+                                                        err);
+      bucket_scan_bins_kernel<<<bins, 1024, 0, s>>>(cnt, tiles, tot);
+      bucket_scan_totals_kernel<<<1, 1024, 0, s>>>(tot, bins, off);
+      const size_t smem = static_cast<size_t>(bins) * (8 + 8 * 4 + 4) + kFastTile * (8 + 2);
+      auto kern = bucket_scatter_fast_kernel<3>;
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      kern<<<grid, 256, smem, s>>>(src, count, b, bins, tiles, cnt, off, slots + k * 3 + q, bins, err);
+      if (launches) *launches += 4;
+      shift += w;
+    }
+    if (np & 1) {  // an odd number of passes ends in tmp
+      e = cudaMemcpyAsync(buf + seg_off[k], tmp + seg_off[k], count * sizeof(uint2),
+                          cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_validate(const uint2* in, uint64_t count, uint32_t nv, uint64_t* block_off,

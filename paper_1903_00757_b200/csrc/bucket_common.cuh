@@ -12,6 +12,7 @@ struct BinCtx {
   const uint64_t* part_off;  // relabelled pool ids (IdMap)
   uint32_t nv, pbits, n;
   uint32_t pmul;  // floor(n 2^32 / nv): the proportional partition guess by a multiply-high
+  uint32_t tshift, tmask;  // vertex-tile digit (R-VTILE sort): (u_local >> tshift) & tmask
 };
 __host__ __device__ inline uint32_t part_guess_mul(uint32_t n, uint32_t nv) {
   return n >= nv ? 0xFFFFFFFFu : static_cast<uint32_t>((static_cast<uint64_t>(n) << 32) / nv);

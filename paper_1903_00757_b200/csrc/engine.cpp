@@ -278,6 +278,24 @@ gv_status prepare(gv_ctx* c) {
     if (gv_status st = place_fused(c, bc)) return st;
     if (gv_status st = release_raw()) return st;
   }
+  // R-VTILE: each block of the rank's rows in vertex-tile order (after the
+  // exchange: an owner's block holds every source's samples by then)
+  if (c->opt.vertex_tile > 0)
+    for (auto& r : c->ranks) {
+      const uint32_t nseg = m * n;
+      std::vector<uint64_t> rows(nseg);
+      uint64_t maxseg = 0;
+      for (uint32_t q = 0; q < nseg; ++q) {
+        rows[q] = psize(c, r.d * m + q / n);
+        maxseg = std::max(maxseg, r.final_off[q + 1] - r.final_off[q]);
+      }
+      CK(r.tile_tmp.ensure(r.final_off[nseg]));
+      CK(r.tile_scratch.ensure(gv::tile_sort_scratch_bytes(maxseg, nseg)));
+      CK(gv::launch_tile_sort(r.blocks.p, r.tile_tmp.p, r.final_off.data(), rows.data(), nseg,
+                              static_cast<uint32_t>(c->opt.vertex_tile), r.tile_scratch.p,
+                              r.compute, &r.kernel_launches));
+      if (!fused) CK(cudaEventRecord(r.ev_bucket, r.compute));  // counted in ms_bucket
+    }
   for (auto& r : c->ranks) CK(cudaEventRecord(r.ev_exch, r.compute));
   c->state = PoolState::Prepared;
   return GV_OK;
@@ -380,6 +398,7 @@ gv_status run_steps(gv_ctx* c) {
     a.loss_acc = c->opt.compute_loss ? r.loss.p : nullptr;
     a.hot_rows = c->hot_rows;
     a.chunk_ctr = c->ring_dynamic ? r.chunk_ctr.p : nullptr;
+    a.vertex_keep = (c->vtile_hint && c->opt.vertex_tile > 0) ? 1u : 0u;
     gv_step_plan plan;
     gv_plan_step(n, c->D, r.d, t, &plan);
     a.desc = r.desc.p + t * m + g0;
@@ -680,6 +699,8 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
     return fail(nullptr, GV_ERR_INVALID_ARG, "n_partitions must be a multiple of the rank count");
   if (o.host_partitions && (o.world_size * o.virtual_ranks != 1 || n_partitions < 2))
     return fail(nullptr, GV_ERR_INVALID_ARG, "host_partitions needs one rank and n_partitions >= 2");
+  if (o.vertex_tile < 0 || o.vertex_tile > 31)
+    return fail(nullptr, GV_ERR_INVALID_ARG, "vertex_tile must be in [0, 31]");
   if (o.pool_ids != GV_IDS_ORIGINAL && o.pool_ids != GV_IDS_RELABELED)
     return fail(nullptr, GV_ERR_INVALID_ARG, "pool_ids must be GV_IDS_ORIGINAL or GV_IDS_RELABELED");
   if (alpha && (alpha->kind != GV_LR_CONSTANT && alpha->kind != GV_LR_LINEAR))
@@ -709,6 +730,7 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
   // GV_HOT_ROWS=<local-id threshold> enables them for experiments.
   if (const char* e = getenv("GV_HOT_ROWS")) c->hot_rows = static_cast<uint32_t>(atol(e));
   if (const char* e = getenv("GV_RING_DYN")) c->ring_dynamic = atoi(e) != 0;
+  if (const char* e = getenv("GV_VTILE_HINT")) c->vtile_hint = atoi(e) != 0;
   c->ranks.resize(c->local);
   for (int v = 0; v < c->local; ++v) c->ranks[v].d = (o.world_size > 1) ? o.rank : v;
   if (o.world_size == 1) c->tr = gv::make_local_transport();  // processes: gv_comm_init
@@ -1229,8 +1251,9 @@ gv_status gv_device_bytes(gv_ctx* c, uint64_t* bytes) {
   for (auto& r : c->ranks) {
     b += (r.vrows + r.crows) * c->stride * 4;
     b += r.blocks.bytes_total() + r.blocks_alt.bytes_total() + r.scratch.bytes_total();
-  b += c->aug_scratch.bytes_total();
+    b += r.tile_tmp.bytes_total() + r.tile_scratch.bytes_total();
   }
+  b += c->aug_scratch.bytes_total();
   *bytes = b;
   return GV_OK;
 }
@@ -1248,6 +1271,7 @@ void gv_destroy(gv_ctx* c) {
     cudaFree(r.vertex);
     cudaFree(r.context);
     r.blocks.release(); r.blocks_alt.release(); r.scratch.release();
+    r.tile_tmp.release(); r.tile_scratch.release();
     r.counts.release(); r.desc.release(); r.loss.release(); r.chunk_ctr.release();
     if (r.counts_host) cudaFreeHost(r.counts_host);
     for (cudaEvent_t e : {r.ev_start, r.ev_bucket, r.ev_exch, r.ev_end,

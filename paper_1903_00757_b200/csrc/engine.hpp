@@ -80,6 +80,8 @@ struct Rank {
   BucketPlan plan{};
   DevBuf<double> loss;
   DevBuf<unsigned long long> chunk_ctr;  // dynamic chunk schedule of the ring kernel
+  DevBuf<uint2> tile_tmp;        // R-VTILE: ping-pong buffer of the vertex-tile sort
+  DevBuf<uint8_t> tile_scratch;  // its per-tile counts, offsets, output pointers
   uint64_t* counts_host = nullptr;  // pinned
   std::vector<uint64_t> local_off;  // this rank's local block_off (bins + 1)
   std::vector<uint64_t> final_off;  // m*n + 1: layout of blocks (g, j) in `blocks`
@@ -127,6 +129,7 @@ struct gv_ctx {
   int threads = 1;
   int sms = 148;
   int ring_dynamic = 1;  // GV_RING_DYN: warps claim chunks from a counter (0: static)
+  int vtile_hint = 0;    // GV_VTILE_HINT: L2 hints with vertex tiles (vertex rows kept)
   uint32_t hot_rows = 0;  // L2 retention: local ids below this are evict_last
   std::string err;
   std::mutex err_mu;  // push may fail on a producer thread while the trainer runs

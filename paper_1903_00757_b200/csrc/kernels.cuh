@@ -33,6 +33,8 @@ struct SgdArgs {
   double* loss_acc;       // nullable
   uint32_t hot_rows;      // local ids < hot_rows are L2 evict_last, others evict_first
                           // (0 = no cache hints)
+  uint32_t vertex_keep;   // 1: vertex rows L2 evict_last, context rows evict_first
+                          // (blocks in vertex-tile order, R-VTILE; GV_VTILE_HINT)
   unsigned long long* chunk_ctr;  // nullable: ring kernel warps claim 32-sample chunks
                                   // from this counter (zeroed by the launcher) instead
                                   // of the static chunk w, w + W, ... schedule
@@ -155,5 +157,17 @@ cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const IdMap& id
                                 const BucketPlan& plan, const void* scratch, const uint64_t* dst_off,
                                 uint2* const* outs, uint32_t bins_per_out, uint32_t* err_dev,
                                 cudaStream_t s, int* launches);
+
+// Vertex-tile order (reading R-VTILE, gv_options.vertex_tile): every block
+// segment [seg_off[k], seg_off[k+1]) of buf (local ids; its vertex partition
+// has seg_rows[k] rows) is stably sorted by the tile u_local >> tile_bits —
+// an LSD radix sort over the tile number in passes of <= 256 bins (one pass
+// up to 256 tiles per partition, two up to 65536, three beyond), ping-ponging
+// through tmp (same size as buf); the result is in buf. seg_off / seg_rows
+// are HOST arrays (nseg + 1 / nseg); scratch of tile_sort_scratch_bytes.
+size_t tile_sort_scratch_bytes(uint64_t max_seg_count, uint32_t nseg);
+cudaError_t launch_tile_sort(uint2* buf, uint2* tmp, const uint64_t* seg_off,
+                             const uint64_t* seg_rows, uint32_t nseg, uint32_t tile_bits,
+                             void* scratch, cudaStream_t s, int* launches);
 
 }  // namespace gv

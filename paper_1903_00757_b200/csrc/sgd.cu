@@ -303,6 +303,7 @@ __device__ __forceinline__ void sample_ids(const SgdArgs& a, uint64_t qg, uint32
     if (my_hot) *my_hot |= (nl < a.hot_rows ? 1u : 0u) << (2 + k);
   }
   if (my_hot) *my_hot |= (smp.x < a.hot_rows ? 1u : 0u) | ((smp.y < a.hot_rows ? 1u : 0u) << 1);
+  if (my_hot && a.vertex_keep) *my_hot = 1u;  // vertex row kept in L2, context rows first out
 }
 
 // ------------------------------------------------------------------------
@@ -599,8 +600,9 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const ChunkSrc& cs, 
   // (profiles/r01_hot_row_combining.json)
   const uint64_t pol_hot = policy_evict_normal(), pol_cold = pol_hot;
 #else
-  const uint64_t pol_hot = a.hot_rows ? policy_evict_last() : policy_evict_normal();
-  const uint64_t pol_cold = a.hot_rows ? policy_evict_first() : policy_evict_normal();
+  const bool hints = a.hot_rows != 0 || a.vertex_keep != 0;
+  const uint64_t pol_hot = hints ? policy_evict_last() : policy_evict_normal();
+  const uint64_t pol_cold = hints ? policy_evict_first() : policy_evict_normal();
 #endif
   auto ids_of = [&](uint32_t j, uint32_t cur_chunk, uint32_t& u, uint32_t* c, uint32_t& hot) {
     const uint32_t pp = G * j + h;

@@ -41,7 +41,8 @@ class gv_options(C.Structure):
                 ("device", C.c_int), ("rank", C.c_int), ("world_size", C.c_int),
                 ("virtual_ranks", C.c_int), ("ordered", C.c_int), ("compute_loss", C.c_int),
                 ("host_threads", C.c_int), ("max_pool_samples", C.c_uint64),
-                ("host_partitions", C.c_int), ("host_pool", C.c_int), ("pool_ids", C.c_int)]
+                ("host_partitions", C.c_int), ("host_pool", C.c_int), ("pool_ids", C.c_int),
+                ("vertex_tile", C.c_int)]
 
 
 class gv_episode_stats(C.Structure):

@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_host_only_calls():
     from paper_1903_00757_b200 import gv
-    assert gv.gv_abi_version() == 3
+    assert gv.gv_abi_version() == 4
     o = gv.gv_default_options()
     assert (o.seed, o.init_seed, o.neg_weight, o.world_size, o.virtual_ranks, o.ordered) == (5, 4, 5.0, 1, 1, 0)
     assert gv.lib.gv_status_string(3) == b"GV_ERR_OUT_OF_RANGE"

@@ -67,4 +67,20 @@ for n, ids in [(1, G.GV_IDS_ORIGINAL), (4, G.GV_IDS_RELABELED), (16, G.GV_IDS_OR
     g.train_episode()
     assert np.isfinite(g.vertex()).all()
     g.close()
+# round 2: vertex-tile order (R-VTILE): one pass + copy back (n = 1 swap
+# mode, 2^4-row tiles of 3000 rows: 188 tiles), two passes (2^1 rows), after
+# the fused exchange (n = 4 on 2 virtual ranks); the dynamic chunk schedule
+# of the ring kernel runs in every Hogwild episode above
+for n, vr, bits, ids in [(1, 1, 4, G.GV_IDS_RELABELED), (1, 1, 1, G.GV_IDS_ORIGINAL),
+                         (4, 2, 2, G.GV_IDS_RELABELED)]:
+    g = G.GraphVite(3000, 128, n, 1, 0.025, total_samples=200_000, virtual_ranks=vr,
+                    vertex_tile=bits, pool_ids=ids)
+    g.load_edges(src, dst)
+    perm, _ = g.partition()
+    g.push(perm[pool] if ids == G.GV_IDS_RELABELED else pool)
+    g.train_episode()
+    g.replay()
+    g.train_episode()
+    assert np.isfinite(g.vertex()).all()
+    g.close()
 print("sanitize drive ok")
