@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def main(rank, world, port, n, pools, count, out_path):
+def main(rank, world, port, n, pools, count, out_path, vtile=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
@@ -85,7 +85,10 @@ def main(rank, world, port, n, pools, count, out_path):
                     c_s = allc[s_]
                     base = int(c_s[rank * m * n:i * n + j].sum())
                     parts.append(chunks[s_][base:base + int(c_s[i * n + j])])
-                blocks[(i, j)] = np.concatenate(parts).astype(np.uint32)
+                blk = np.concatenate(parts).astype(np.uint32)
+                if vtile:  # R-VTILE: the owner orders its block by vertex tile after the exchange
+                    blk = blk[np.argsort(blk[:, 0] >> vtile, kind="stable")]
+                blocks[(i, j)] = blk
         glob = allc.sum(0)
         # a7/a8 with the product's plan
         pending = None  # (partition, source) received for the next step
@@ -145,4 +148,5 @@ def main(rank, world, port, n, pools, count, out_path):
 
 if __name__ == "__main__":
     r, w, port, n, pools, count, out = sys.argv[1:8]
-    main(int(r), int(w), int(port), int(n), int(pools), int(count), out)
+    vt = int(sys.argv[8]) if len(sys.argv) > 8 else 0
+    main(int(r), int(w), int(port), int(n), int(pools), int(count), out, vt)

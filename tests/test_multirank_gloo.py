@@ -26,21 +26,25 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("n,pools,count", [(2, 2, 30_000), (4, 2, 40_001), (8, 1, 50_000)])
-def test_two_ranks_match_serial_oracle_bitwise(tmp_path, n, pools, count):
+@pytest.mark.parametrize("n,pools,count,vt", [(2, 2, 30_000, 0), (4, 2, 40_001, 0),
+                                              (8, 1, 50_000, 0), (4, 2, 40_001, 3), (2, 1, 30_000, 6)])
+def test_two_ranks_match_serial_oracle_bitwise(tmp_path, n, pools, count, vt):
+    """vt > 0 (R-VTILE): each owner orders its blocks by vertex tile after the
+    block-row exchange — as the engine does — and the result must equal the
+    serial oracle trainer with the same vertex_tile, bit for bit."""
     world = 2
     port = _free_port()
     out = str(tmp_path / "res.npz")
     worker = os.path.join(ROOT, "tests", "_multirank_worker.py")
     procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), str(port), str(n),
-                               str(pools), str(count), out]) for r in range(world)]
+                               str(pools), str(count), out, str(vt)]) for r in range(world)]
     for p in procs:
         assert p.wait(timeout=300) == 0
     res = np.load(out)
     # serial oracle, same graph, pools and hyper-parameters
     nv, ne, d = 1500, 7000, 16
     src, dst = synth.chung_lu(nv, ne, gamma=2.1, wmax=150.0, seed=1)
-    o = O.Trainer(nv, d, n, K=2, lr0=0.05, lr_kind=1, total_samples=pools * count)
+    o = O.Trainer(nv, d, n, K=2, lr0=0.05, lr_kind=1, total_samples=pools * count, vertex_tile=vt)
     o.load_edges(src, dst)
     for e in range(pools):
         o.train_pool(synth.edge_pool(src, dst, count, seed=500 + e))
