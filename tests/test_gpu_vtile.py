@@ -122,3 +122,25 @@ def test_vertex_tile_ordered_matches_oracle(c1_graph, n, vr, bits, lr_kind):
     assert_matrix_parity(p.vertex(), o.get("vertex"), "vertex")
     assert_matrix_parity(p.context(), o.get("context"), "context")
     p.close()
+
+
+@pytest.mark.parametrize("n,bits", [(2, 5), (4, 3)])
+def test_vertex_tile_out_of_core_matches_oracle(c1_graph, n, bits):
+    """Host-resident partitions (NEXT-3) train the same tiled blocks: ordered
+    mode equals the oracle trainer with the same vertex_tile."""
+    src, dst = c1_graph
+    count = 150_000
+    p = G.GraphVite(C1["nv"], 32, n, 1, 0.025, total_samples=2 * count, ordered=1,
+                    host_partitions=1, vertex_tile=bits)
+    p.load_edges(src, dst)
+    o = O.Trainer(C1["nv"], 32, n, K=1, lr0=0.025, lr_kind=1, total_samples=2 * count,
+                  vertex_tile=bits)
+    o.load_edges(src, dst)
+    for k in range(2):
+        pool = synth.edge_pool(src, dst, count, seed=700 + k)
+        p.push(pool)
+        p.train_episode()
+        o.train_pool(pool)
+    assert_matrix_parity(p.vertex(), o.get("vertex"), "vertex")
+    assert_matrix_parity(p.context(), o.get("context"), "context")
+    p.close()
