@@ -798,15 +798,19 @@ def test_device_blocks_bitexact(c1_graph, n, ids, segments, s, count):
     p.close()
 
 
-@pytest.mark.parametrize("n,ids", [(4, G.GV_IDS_ORIGINAL), (8, G.GV_IDS_RELABELED)])
-def test_device_blocks_pools_train_like_oracle(c1_graph, n, ids):
+@pytest.mark.parametrize("n,ids,vt", [(4, G.GV_IDS_ORIGINAL, 0), (8, G.GV_IDS_RELABELED, 0),
+                                      (1, G.GV_IDS_RELABELED, 5), (4, G.GV_IDS_ORIGINAL, 3)])
+def test_device_blocks_pools_train_like_oracle(c1_graph, n, ids, vt):
     """Pools bucketed in the sampler, pool k+1 generated on the copy stream
     while pool k trains (the two block buffers alternate), ordered kernel:
     equals the oracle trained on its own augmentation of the same seeds; a
-    second sampler call while a pool is pending is refused."""
+    second sampler call while a pool is pending is refused. vt > 0: the
+    sampler's blocks then put in vertex-tile order (R-VTILE) = the oracle
+    with the same vertex_tile."""
     src, dst = c1_graph
     P, pools, segs = 250_000, 3, 96
-    g = G.GraphVite(C1["nv"], 64, n, 1, 0.025, total_samples=P * pools, ordered=1, pool_ids=ids)
+    g = G.GraphVite(C1["nv"], 64, n, 1, 0.025, total_samples=P * pools, ordered=1, pool_ids=ids,
+                    vertex_tile=vt)
     g.load_edges(src, dst)
     g.augment_device_blocks(40, 2, segs, P, 500)
     with pytest.raises(G.GVError):
@@ -815,7 +819,8 @@ def test_device_blocks_pools_train_like_oracle(c1_graph, n, ids):
         g.train_episode(stats=False)
         if k + 1 < pools:
             g.augment_device_blocks(40, 2, segs, P, 501 + k)
-    o = O.Trainer(C1["nv"], 64, n, K=1, lr0=0.025, lr_kind=1, total_samples=P * pools)
+    o = O.Trainer(C1["nv"], 64, n, K=1, lr0=0.025, lr_kind=1, total_samples=P * pools,
+                  vertex_tile=vt)
     o.load_edges(src, dst)
     sampler = O.Sampler(O.Graph(C1["nv"], src, dst))
     for k in range(pools):
