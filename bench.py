@@ -252,7 +252,7 @@ def cpu_baselines(src, dst, threads):
     cpu = {"value": arm.sample / dt, "unit": "samples/s", "cores": 1, "kind": "oracle",
            "sample": arm.describe(dt)}
     cores = os.cpu_count() or 1
-    hog_n = 4 * arm.sample
+    hog_n = max(4 * arm.sample, 100_000_000)  # >= 1e8 samples
     pool = arm.pool(1001, hog_n)
     t0 = time.perf_counter()
     arm.t.train_pool_hogwild(pool, cores)
