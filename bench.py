@@ -60,6 +60,25 @@ CFG = {}
 BYTES_PER_SAMPLE = lambda d, K: 2 * (2 + K) * d * 4  # noqa: E731  (BASELINE.json north_star)
 
 
+def distinct_vertex_rows(u, nv):
+    """Number of distinct vertex ids in a pool's u column."""
+    seen = np.zeros(nv, dtype=np.bool_)
+    seen[u] = True
+    return int(seen.sum())
+
+
+def compulsory_bytes_per_sample(d, K, samples, distinct_u=None):
+    """Row bytes a schedule must move per sample (DESIGN.md §6 / §11).
+    Pool order: every row of a sample read and written once, 2(2+K)d4.
+    Vertex-tile order (R-VTILE, n = 1): the context rows (positive and K
+    negatives) still once per sample, a vertex row once per pool — its tile
+    stays in L2 while the tile's samples run: 2(1+K)d4 + 2d4 distinct/samples."""
+    if distinct_u is None:
+        return BYTES_PER_SAMPLE(d, K)
+    row = d * 4
+    return 2 * (1 + K) * row + 2 * row * distinct_u / samples
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -364,10 +383,7 @@ def measure(args, world, rank, dev, n, *, steps, warmup, e2e=True, pipeline=True
     # context rows (positive and negatives) are random, once per sample
     distinct_u = None
     if args.vertex_tile > 0 and n == 1 and args.pool_ids == "relabeled":
-        seen = np.zeros(CFG["nv"], dtype=np.bool_)
-        seen[host_pool[:, 0].numpy()] = True
-        distinct_u = int(seen.sum())
-        del seen
+        distinct_u = distinct_vertex_rows(host_pool[:, 0].numpy(), CFG["nv"])
     g.push(host_pool)
     stream = torch.cuda.ExternalStream(g.stream())
 
@@ -412,11 +428,8 @@ def measure(args, world, rank, dev, n, *, steps, warmup, e2e=True, pipeline=True
         ms = allmax(ms)
     value = samples / (ms / 1e3)
     # roofline of the dominant kernel (block-SGD): algorithmic bytes per launch / launch time
-    bps = BYTES_PER_SAMPLE(CFG["d"], CFG["K"])
-    bps_untiled = bps
-    if distinct_u is not None:  # context rows per sample + each vertex row once per pool
-        row = CFG["d"] * 4
-        bps = 2 * (1 + CFG["K"]) * row + 2 * row * distinct_u / (P * args.vranks)
+    bps_untiled = BYTES_PER_SAMPLE(CFG["d"], CFG["K"])
+    bps = compulsory_bytes_per_sample(CFG["d"], CFG["K"], P * args.vranks, distinct_u)
     local_samples = samples // world  # all virtual ranks of this process
     avg_launch_ms = sgd_ms / max(sgd_launches / args.vranks, 1)  # ms_sgd: max over v-ranks
     per_launch_samples = local_samples / max(sgd_launches, 1)

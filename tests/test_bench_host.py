@@ -46,3 +46,18 @@ def test_reference_arm_json_line():
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] == 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert "1,138,499 nodes" in line["config"]["workload"]
+
+
+def test_compulsory_bytes_model():
+    """The roofline's bytes per sample: pool order is the
+    per-sample model 2(2+K)d4 (3072 B at d = 128, K = 1, BASELINE.json); in
+    vertex-tile order a pool whose vertex ids are all distinct needs the
+    same bytes (no repeat to serve from L2), one repeated vertex needs only
+    the context rows plus one vertex row per pool."""
+    import numpy as np
+    assert bench.compulsory_bytes_per_sample(128, 1, 1000) == 3072
+    assert bench.compulsory_bytes_per_sample(128, 1, 1000, distinct_u=1000) == 3072
+    assert bench.compulsory_bytes_per_sample(128, 1, 1000, distinct_u=1) == 2048 + 1024 / 1000
+    assert bench.compulsory_bytes_per_sample(96, 3, 10, distinct_u=5) == 2 * 4 * 384 + 768 / 2
+    u = np.array([3, 1, 3, 3, 0, 1], np.int64)
+    assert bench.distinct_vertex_rows(u, 5) == 3
