@@ -575,13 +575,27 @@ int tile_digit_passes(uint64_t rows, uint32_t tile_bits, int* tb_out) {
   *tb_out = tb;
   return (tb + 7) / 8;
 }
+// widest digit (bins) and largest segment of a tile sort: the per-tile
+// count table is sized by them (bins x tiles x 4 B)
+void tile_sort_extent(const uint64_t* seg_off, const uint64_t* seg_rows, uint32_t nseg,
+                      uint32_t tile_bits, uint64_t* max_count, uint32_t* max_bins) {
+  *max_count = 0;
+  *max_bins = 1;
+  for (uint32_t k = 0; k < nseg; ++k) {
+    int tb = 0;
+    const int np = tile_digit_passes(seg_rows[k], tile_bits, &tb);
+    if (np == 0) continue;
+    *max_count = std::max(*max_count, seg_off[k + 1] - seg_off[k]);
+    *max_bins = std::max(*max_bins, 1u << ((tb + np - 1) / np));  // the first (widest) pass
+  }
+}
 struct TileLayout {
   size_t slots, cnt, tot, off, err, end;
-  TileLayout(uint64_t max_count, uint32_t nseg) {
+  TileLayout(uint64_t max_count, uint32_t nseg, uint32_t max_bins) {
     const uint64_t tiles = std::max<uint64_t>((max_count + kFastTile - 1) / kFastTile, 1);
     slots = 0;
     cnt = align256(static_cast<size_t>(nseg) * 3 * 8);
-    tot = cnt + align256(static_cast<size_t>(256) * tiles * 4);
+    tot = cnt + align256(static_cast<size_t>(max_bins) * tiles * 4);
     off = tot + align256(256 * 8);
     err = off + align256(257 * 8);
     end = err + 256;
@@ -589,8 +603,12 @@ struct TileLayout {
 };
 }  // namespace
 
-size_t tile_sort_scratch_bytes(uint64_t max_seg_count, uint32_t nseg) {
-  return TileLayout(max_seg_count, nseg).end;
+size_t tile_sort_scratch_bytes(const uint64_t* seg_off, const uint64_t* seg_rows, uint32_t nseg,
+                               uint32_t tile_bits) {
+  uint64_t max_count = 0;
+  uint32_t max_bins = 1;
+  tile_sort_extent(seg_off, seg_rows, nseg, tile_bits, &max_count, &max_bins);
+  return TileLayout(max_count, nseg, max_bins).end;
 }
 
 cudaError_t launch_tile_sort(uint2* buf, uint2* tmp, const uint64_t* seg_off,
@@ -598,8 +616,9 @@ cudaError_t launch_tile_sort(uint2* buf, uint2* tmp, const uint64_t* seg_off,
                              void* scratch, cudaStream_t s, int* launches) {
   if (tile_bits == 0 || nseg == 0) return cudaSuccess;
   uint64_t max_count = 0;
-  for (uint32_t k = 0; k < nseg; ++k) max_count = std::max(max_count, seg_off[k + 1] - seg_off[k]);
-  const TileLayout L(max_count, nseg);
+  uint32_t max_bins = 1;
+  tile_sort_extent(seg_off, seg_rows, nseg, tile_bits, &max_count, &max_bins);
+  const TileLayout L(max_count, nseg, max_bins);
   char* base = static_cast<char*>(scratch);
   uint2** slots = reinterpret_cast<uint2**>(base + L.slots);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(base + L.cnt);

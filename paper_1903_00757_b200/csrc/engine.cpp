@@ -284,15 +284,12 @@ gv_status prepare(gv_ctx* c) {
     for (auto& r : c->ranks) {
       const uint32_t nseg = m * n;
       std::vector<uint64_t> rows(nseg);
-      uint64_t maxseg = 0;
-      for (uint32_t q = 0; q < nseg; ++q) {
-        rows[q] = psize(c, r.d * m + q / n);
-        maxseg = std::max(maxseg, r.final_off[q + 1] - r.final_off[q]);
-      }
+      for (uint32_t q = 0; q < nseg; ++q) rows[q] = psize(c, r.d * m + q / n);
+      const uint32_t b = static_cast<uint32_t>(c->opt.vertex_tile);
       CK(r.tile_tmp.ensure(r.final_off[nseg]));
-      CK(r.tile_scratch.ensure(gv::tile_sort_scratch_bytes(maxseg, nseg)));
+      CK(r.tile_scratch.ensure(gv::tile_sort_scratch_bytes(r.final_off.data(), rows.data(), nseg, b)));
       CK(gv::launch_tile_sort(r.blocks.p, r.tile_tmp.p, r.final_off.data(), rows.data(), nseg,
-                              static_cast<uint32_t>(c->opt.vertex_tile), r.tile_scratch.p,
+                              b, r.tile_scratch.p,
                               r.compute, &r.kernel_launches));
       if (!fused) CK(cudaEventRecord(r.ev_bucket, r.compute));  // counted in ms_bucket
     }

@@ -165,7 +165,8 @@ cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const IdMap& id
 // up to 256 tiles per partition, two up to 65536, three beyond), ping-ponging
 // through tmp (same size as buf); the result is in buf. seg_off / seg_rows
 // are HOST arrays (nseg + 1 / nseg); scratch of tile_sort_scratch_bytes.
-size_t tile_sort_scratch_bytes(uint64_t max_seg_count, uint32_t nseg);
+size_t tile_sort_scratch_bytes(const uint64_t* seg_off, const uint64_t* seg_rows, uint32_t nseg,
+                               uint32_t tile_bits);
 cudaError_t launch_tile_sort(uint2* buf, uint2* tmp, const uint64_t* seg_off,
                              const uint64_t* seg_rows, uint32_t nseg, uint32_t tile_bits,
                              void* scratch, cudaStream_t s, int* launches);

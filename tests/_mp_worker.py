@@ -23,7 +23,7 @@ def graph(kind, nv, ne):
 
 
 def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000, grow=0, aug=0,
-         kind=0, relabeled=0):
+         kind=0, relabeled=0, vtile=0):
     import synth
     from paper_1903_00757_b200 import gv as G
     d = 32 if kind == 0 else 128
@@ -31,7 +31,8 @@ def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000
     sizes = [count * (4 ** e if grow else 1) for e in range(pools)]  # grow: receive buffers realloc
     g = G.GraphVite(nv, d, n, 1, 0.025, total_samples=sum(sizes), rank=rank, world_size=world,
                     ordered=ordered,
-                    pool_ids=G.GV_IDS_RELABELED if relabeled else G.GV_IDS_ORIGINAL)
+                    pool_ids=G.GV_IDS_RELABELED if relabeled else G.GV_IDS_ORIGINAL,
+                    vertex_tile=vtile)
     G.gv_comm_init(g.ctx, bytes.fromhex(uid_hex))
     g.load_edges(src, dst)
     perm, _ = g.partition()
@@ -59,4 +60,4 @@ def main(rank, world, uid_hex, n, pools, count, ordered, out, nv=4000, ne=20_000
 if __name__ == "__main__":
     a = sys.argv[1:]
     main(int(a[0]), int(a[1]), a[2], int(a[3]), int(a[4]), int(a[5]), int(a[6]), a[7],
-         *(int(x) for x in a[8:14]))
+         *(int(x) for x in a[8:15]))

@@ -24,14 +24,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _run(tmp_path, world, n, pools, count, ordered, nv=4000, ne=20_000, grow=0, aug=0, kind=0,
-         relabeled=0):
+         relabeled=0, vtile=0):
     uid = G.gv_comm_unique_id().hex()
     worker = os.path.join(ROOT, "tests", "_mp_worker.py")
     outs = [str(tmp_path / f"r{r}.npz") for r in range(world)]
     env = dict(os.environ, GV_IPC_TIMEOUT="120")
     procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), uid, str(n), str(pools),
                                str(count), str(ordered), outs[r], str(nv), str(ne), str(grow),
-                               str(aug), str(kind), str(relabeled)],
+                               str(aug), str(kind), str(relabeled), str(vtile)],
                               env=env)
              for r in range(world)]
     codes = [p.wait(timeout=600) for p in procs]
@@ -49,10 +49,10 @@ def _run(tmp_path, world, n, pools, count, ordered, nv=4000, ne=20_000, grow=0, 
     return V, C, np.sum(losses, axis=0)
 
 
-def _oracle(n, pools, count, nv=4000, ne=20_000, grow=0):
+def _oracle(n, pools, count, nv=4000, ne=20_000, grow=0, vtile=0):
     src, dst = synth.chung_lu(nv, ne, gamma=2.1, wmax=400.0, seed=11)
     sizes = [count * (4 ** e if grow else 1) for e in range(pools)]
-    o = O.Trainer(nv, 32, n, K=1, lr0=0.025, lr_kind=1, total_samples=sum(sizes))
+    o = O.Trainer(nv, 32, n, K=1, lr0=0.025, lr_kind=1, total_samples=sum(sizes), vertex_tile=vtile)
     o.load_edges(src, dst)
     loss = [o.train_pool(synth.edge_pool(src, dst, sizes[e], seed=900 + e)) for e in range(pools)]
     return o.get("vertex"), o.get("context"), np.array(loss)
@@ -67,6 +67,20 @@ def test_processes_ordered_match_oracle(tmp_path, world, n):
     pools, count = 2, 200_001
     V, C, loss = _run(tmp_path, world, n, pools, count, ordered=1)
     Vo, Co, lo = _oracle(n, pools, count)
+    assert_matrix_parity(V, Vo, "vertex")
+    assert_matrix_parity(C, Co, "context")
+    np.testing.assert_allclose(loss, lo, rtol=1e-4)
+
+
+@pytest.mark.parametrize("world,n,vt", [(2, 4, 4), (4, 8, 2)])
+def test_processes_vertex_tiles_match_oracle(tmp_path, world, n, vt):
+    """R-VTILE over the CUDA-IPC transport: every owner puts its blocks in
+    vertex-tile order after all sources have stored their samples (the
+    fused exchange); ordered mode equals the serial oracle with the same
+    vertex_tile."""
+    pools, count = 2, 200_001
+    V, C, loss = _run(tmp_path, world, n, pools, count, ordered=1, relabeled=1, vtile=vt)
+    Vo, Co, lo = _oracle(n, pools, count, vtile=vt)
     assert_matrix_parity(V, Vo, "vertex")
     assert_matrix_parity(C, Co, "context")
     np.testing.assert_allclose(loss, lo, rtol=1e-4)
