@@ -144,3 +144,26 @@ def test_vertex_tile_out_of_core_matches_oracle(c1_graph, n, bits):
     assert_matrix_parity(p.vertex(), o.get("vertex"), "vertex")
     assert_matrix_parity(p.context(), o.get("context"), "context")
     p.close()
+
+
+@pytest.mark.parametrize("n,K,d,host_pool", [(1, 3, 64, 1), (4, 2, 128, 0), (2, 5, 256, 1)])
+def test_vertex_tile_shapes_and_host_pool(c1_graph, n, K, d, host_pool):
+    """Tiled blocks with K > 1 negatives, d up to 256 (the full-warp kernel
+    above 128) and the raw pool in pinned host memory: ordered mode
+    equals the oracle trainer with the same vertex_tile."""
+    src, dst = c1_graph
+    count = 120_000
+    p = G.GraphVite(C1["nv"], d, n, K, 0.025, total_samples=count, ordered=1,
+                    neg_weight=5.0 / K, host_pool=host_pool, vertex_tile=4)
+    p.load_edges(src, dst)
+    o = O.Trainer(C1["nv"], d, n, K=K, lr0=0.025, lr_kind=1, total_samples=count,
+                  neg_weight=5.0 / K, vertex_tile=4)
+    o.load_edges(src, dst)
+    pool = synth.edge_pool(src, dst, count, seed=900 + n)
+    p.push(pool)
+    st = p.train_episode()
+    lo = o.train_pool(pool)
+    assert abs(st["loss_sum"] - lo) <= 1e-4 * abs(lo)
+    assert_matrix_parity(p.vertex(), o.get("vertex"), "vertex")
+    assert_matrix_parity(p.context(), o.get("context"), "context")
+    p.close()
