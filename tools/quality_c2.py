@@ -7,7 +7,7 @@ run at full size (fig:episode_size). Writes one JSON line to stdout.
 (It is also the run that exposed the divergence of the withdrawn hot-row
 combining, profiles/README.md.)
 
-    python tools/quality_c2.py [pools] [dcsbm|chung_lu]
+    python tools/quality_c2.py [pools] [dcsbm|chung_lu] [vertex_tile]
 """
 import json
 import os
@@ -38,15 +38,16 @@ def auc(V, pos, neg):
 def main():
     pools = int(sys.argv[1]) if len(sys.argv) > 1 else 5
     kind = sys.argv[2] if len(sys.argv) > 2 else "dcsbm"
+    vt = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # R-VTILE: blocks in vertex-tile order
     if kind == "dcsbm":  # C2's size and degree shape with 200 communities (mu = 0.1)
         src, dst, _ = synth.dcsbm(NV, NE, gamma=2.1, wmax=3e4, c=200, mu=0.1, seed=1)
     else:  # the bench graph: no community structure, so link prediction is near chance
         src, dst = synth.chung_lu(NV, NE, gamma=2.1, wmax=3e4, seed=1)
     tr_s, tr_d, pos, neg = synth.linkpred_split(src, dst, NV, holdout=0.01, seed=6)
     out = {"workload": f"C2-sized {kind} graph, 1% held out, walk 40, s=5, GPU augmentation",
-           "pools": pools, "samples": pools * POOL, "runs": {}}
+           "pools": pools, "samples": pools * POOL, "vertex_tile": vt, "runs": {}}
     for name, n in [("n1", 1), ("n4", 4), ("n8", 8)]:
-        g = G.GraphVite(NV, 128, n, 1, 0.025, total_samples=pools * POOL, ordered=0)
+        g = G.GraphVite(NV, 128, n, 1, 0.025, total_samples=pools * POOL, ordered=0, vertex_tile=vt)
         g.load_edges(tr_s, tr_d)
         t0 = time.time()
         st = None
