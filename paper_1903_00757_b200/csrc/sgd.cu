@@ -688,6 +688,9 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const ChunkSrc& cs, 
       if ((hot >> r) & 1u) return;
 #elif GV_SKIP_HOT_EXPERIMENT == 2
       if (((hot >> r) & 1u) && h == 0) return;  // a quarter of the hot rows' deltas (lane group 0)
+#elif GV_SKIP_HOT_EXPERIMENT == 3
+      if (((hot >> r) & 1u) && h != 0) return;  // three quarters: each hot address sees 1/4 of its
+                                                // deltas (the load a 4-way sharded row would see)
 #endif
       if (kRingTmaRed || (kRingTmaRedV && r == 0)) {
 #pragma unroll
