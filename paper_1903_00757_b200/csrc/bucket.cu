@@ -568,6 +568,8 @@ cudaError_t launch_bucket(const uint2* in, uint64_t count, const IdMap& ids,
 
 // ------------------------------------------------------------ vertex tiles
 namespace {
+// passes of <= 8 bits over a tile number below 2^32
+constexpr int kTilePassMax = 4;
 int tile_digit_passes(uint64_t rows, uint32_t tile_bits, int* tb_out) {
   const uint64_t tiles = rows == 0 ? 1 : ((rows - 1) >> tile_bits) + 1;
   int tb = 0;
@@ -594,7 +596,7 @@ struct TileLayout {
   TileLayout(uint64_t max_count, uint32_t nseg, uint32_t max_bins) {
     const uint64_t tiles = std::max<uint64_t>((max_count + kFastTile - 1) / kFastTile, 1);
     slots = 0;
-    cnt = align256(static_cast<size_t>(nseg) * 3 * 8);
+    cnt = align256(static_cast<size_t>(nseg) * kTilePassMax * 8);
     tot = cnt + align256(static_cast<size_t>(max_bins) * tiles * 4);
     off = tot + align256(256 * 8);
     err = off + align256(257 * 8);
@@ -626,11 +628,11 @@ cudaError_t launch_tile_sort(uint2* buf, uint2* tmp, const uint64_t* seg_off,
   uint64_t* off = reinterpret_cast<uint64_t*>(base + L.off);
   uint32_t* err = reinterpret_cast<uint32_t*>(base + L.err);  // never written by the tile digit
   // output pointer of every (segment, pass): one host-to-device copy
-  std::vector<uint2*> ptr(static_cast<size_t>(nseg) * 3, nullptr);
+  std::vector<uint2*> ptr(static_cast<size_t>(nseg) * kTilePassMax, nullptr);
   for (uint32_t k = 0; k < nseg; ++k) {
     int tb = 0;
     const int np = tile_digit_passes(seg_rows[k], tile_bits, &tb);
-    for (int q = 0; q < np; ++q) ptr[k * 3 + q] = ((q & 1) ? buf : tmp) + seg_off[k];
+    for (int q = 0; q < np; ++q) ptr[k * kTilePassMax + q] = ((q & 1) ? buf : tmp) + seg_off[k];
   }
   cudaError_t e = cudaMemcpyAsync(slots, ptr.data(), ptr.size() * sizeof(uint2*),
                                   cudaMemcpyHostToDevice, s);  // pageable: staged before return
@@ -659,7 +661,7 @@ cudaError_t launch_tile_sort(uint2* buf, uint2* tmp, const uint64_t* seg_off,
       auto kern = bucket_scatter_fast_kernel<3>;
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      kern<<<grid, 256, smem, s>>>(src, count, b, bins, tiles, cnt, off, slots + k * 3 + q, bins, err);
+      kern<<<grid, 256, smem, s>>>(src, count, b, bins, tiles, cnt, off, slots + k * kTilePassMax + q, bins, err);
       if (launches) *launches += 4;
       shift += w;
     }

@@ -162,7 +162,7 @@ cudaError_t launch_bucket_place(const uint2* in, uint64_t count, const IdMap& id
 // segment [seg_off[k], seg_off[k+1]) of buf (local ids; its vertex partition
 // has seg_rows[k] rows) is stably sorted by the tile u_local >> tile_bits —
 // an LSD radix sort over the tile number in passes of <= 256 bins (one pass
-// up to 256 tiles per partition, two up to 65536, three beyond), ping-ponging
+// up to 256 tiles per partition, two up to 65536, three up to 2^24, four beyond), ping-ponging
 // through tmp (same size as buf); the result is in buf. seg_off / seg_rows
 // are HOST arrays (nseg + 1 / nseg); scratch of tile_sort_scratch_bytes.
 size_t tile_sort_scratch_bytes(const uint64_t* seg_off, const uint64_t* seg_rows, uint32_t nseg,
