@@ -148,6 +148,7 @@ def set_config(name, args=None):
             CFG["pool"] = args.pool
         if args.cpu_sample:
             CFG["cpu_sample"] = args.cpu_sample
+        CFG["vertex_tile"] = args.vertex_tile
     if CFG["neg_weight"] is None:
         CFG["neg_weight"] = 5.0 / CFG["K"]
 
@@ -157,7 +158,9 @@ def workload_name(world=1, n=1):
             f"{CFG['ne']:,} edges (chung-lu gamma {CFG['gamma']}, wmax {CFG['wmax']:g}"
             f"{', edge draws, duplicates merged by ingest' if CFG['gen'] == 'draws' else ''}), "
             f"d={CFG['d']}, K={CFG['K']}, walk {CFG['walk']}, s={CFG['s']}, "
-            f"pool {CFG['pool']:,} samples per rank, n={n}, {world} rank(s)")
+            f"pool {CFG['pool']:,} samples per rank, n={n}, {world} rank(s)"
+            + (f", blocks in vertex-tile order (2^{CFG['vertex_tile']} rows, R-VTILE)"
+               if CFG.get("vertex_tile") else ""))
 
 
 def peaks():
@@ -240,7 +243,8 @@ class OracleArm:
         t0 = time.perf_counter()
         self.t = O.Trainer(CFG["nv"], CFG["d"], 1, K=CFG["K"], lr0=CFG["lr"], lr_kind=1,
                            neg_weight=CFG["neg_weight"], seed=CFG["seed"],
-                           total_samples=64 * sample)
+                           total_samples=64 * sample,
+                           vertex_tile=CFG.get("vertex_tile", 0))  # the arm's sample order
         self.t.load_edges(src, dst)
         self.sampler = self.t.sampler()
         self.setup_s = time.perf_counter() - t0
@@ -257,7 +261,8 @@ class OracleArm:
     def describe(self, dt):
         return (f"{self.sample:,} samples per step (a pool of the {CFG['key']} {CFG['name']} graph "
                 f"augmented by the oracle's sampler: walk {CFG['walk']}, s={CFG['s']}, "
-                f"{self.threads} segments), d={CFG['d']}, n=1, serial C oracle, {dt:.2f} s per "
+                f"{self.threads} segments), d={CFG['d']}, n=1, vertex_tile={CFG.get('vertex_tile', 0)}, "
+                f"serial C oracle, {dt:.2f} s per "
                 f"step; oracle setup (ingest, partition, alias, init, walk tables) "
                 f"{self.setup_s:.0f} s, untimed")
 
