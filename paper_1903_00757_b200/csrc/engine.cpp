@@ -395,7 +395,7 @@ gv_status run_steps(gv_ctx* c) {
     a.loss_acc = c->opt.compute_loss ? r.loss.p : nullptr;
     a.hot_rows = c->hot_rows;
     a.chunk_ctr = c->ring_dynamic ? r.chunk_ctr.p : nullptr;
-    a.vertex_keep = (c->vtile_hint && c->opt.vertex_tile > 0) ? 1u : 0u;
+    a.vertex_keep = (c->vtile_hint && c->opt.vertex_tile > 0) ? static_cast<uint32_t>(c->vtile_hint) : 0u;
     gv_step_plan plan;
     gv_plan_step(n, c->D, r.d, t, &plan);
     a.desc = r.desc.p + t * m + g0;
@@ -727,7 +727,7 @@ gv_status gv_create(uint32_t num_nodes, uint32_t dim, uint32_t n_partitions,
   // GV_HOT_ROWS=<local-id threshold> enables them for experiments.
   if (const char* e = getenv("GV_HOT_ROWS")) c->hot_rows = static_cast<uint32_t>(atol(e));
   if (const char* e = getenv("GV_RING_DYN")) c->ring_dynamic = atoi(e) != 0;
-  if (const char* e = getenv("GV_VTILE_HINT")) c->vtile_hint = atoi(e) != 0;
+  if (const char* e = getenv("GV_VTILE_HINT")) c->vtile_hint = atoi(e);  // 1: vertex kept, context first out; 2: vertex kept
   c->ranks.resize(c->local);
   for (int v = 0; v < c->local; ++v) c->ranks[v].d = (o.world_size > 1) ? o.rank : v;
   if (o.world_size == 1) c->tr = gv::make_local_transport();  // processes: gv_comm_init

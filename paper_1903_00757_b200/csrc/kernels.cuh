@@ -33,8 +33,9 @@ struct SgdArgs {
   double* loss_acc;       // nullable
   uint32_t hot_rows;      // local ids < hot_rows are L2 evict_last, others evict_first
                           // (0 = no cache hints)
-  uint32_t vertex_keep;   // 1: vertex rows L2 evict_last, context rows evict_first
-                          // (blocks in vertex-tile order, R-VTILE; GV_VTILE_HINT)
+  uint32_t vertex_keep;   // 1: vertex rows L2 evict_last, context rows evict_first;
+                          // 2: vertex rows evict_last only (blocks in vertex-tile
+                          // order, R-VTILE; GV_VTILE_HINT, measurement)
   unsigned long long* chunk_ctr;  // nullable: ring kernel warps claim 32-sample chunks
                                   // from this counter (zeroed by the launcher) instead
                                   // of the static chunk w, w + W, ... schedule

@@ -602,7 +602,9 @@ __device__ __forceinline__ float run_ring(const SgdArgs& a, const ChunkSrc& cs, 
 #else
   const bool hints = a.hot_rows != 0 || a.vertex_keep != 0;
   const uint64_t pol_hot = hints ? policy_evict_last() : policy_evict_normal();
-  const uint64_t pol_cold = hints ? policy_evict_first() : policy_evict_normal();
+  // vertex_keep 2: only the vertex rows get a hint (evict_last), context rows none
+  const uint64_t pol_cold =
+      (hints && a.vertex_keep != 2) ? policy_evict_first() : policy_evict_normal();
 #endif
   auto ids_of = [&](uint32_t j, uint32_t cur_chunk, uint32_t& u, uint32_t* c, uint32_t& hot) {
     const uint32_t pp = G * j + h;
